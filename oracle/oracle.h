@@ -1,0 +1,102 @@
+/* oracle.h — plain, slow, obviously-correct CPU oracle of the inpainting hot path.
+ *
+ * TEST INFRASTRUCTURE ONLY.  Only tests/, __graft_entry__.smoke() and bench.py's
+ * cpu_baseline / --impl reference legs may load this library.  The product path
+ * (paper_1503_05528_b200/) never links, imports or calls it, and shares no code
+ * with it (no common headers, kernels, helpers or constant tables).
+ *
+ * Paper: Newson et al., "Video inpainting of complex scenes", arXiv 1503.05528.
+ * Citations "P:n" are PAPER.md line numbers; "R<k>" are the readings listed in
+ * DESIGN.md §2 (the paper's silent/garbled points and the reading adopted).
+ *
+ * Data model (independent of the GPU layout):
+ *   colour   u8  [T][H][W][3]        (u : Omega -> R^3)
+ *   texture  u8  [T][H][W][2]        half-grey-level units, T_q = round(2T)  (Eq. 8; R24)
+ *   occ      u8  [T][H][W]           1 = in H
+ *   src/tgt  u8  [T][H][W]           membership of D~ / H~
+ *   NNF      over the sorted target list: dx,dy,dt (int32), D (u32), n (u8)   (phi)
+ * Linear index p = (t*H + y)*W + x; t-major order is the lexicographic order (R28).
+ *
+ * Parity status: every function here is pinned by a `-m "not gpu"` test except
+ * where its comment says "parity unpinned".
+ */
+#ifndef VINP_ORACLE_H
+#define VINP_ORACLE_H
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+typedef struct {
+  int W, H, T;
+  uint8_t* rgb;      /* [N][3] */
+  uint8_t* tex;      /* [N][2] */
+  uint8_t* occ;      /* [N]    */
+  uint8_t* src;      /* [N] D~ */
+  uint8_t* tgt;      /* [N] H~ */
+  uint8_t* layer;    /* [N] onion layer (coarsest level) or NULL */
+  int32_t* slot;     /* [N] voxel -> target slot or -1 */
+  int32_t* targets; int32_t n_targets;
+  int32_t* holes;   int32_t n_holes;
+  int32_t* sources; int32_t n_sources;
+} or_level;
+
+typedef struct {
+  int32_t *dx, *dy, *dt;
+  uint32_t* D;
+  uint8_t* n;
+} or_nnf;
+
+enum { OR_WEIGHTED = 0, OR_UNWEIGHTED = 1, OR_BEST_PATCH = 2 };
+
+void or_philox4x32_10(const uint32_t ctr[4], uint64_t seed, uint32_t out[4]);
+
+void or_pyramid_down(const uint8_t* rgb, const uint8_t* occ, int W, int H, int T,
+                     uint8_t* rgb_c, uint8_t* occ_c);
+void or_texture(const uint8_t* rgb, const uint8_t* occ, int W, int H, int T, int h, uint8_t* tex);
+void or_texture_decimate(const uint8_t* tex1, int W1, int H1, int T, int level,
+                         int Wl, int Hl, uint8_t* texl);
+void or_sets(const uint8_t* occ, int W, int H, int T, uint8_t* src, uint8_t* tgt);
+int or_layers(const uint8_t* occ, int W, int H, int T, uint8_t* layer);
+
+void or_patch_ssd(const or_level* lv, int32_t p, int32_t q, int lambda, int kb,
+                  uint32_t* D, uint32_t* n);
+
+int64_t or_nnf_init_random(const or_level* lv, or_nnf* nnf, uint64_t seed, int level,
+                           uint32_t outer_code, int32_t b, int32_t e);
+void or_nnf_upsample(const or_level* coarse, const or_nnf* cn, const or_level* fine, or_nnf* fn,
+                     uint64_t seed, int level, int32_t b, int32_t e);
+int64_t or_nnf_evaluate(const or_level* lv, or_nnf* nnf, int lambda, int kb, int only_layer,
+                        int32_t b, int32_t e);
+int64_t or_propagate(const or_level* lv, const or_nnf* in, or_nnf* out, int lambda, int step,
+                     int sign, int kb, int only_layer, int32_t b, int32_t e);
+int64_t or_random_search(const or_level* lv, const or_nnf* in, or_nnf* out, int lambda,
+                         uint64_t seed, double rho, int rmax, int level, uint32_t outer_code,
+                         int pm_iter, int kb, int only_layer, int32_t b, int32_t e);
+void or_reconstruct(or_level* lv, const or_nnf* nnf, int mode, int layer_j, int32_t hb, int32_t he,
+                    float* out_rgb, float* out_tex);
+void or_commit(or_level* lv, const float* out_rgb, const float* out_tex, int32_t hb, int32_t he);
+int64_t or_change_l1(const float* a, const float* b, int64_t n);
+double or_energy(const or_level* lv, const or_nnf* nnf);
+int64_t or_brute_force(const or_level* lv, or_nnf* out, int lambda, int32_t b, int32_t e);
+
+/* Whole Alg. 4 (without alignment) on host buffers; returns 0 on success. */
+typedef struct {
+  int levels, pm_iters, fixed_outer, max_outer, lambda, tex_half, n_steps;
+  int steps[8];
+  uint64_t seed;
+  double rho;
+} or_params;
+typedef struct {
+  int outer_iters[16];
+  int64_t patch_updates[16];
+  int onion_layers;
+} or_stats;
+int or_inpaint(const uint8_t* rgb, const uint8_t* occ, int W, int H, int T, const or_params* prm,
+               uint8_t* out_rgb, or_stats* st);
+
+#ifdef __cplusplus
+}
+#endif
+#endif

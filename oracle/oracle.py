@@ -1,0 +1,293 @@
+"""ctypes wrapper of the CPU oracle (oracle/liboracle.so).
+
+TEST INFRASTRUCTURE ONLY: imported by tests/, __graft_entry__.smoke() and bench.py's
+cpu_baseline / --impl reference legs.  Never imported by paper_1503_05528_b200/.
+The arithmetic lives in oracle.c (cited there, line by line, to PAPER.md); this module only
+marshals numpy arrays.
+"""
+from __future__ import annotations
+
+import ctypes as C
+import os
+from dataclasses import dataclass
+
+import numpy as np
+
+_HERE = os.path.dirname(os.path.abspath(__file__))
+_LIB_PATH = os.path.join(_HERE, "liboracle.so")
+_lib = None
+
+
+def build(force: bool = False) -> str:
+    src = os.path.join(_HERE, "oracle.c")
+    if force or not os.path.exists(_LIB_PATH) or os.path.getmtime(_LIB_PATH) < max(
+            os.path.getmtime(src), os.path.getmtime(os.path.join(_HERE, "oracle.h"))):
+        cmd = f"gcc -O2 -std=c11 -fopenmp -fPIC -shared -o {_LIB_PATH} {src} -lm"
+        if os.system(cmd) != 0:
+            raise RuntimeError("oracle build failed: " + cmd)
+    return _LIB_PATH
+
+
+class OrLevel(C.Structure):
+    _fields_ = [("W", C.c_int), ("H", C.c_int), ("T", C.c_int),
+                ("rgb", C.c_void_p), ("tex", C.c_void_p), ("occ", C.c_void_p),
+                ("src", C.c_void_p), ("tgt", C.c_void_p), ("layer", C.c_void_p),
+                ("slot", C.c_void_p),
+                ("targets", C.c_void_p), ("n_targets", C.c_int32),
+                ("holes", C.c_void_p), ("n_holes", C.c_int32),
+                ("sources", C.c_void_p), ("n_sources", C.c_int32)]
+
+
+class OrNNF(C.Structure):
+    _fields_ = [("dx", C.c_void_p), ("dy", C.c_void_p), ("dt", C.c_void_p),
+                ("D", C.c_void_p), ("n", C.c_void_p)]
+
+
+class OrParams(C.Structure):
+    _fields_ = [("levels", C.c_int), ("pm_iters", C.c_int), ("fixed_outer", C.c_int),
+                ("max_outer", C.c_int), ("lambda_", C.c_int), ("tex_half", C.c_int),
+                ("n_steps", C.c_int), ("steps", C.c_int * 8), ("seed", C.c_uint64),
+                ("rho", C.c_double)]
+
+
+class OrStats(C.Structure):
+    _fields_ = [("outer_iters", C.c_int * 16), ("patch_updates", C.c_int64 * 16),
+                ("onion_layers", C.c_int)]
+
+
+def lib():
+    global _lib
+    if _lib is None:
+        build()
+        _lib = C.CDLL(_LIB_PATH)
+        P, I, I32, I64, U64, D = C.c_void_p, C.c_int, C.c_int32, C.c_int64, C.c_uint64, C.c_double
+        sig = {
+            "or_philox4x32_10": (None, [P, U64, P]),
+            "or_pyramid_down": (None, [P, P, I, I, I, P, P]),
+            "or_texture": (None, [P, P, I, I, I, I, P]),
+            "or_texture_decimate": (None, [P, I, I, I, I, I, I, P]),
+            "or_sets": (None, [P, I, I, I, P, P]),
+            "or_layers": (I, [P, I, I, I, P]),
+            "or_patch_ssd": (None, [P, I32, I32, I, I, P, P]),
+            "or_nnf_init_random": (I64, [P, P, U64, I, C.c_uint32, I32, I32]),
+            "or_nnf_upsample": (None, [P, P, P, P, U64, I, I32, I32]),
+            "or_nnf_evaluate": (I64, [P, P, I, I, I, I32, I32]),
+            "or_propagate": (I64, [P, P, P, I, I, I, I, I, I32, I32]),
+            "or_random_search": (I64, [P, P, P, I, U64, D, I, I, C.c_uint32, I, I, I, I32, I32]),
+            "or_reconstruct": (None, [P, P, I, I, I32, I32, P, P]),
+            "or_commit": (None, [P, P, P, I32, I32]),
+            "or_change_l1": (I64, [P, P, I64]),
+            "or_energy": (D, [P, P]),
+            "or_brute_force": (I64, [P, P, I, I32, I32]),
+            "or_inpaint": (I, [P, P, I, I, I, P, P, P]),
+        }
+        for name, (res, args) in sig.items():
+            f = getattr(_lib, name)
+            f.restype = res
+            f.argtypes = args
+    return _lib
+
+
+def _p(a):
+    return None if a is None else a.ctypes.data
+
+
+def philox(ctr, seed):
+    c = np.ascontiguousarray(np.asarray(ctr, dtype=np.uint32))
+    out = np.zeros(4, dtype=np.uint32)
+    lib().or_philox4x32_10(_p(c), seed, _p(out))
+    return out
+
+
+def pyramid_down(rgb, occ):
+    T, H, W, _ = rgb.shape
+    Wc, Hc = (W + 1) // 2, (H + 1) // 2
+    rc = np.zeros((T, Hc, Wc, 3), np.uint8)
+    oc = np.zeros((T, Hc, Wc), np.uint8)
+    lib().or_pyramid_down(_p(np.ascontiguousarray(rgb)), _p(np.ascontiguousarray(occ)), W, H, T,
+                          _p(rc), _p(oc))
+    return rc, oc
+
+
+def texture(rgb, occ, h):
+    T, H, W, _ = rgb.shape
+    tex = np.zeros((T, H, W, 2), np.uint8)
+    lib().or_texture(_p(np.ascontiguousarray(rgb)), _p(np.ascontiguousarray(occ)), W, H, T, h,
+                     _p(tex))
+    return tex
+
+
+def texture_decimate(tex1, level, Wl, Hl):
+    T, H1, W1, _ = tex1.shape
+    out = np.zeros((T, Hl, Wl, 2), np.uint8)
+    lib().or_texture_decimate(_p(np.ascontiguousarray(tex1)), W1, H1, T, level, Wl, Hl, _p(out))
+    return out
+
+
+def sets(occ):
+    T, H, W = occ.shape
+    src = np.zeros_like(occ)
+    tgt = np.zeros_like(occ)
+    lib().or_sets(_p(np.ascontiguousarray(occ)), W, H, T, _p(src), _p(tgt))
+    return src, tgt
+
+
+def layers(occ):
+    T, H, W = occ.shape
+    lay = np.zeros_like(occ)
+    n = lib().or_layers(_p(np.ascontiguousarray(occ)), W, H, T, _p(lay))
+    return lay, n
+
+
+class Level:
+    """One pyramid level on host buffers (the oracle's own data model)."""
+
+    def __init__(self, rgb, tex, occ, with_layers=False):
+        self.rgb = np.ascontiguousarray(rgb, dtype=np.uint8)
+        self.tex = np.ascontiguousarray(tex, dtype=np.uint8)
+        self.occ = np.ascontiguousarray(occ, dtype=np.uint8)
+        self.T, self.H, self.W = occ.shape
+        self.src, self.tgt = sets(self.occ)
+        self.targets = np.flatnonzero(self.tgt.ravel()).astype(np.int32)
+        self.holes = np.flatnonzero(self.occ.ravel()).astype(np.int32)
+        self.sources = np.flatnonzero(self.src.ravel()).astype(np.int32)
+        self.slot = np.full(self.occ.size, -1, np.int32)
+        self.slot[self.targets] = np.arange(len(self.targets), dtype=np.int32)
+        self.layer = None
+        self.n_layers = 0
+        if with_layers:
+            self.layer, self.n_layers = layers(self.occ)
+        self._s = None
+
+    def struct(self):
+        s = OrLevel(self.W, self.H, self.T, _p(self.rgb), _p(self.tex), _p(self.occ), _p(self.src),
+                    _p(self.tgt), _p(self.layer), _p(self.slot), _p(self.targets),
+                    len(self.targets), _p(self.holes), len(self.holes), _p(self.sources),
+                    len(self.sources))
+        self._s = s
+        return C.byref(s)
+
+    @property
+    def rmax(self):
+        return max(self.W, self.H, self.T)
+
+
+@dataclass
+class NNF:
+    dx: np.ndarray
+    dy: np.ndarray
+    dt: np.ndarray
+    D: np.ndarray
+    n: np.ndarray
+
+    @classmethod
+    def empty(cls, n):
+        z = lambda dt: np.zeros(max(n, 1), dt)
+        return cls(z(np.int32), z(np.int32), z(np.int32), z(np.uint32), z(np.uint8))
+
+    def copy(self):
+        return NNF(self.dx.copy(), self.dy.copy(), self.dt.copy(), self.D.copy(), self.n.copy())
+
+    def struct(self):
+        self._s = OrNNF(_p(self.dx), _p(self.dy), _p(self.dt), _p(self.D), _p(self.n))
+        return C.byref(self._s)
+
+
+def patch_ssd(lv: Level, p, q, lam, kb=-1):
+    D = np.zeros(1, np.uint32)
+    n = np.zeros(1, np.uint32)
+    lib().or_patch_ssd(lv.struct(), int(p), int(q), lam, kb, _p(D), _p(n))
+    return int(D[0]), int(n[0])
+
+
+def init_random(lv, nnf, seed, level, outer_code, b=0, e=None):
+    e = len(lv.targets) if e is None else e
+    return lib().or_nnf_init_random(lv.struct(), nnf.struct(), seed, level, outer_code, b, e)
+
+
+def upsample(coarse, cn, fine, fn, seed, level, b=0, e=None):
+    e = len(fine.targets) if e is None else e
+    lib().or_nnf_upsample(coarse.struct(), cn.struct(), fine.struct(), fn.struct(), seed, level, b, e)
+
+
+def evaluate(lv, nnf, lam, kb=-1, ol=-1, b=0, e=None):
+    e = len(lv.targets) if e is None else e
+    return lib().or_nnf_evaluate(lv.struct(), nnf.struct(), lam, kb, ol, b, e)
+
+
+def propagate(lv, nin, nout, lam, step, sign, kb=-1, ol=-1, b=0, e=None):
+    e = len(lv.targets) if e is None else e
+    return lib().or_propagate(lv.struct(), nin.struct(), nout.struct(), lam, step, sign, kb, ol, b, e)
+
+
+def random_search(lv, nin, nout, lam, seed, rho, rmax, level, outer_code, pm_iter, kb=-1, ol=-1,
+                  b=0, e=None):
+    e = len(lv.targets) if e is None else e
+    return lib().or_random_search(lv.struct(), nin.struct(), nout.struct(), lam, seed, rho, rmax,
+                                  level, outer_code, pm_iter, kb, ol, b, e)
+
+
+def reconstruct(lv, nnf, mode, layer_j=-1, hb=0, he=None, out_rgb=None, out_tex=None):
+    he = len(lv.holes) if he is None else he
+    nh = max(len(lv.holes), 1)
+    out_rgb = np.zeros((nh, 3), np.float32) if out_rgb is None else out_rgb
+    out_tex = np.zeros((nh, 2), np.float32) if out_tex is None else out_tex
+    lib().or_reconstruct(lv.struct(), nnf.struct(), mode, layer_j, hb, he, _p(out_rgb), _p(out_tex))
+    return out_rgb, out_tex
+
+
+def commit(lv, out_rgb, out_tex, hb=0, he=None):
+    he = len(lv.holes) if he is None else he
+    lib().or_commit(lv.struct(), _p(out_rgb), _p(out_tex), hb, he)
+
+
+def change_l1(a, b):
+    a = np.ascontiguousarray(a, np.float32).ravel()
+    b = np.ascontiguousarray(b, np.float32).ravel()
+    return lib().or_change_l1(_p(a), _p(b), a.size)
+
+
+def energy(lv, nnf):
+    return lib().or_energy(lv.struct(), nnf.struct())
+
+
+def brute_force(lv, nnf, lam, b=0, e=None):
+    e = len(lv.targets) if e is None else e
+    return lib().or_brute_force(lv.struct(), nnf.struct(), lam, b, e)
+
+
+WEIGHTED, UNWEIGHTED, BEST_PATCH = 0, 1, 2
+
+
+def ann_search(lv, a: NNF, lam, seed, level, outer_code, pm_iters, steps=(8, 4, 2, 1), rho=0.5,
+               kb=-1, ol=-1):
+    """Alg. 1 schedule (R3/R5/R6), same as or_inpaint's internal ann_search; result in ``a``."""
+    b = a.copy()
+    cnt = evaluate(lv, a, lam, kb, ol)
+    for k in range(1, pm_iters + 1):
+        sign = 1 if k % 2 == 1 else -1
+        for s in steps:
+            cnt += propagate(lv, a, b, lam, s, sign, kb, ol)
+            a, b = b, a
+        cnt += random_search(lv, a, b, lam, seed, rho, lv.rmax, level, outer_code, k, kb, ol)
+        a, b = b, a
+    return a, cnt
+
+
+def inpaint(rgb, occ, levels, pm_iters=10, fixed_outer=0, max_outer=20, lam=50, seed=1,
+            steps=(8, 4, 2, 1), rho=0.5, tex_half=-1):
+    T, H, W, _ = rgb.shape
+    prm = OrParams()
+    prm.levels, prm.pm_iters, prm.fixed_outer, prm.max_outer = levels, pm_iters, fixed_outer, max_outer
+    prm.lambda_, prm.tex_half, prm.n_steps = lam, tex_half, len(steps)
+    for i, s in enumerate(steps):
+        prm.steps[i] = s
+    prm.seed, prm.rho = seed, rho
+    st = OrStats()
+    out = np.zeros_like(rgb)
+    rc = lib().or_inpaint(_p(np.ascontiguousarray(rgb)), _p(np.ascontiguousarray(occ)), W, H, T,
+                          C.byref(prm), _p(out), C.byref(st))
+    if rc != 0:
+        raise RuntimeError(f"or_inpaint failed: {rc}")
+    return out, dict(outer_iters=list(st.outer_iters)[:levels],
+                     patch_updates=list(st.patch_updates)[:levels], onion_layers=st.onion_layers)
