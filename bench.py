@@ -1,0 +1,336 @@
+#!/usr/bin/env python
+"""Benchmark of the inpainting hot path (BASELINE.json metric: PatchMatch patch-updates/s,
+inpaint s/pyramid level, % of the HBM roofline) on config c5 (1920x1080x100, L=4, K=10).
+
+A step = one full Alg. 4 pass of the hot path (pyramid, texture, sets,
+onion peel, per-level PatchMatch + reconstruction with the stopping rule, upsampling, best-patch)
+over the synthetic c5 video already resident in HBM.  `--impl reference` times the CPU oracle
+(the reference arm of this tier) on a bounded sample of the same workload.
+
+  python bench.py [--gpus N] [--steps K] [--warmup W] [--impl vinp|reference] [--config c5]
+Multi-GPU: launched by torch.distributed.run, one rank per GPU (NCCL), target slabs + all-gather.
+"""
+from __future__ import annotations
+
+import argparse
+import json
+import os
+import statistics
+import subprocess
+import sys
+import threading
+import time
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, ROOT)
+
+B_PU, B_TP, B_HOLE = 625, 29, 662  # algorithmic bytes: per patch-update / target-pass / hole
+
+
+def _peaks():
+    try:
+        with open(os.path.join(ROOT, "MEASURED_PEAKS.json")) as f:
+            p = json.load(f)
+        return float(p["hbm_gbs"]), "measured"
+    except Exception:
+        return 6650.0, "fallback"
+
+
+class Clocks:
+    """nvidia-smi sampling during the timed region (B200_PROFILING.md clocks line)."""
+
+    def __init__(self, index):
+        self.index, self.rows, self.p = index, [], None
+
+    def __enter__(self):
+        q = ("clocks.sm,clocks.max.sm,power.draw,clocks_event_reasons.active,"
+             "clocks_event_reasons.hw_slowdown,clocks_event_reasons.hw_thermal_slowdown,"
+             "clocks_event_reasons.sw_thermal_slowdown,clocks_event_reasons.sw_power_cap")
+        try:
+            self.p = subprocess.Popen(["nvidia-smi", "-i", str(self.index), f"--query-gpu={q}",
+                                       "--format=csv,noheader,nounits", "-lms", "200"],
+                                      stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
+            self.t = threading.Thread(target=self._read, daemon=True)
+            self.t.start()
+        except Exception:
+            self.p = None
+        return self
+
+    def _read(self):
+        for line in self.p.stdout:
+            self.rows.append([x.strip() for x in line.split(",")])
+
+    def __exit__(self, *a):
+        if self.p:
+            self.p.terminate()
+            try:
+                self.p.wait(2)
+            except Exception:
+                pass
+
+    def summary(self):
+        if not self.rows:
+            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["unavailable"]}
+        sm = [float(r[0]) for r in self.rows if r[0].replace(".", "").isdigit()]
+        mx = [float(r[1]) for r in self.rows if r[1].replace(".", "").isdigit()]
+        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+        reasons = set()
+        for r in self.rows:
+            for n, v in zip(names, r[4:8]):
+                if v.lower().startswith("active"):
+                    reasons.add(n)
+        return {"sm_mhz": statistics.median(sm) if sm else None, "sm_max_mhz": max(mx) if mx else None,
+                "reasons": sorted(reasons), "samples": len(self.rows)}
+
+
+def _cfg(name):
+    from gen.synth import CONFIGS
+    from paper_1503_05528_b200 import Config
+    c = CONFIGS[name]
+    return Config(levels=c.levels, pm_iters=c.pm_iters, fixed_outer=c.fixed_outer, max_outer=c.max_outer,
+                  lam=c.lam, seed=c.seed)
+
+
+# ----------------------------------------------------------------------------- oracle sample
+def oracle_sample(name, frames, t0, pm_iters=1):
+    """The CPU oracle on a bounded sample of config `name`: a temporal crop of `frames` frames
+    starting at t0, finest level, random init + evaluate + `pm_iters` PatchMatch iterations.
+    Returns (patch_updates, seconds, threads)."""
+    import numpy as np
+    import torch
+    import oracle.oracle as orc
+    from gen.synth import generate, CONFIGS
+    v, m, _ = generate(name, device="cuda" if torch.cuda.is_available() else "cpu", frames=t0 + frames)
+    rgb = np.ascontiguousarray(v[t0:t0 + frames].cpu().numpy())
+    occ = np.ascontiguousarray(m[t0:t0 + frames].cpu().numpy())
+    L = CONFIGS[name].levels
+    tex = orc.texture(rgb, occ, max(1, 2 ** (L - 2)) if L >= 2 else 1)
+    lv = orc.Level(rgb, tex, occ)
+    f = orc.NNF.empty(len(lv.targets))
+    orc.init_random(lv, f, CONFIGS[name].seed, 1, 0)
+    t = time.perf_counter()
+    f, cnt = orc.ann_search(lv, f, CONFIGS[name].lam, CONFIGS[name].seed, 1, 0, pm_iters)
+    dt = time.perf_counter() - t
+    threads = int(os.environ.get("OMP_NUM_THREADS", os.cpu_count() or 1))
+    return int(cnt), dt, threads
+
+
+def run_reference(args):
+    rank = int(os.environ.get("RANK", "0"))
+    if rank != 0:
+        return 0
+    frames, t0 = 4, 48
+    for _ in range(args.warmup):
+        oracle_sample(args.config, frames, t0)
+    tot_pu, tot_s = 0, 0.0
+    for _ in range(args.steps):
+        pu, s, thr = oracle_sample(args.config, frames, t0)
+        tot_pu += pu
+        tot_s += s
+    val = tot_pu / tot_s
+    sample = f"{args.config} frames [{t0},{t0 + frames}) at level 1: evaluate + 1 PatchMatch iteration from random init"
+    line = {"impl": "reference", "metric": "PatchMatch patch-updates/sec", "value": val,
+            "unit": "patch-updates/s", "n_gpus": args.gpus, "steps": args.steps, "warmup": args.warmup,
+            "ms_per_step": 1000 * tot_s / args.steps, "higher_is_better": True, "dtype": "u8",
+            "data": "synthetic", "config": {"workload": args.config, "sample": sample},
+            "cpu_baseline": {"value": val, "unit": "patch-updates/s", "cores": thr, "kind": "oracle",
+                             "sample": sample},
+            "e2e": {"value": val, "unit": "patch-updates/s", "h2d_bytes_per_step": 0,
+                    "d2h_bytes_per_step": 0}}
+    print(json.dumps(line), flush=True)
+    return 0
+
+
+# ----------------------------------------------------------------------------- GPU arm
+def main():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=2)
+    ap.add_argument("--warmup", type=int, default=3)
+    ap.add_argument("--impl", default="vinp", choices=["vinp", "reference"])
+    ap.add_argument("--config", default="c5")
+    ap.add_argument("--no-e2e", action="store_true")
+    ap.add_argument("--no-cpu", action="store_true")
+    args = ap.parse_args()
+    if args.impl == "reference":
+        return run_reference(args)
+
+    import torch
+    import torch.distributed as dist
+    from gen.synth import generate, CONFIGS
+    from paper_1503_05528_b200 import Exchange, Inpainter, inpaint, vinp as V
+
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    rank = int(os.environ.get("RANK", "0"))
+    local = int(os.environ.get("LOCAL_RANK", "0"))
+    torch.cuda.set_device(local)
+    dev = torch.device("cuda", local)
+    if world > 1:
+        dist.init_process_group("nccl", device_id=dev)
+    ex = Exchange()
+    cfg = _cfg(args.config)
+    c = CONFIGS[args.config]
+    v, m, _ = generate(args.config, device=dev)
+    torch.cuda.synchronize()
+    ip = Inpainter(c.W, c.H, c.T, cfg, dev, ex)
+
+    def step():
+        ip.load(v, m)
+        return ip.run(timing=False)
+
+    def barrier():
+        if world > 1:
+            dist.barrier()
+        torch.cuda.synchronize()
+
+    for _ in range(args.warmup):
+        step()
+    barrier()
+    n0 = V.launch_count()
+    pu = 0
+    with Clocks(local) as clk:
+        e0 = torch.cuda.Event(enable_timing=True)
+        e1 = torch.cuda.Event(enable_timing=True)
+        e0.record()
+        for _ in range(args.steps):
+            st = step()
+            pu += st.total_patch_updates
+        e1.record()
+        barrier()
+    launches = V.launch_count() - n0
+    ms = e0.elapsed_time(e1)
+    t = torch.tensor([ms], dtype=torch.float64, device=dev)
+    if world > 1:
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+    ms = float(t.item())
+    value = pu / (ms / 1000.0)
+
+    # per-level seconds (one timed run with per-level events)
+    ip.load(v, m)
+    stats = ip.run(timing=True)
+    levels = [{"level": l["level"], "outer": l["outer"], "s": l["ms"] / 1000.0} for l in stats.levels]
+
+    # dominant-kernel roofline: one instrumented step with events around every pass
+    roof = measure_roofline(ip, v, m, dev)
+
+    e2e = None
+    if not args.no_e2e:
+        rgb_h = v.cpu().pin_memory()
+        m_h = m.cpu().pin_memory()
+        for _ in range(1):
+            out, s2, _ = inpaint(rgb_h, m_h, cfg, device=dev, exchange=ex)
+            out.cpu()
+        barrier()
+        t0 = time.perf_counter()
+        ea, eb = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        ea.record()
+        pu2 = 0
+        for _ in range(args.steps):
+            out, s2, _ = inpaint(rgb_h, m_h, cfg, device=dev, exchange=ex)
+            res = out.cpu()
+            pu2 += s2.total_patch_updates
+        eb.record()
+        barrier()
+        ms2 = ea.elapsed_time(eb)
+        t2 = torch.tensor([ms2], dtype=torch.float64, device=dev)
+        if world > 1:
+            dist.all_reduce(t2, op=dist.ReduceOp.MAX)
+        e2e = {"value": pu2 / (float(t2.item()) / 1000.0), "unit": "patch-updates/s",
+               "h2d_bytes_per_step": int(v.numel() + m.numel()), "d2h_bytes_per_step": int(res.numel())}
+
+    cpu = None
+    if rank == 0 and world == 1 and not args.no_cpu:
+        frames, t0 = 4, 48
+        pu_c, s_c, thr = oracle_sample(args.config, frames, t0)
+        cpu = {"value": pu_c / s_c, "unit": "patch-updates/s", "cores": thr, "kind": "oracle",
+               "sample": f"{args.config} frames [{t0},{t0 + frames}) level 1: evaluate + 1 PM iteration "
+                         f"from random init ({pu_c} patch-updates in {s_c:.1f} s)"}
+
+    if rank == 0:
+        line = {"metric": "PatchMatch patch-updates/sec", "value": value, "unit": "patch-updates/s",
+                "n_gpus": world, "steps": args.steps, "warmup": args.warmup, "ms_per_step": ms / args.steps,
+                "higher_is_better": True, "scaling": "strong", "vs_baseline": None, "dtype": "u8",
+                "data": "synthetic",
+                "config": {"workload": args.config, "dims": [c.W, c.H, c.T], "levels": c.levels,
+                           "pm_iters": c.pm_iters, "patch": "5x5x5", "lambda": c.lam,
+                           "l2": "inputs larger than L2 (level-1 volume 1.66 GB)",
+                           "parallelism": f"target slabs x{world}"},
+                "patch_updates_per_step": pu // args.steps, "sec_per_level": levels,
+                "roofline": roof, "cpu_baseline": cpu, "e2e": e2e, "gpu_launches": launches,
+                "clocks": clk.summary()}
+        print(json.dumps(line), flush=True)
+    if world > 1:
+        dist.destroy_process_group()
+    return 0
+
+
+def measure_roofline(ip, v, m, dev):
+    """Times every libvinp pass of one full step with CUDA events on the launching stream and
+    attributes algorithmic bytes to each kernel; returns the dominant kernel's line."""
+    import torch
+    from paper_1503_05528_b200 import vinp as V
+    peak, kind = _peaks()
+    rec = []
+    snaps = []
+    orig = {}
+
+    def wrap(name, nt_fn):
+        f = getattr(V, name)
+        orig[name] = f
+
+        def g(*a, **k):
+            s0 = torch.cuda.Event(enable_timing=True)
+            s1 = torch.cuda.Event(enable_timing=True)
+            c0 = ip.counter.clone()
+            s0.record()
+            f(*a, **k)
+            s1.record()
+            rec.append((name, s0, s1, c0, ip.counter.clone(), nt_fn(*a, **k)))
+        setattr(V, name, g)
+
+    # slot range [b, e) of each call, from its positional arguments (see paper_1503_05528_b200/vinp.py)
+    wrap("propagate", lambda lv, *a, **k: (a[7], a[8]))
+    wrap("random_search", lambda lv, *a, **k: (a[7], a[8]))
+    wrap("nnf_evaluate", lambda lv, *a, **k: (a[4], a[5]))
+    wrap("reconstruct", lambda lv, *a, **k: (a[5], a[6]))
+    try:
+        ip.load(v, m)
+        ip.run(timing=False)
+        torch.cuda.synchronize()
+    finally:
+        for k2, f in orig.items():
+            setattr(V, k2, f)
+    agg = {}
+    for name, s0, s1, c0, c1, (b, e) in rec:
+        ms = s0.elapsed_time(s1)
+        pu = int(c1.item() - c0.item())
+        slots = e - b
+        if name == "reconstruct":
+            by = B_HOLE * slots
+        else:
+            by = B_PU * pu + B_TP * slots
+        a = agg.setdefault(name, {"ms": 0.0, "bytes": 0, "launches": 0, "pu": 0})
+        a["ms"] += ms
+        a["bytes"] += by
+        a["launches"] += 1
+        a["pu"] += pu
+    tot = sum(a["ms"] for a in agg.values())
+    dom = max(agg, key=lambda k: agg[k]["ms"])
+    a = agg[dom]
+    achieved = a["bytes"] / (a["ms"] / 1000.0) / 1e9
+    kernels = {k: {"share": round(x["ms"] / tot, 4), "GB/s": round(x["bytes"] / (x["ms"] / 1000) / 1e9, 1),
+                   "launches": x["launches"], "patch_updates": x["pu"]} for k, x in agg.items()}
+    traffic = None
+    try:
+        with open(os.path.join(ROOT, "profiles", "traffic.json")) as f:
+            traffic = json.load(f).get(dom)
+    except Exception:
+        pass
+    return {"kernel": f"vinp_{dom}", "bound": "hbm", "achieved": round(achieved, 1), "peak": peak,
+            "peak_kind": kind, "unit": "GB/s", "frac": round(achieved / peak, 4),
+            "traffic": traffic, "bytes_per_launch": a["bytes"] / a["launches"],
+            "avg_launch_ms": a["ms"] / a["launches"], "kernels": kernels}
+
+
+if __name__ == "__main__":
+    sys.exit(main())

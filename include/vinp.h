@@ -1,0 +1,198 @@
+/* vinp.h — C ABI of the B200 (sm_100a) video-inpainting hot path.
+ *
+ * Paper: A. Newson, A. Almansa, M. Fradet, Y. Gousseau, P. Perez, "Video inpainting of complex
+ * scenes", arXiv 1503.05528.  "P:n" = line n of the paper source; "R<k>" = reading k
+ * in DESIGN.md §2 (where the paper is silent or garbled).  Every call below names the passage
+ * that defines its operation.
+ *
+ * Conventions (all calls)
+ *  - Buffers are DEVICE pointers owned by the caller (allocated as torch tensors by the Python
+ *    binding).  The library never allocates device memory; scratch comes from caller-provided
+ *    workspaces whose size is returned by the *_ws_bytes queries.
+ *  - `stream` is a cudaStream_t passed as void*.  Calls enqueue work and return without
+ *    synchronising, except where a call says it returns host-visible counts.
+ *  - Return value: VINP_OK or an error code.  Argument errors are detected synchronously;
+ *    device faults surface as VINP_E_CUDA on this or a later call.  vinp_last_error() gives a
+ *    thread-local message valid until the next call on that thread.  No C++ exception crosses
+ *    the ABI.
+ *  - Volumes are t-major: linear index p = (t*H + y)*W + x; this order is also the
+ *    lexicographic order of every tie-break (R28).
+ *  - Patches are 5x5x5; lambda must lie in [0, 126] so that D fits in 32 bits.
+ *
+ * Data layout in HBM (one vinp_level per pyramid level, level 1 = finest)
+ *  - vox   u64 [T][H][W]: bits 0-7 R, 8-15 G, 16-23 B (working copy u), bits 32-39 T_x,
+ *          40-47 T_y in half-grey-level units (T_q = round(2T), Eq. 8, R24); rest 0.
+ *  - flags u8  [T][H][W]: bit0 = p in H (occlusion), bit1 = p in D~ (valid source
+ *          centre), bit2 = p in H~ (target).
+ *  - layer u8  [T][H][W]: onion layer = L_inf distance to D (Alg. 3, R22); coarsest level only,
+ *          else NULL.
+ *  - slot  i32 [T][H][W]: voxel -> index in `targets`, or -1.
+ *  - targets / holes / sources: sorted i32 lists of H~, H and D~.
+ *  - NNF (shift map phi) over target slots: e[s] = (D << 32) | q with q = p + phi(p)
+ *    the source linear index and D the integer patch distance below; n[s] = |N_p cap Omega cap K|.
+ *
+ * Integer patch distance (Eq. 9, partial form Eq. 12; R23-R24):
+ *    D(p,q) = sum_{r in N_p cap Omega cap K} 4 ||u(r) - u(r-p+q)||^2 + lambda ||T_q(r) - T_q(r-p+q)||^2
+ *    d^2(p,q) = D / (4n).
+ *  K ("known") is Omega when kb < 0, else {r : layer(r) < kb} (onion peel, Alg. 3).
+ *  `only_layer` >= 0 restricts a pass to targets p with layer(p) == only_layer (others are
+ *  copied from `in` to `out` unchanged).
+ */
+#ifndef VINP_H
+#define VINP_H
+#include <stddef.h>
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+typedef enum {
+  VINP_OK = 0,
+  VINP_E_INVALID = 1,     /* null pointer, bad shape or range (synchronous) */
+  VINP_E_NO_SOURCE = 2,   /* D~ empty at a level: nothing to inpaint from */
+  VINP_E_CUDA = 3,        /* launch or runtime error */
+  VINP_E_UNSUPPORTED = 4  /* lambda outside [0,126], dims too large, ... */
+} vinp_status;
+
+enum { VINP_WEIGHTED = 0, VINP_UNWEIGHTED = 1, VINP_BEST_PATCH = 2 };
+
+typedef struct {
+  int32_t W, H, T;   /* dims of this level: W_l = ceil(W/2^(l-1)), T never subsampled */
+  int32_t level;     /* 1 = finest; enters the Philox counter */
+  uint64_t* vox;
+  uint8_t* flags;
+  uint8_t* layer;    /* or NULL */
+  int32_t* slot;
+  int32_t* targets; int32_t n_targets;
+  int32_t* holes;   int32_t n_holes;
+  int32_t* sources; int32_t n_sources;
+} vinp_level;
+
+typedef struct {
+  uint64_t* e;  /* [n_targets] (D << 32) | source index */
+  uint8_t* n;   /* [n_targets] patch voxel count; may be shared by ping-pong buffers */
+} vinp_nnf;
+
+typedef struct {
+  int32_t lambda;    /* texture weight, 50 */
+  int32_t tex_half;  /* half-width h of the texture window nu (R15); -1 = max(1, 2^(L-2)) */
+  uint64_t seed;     /* Philox key */
+  double rho;        /* random-search window reduction, 0.5 */
+  int32_t rmax;      /* random-search radius; -1 = max(W_l, H_l, T) (R7) */
+} vinp_params;
+
+const char* vinp_last_error(void);
+int vinp_version(void);
+/* Number of kernels this library has launched since it was loaded (evidence counter). */
+uint64_t vinp_launch_count(void);
+
+/* ---- a1: video + occlusion pyramid (Alg. 4; spatial only P:878-882; R17/R18) ----
+ * rgb: u8 [T][H][W][3] and mask: u8 [T][H][W] (nonzero = occluded), device, level-1 dims.
+ * Writes vox colour bytes and flags bit0 of levels 1..L (lv[0..L-1]); texture bytes are zeroed.
+ * Coarse value = round-half-up of the binomial (1,4,6,4,1)^2 mean over unoccluded fine voxels
+ * (reflect-101 borders), 0 if none; coarse occluded iff any of its 2x2 fine voxels is. */
+vinp_status vinp_build_pyramid(const uint8_t* rgb, const uint8_t* mask, vinp_level* lv, int L,
+                               void* stream);
+
+/* ---- a3: texture features + texture pyramid (Eq. 8; Eq. 10; R14-R16) ----
+ * Computes T on level 1 from its colour and occlusion (masked central differences of the
+ * x1000 Rec.601 luma, mean over the (2h+1)^2 window) and writes T^l(x,y,t) = T(2^(l-1)x,
+ * 2^(l-1)y, t) into the texture bytes of every level.  ws: vinp_texture_ws_bytes(lv[0]). */
+size_t vinp_texture_ws_bytes(const vinp_level* lv1);
+vinp_status vinp_texture_features(const vinp_params* prm, vinp_level* lv, int L, void* ws,
+                                  size_t ws_bytes, void* stream);
+
+/* ---- a2: source/target sets ----
+ * vinp_build_sets: flags bit1 (D~) and bit2 (H~) from bit0 for levels 1..L, and returns the
+ * list sizes in counts_out[3l+0..2] = |H~|, |H|, |D~| (host memory; this call synchronises).
+ * vinp_build_lists: fills targets/holes/sources (ascending) and slot for levels 1..L into
+ * caller buffers sized from those counts; sets lv[l].n_*.  ws: vinp_sets_ws_bytes. */
+size_t vinp_sets_ws_bytes(const vinp_level* lv1);
+vinp_status vinp_build_sets(vinp_level* lv, int L, int32_t* counts_out, void* ws, size_t ws_bytes,
+                            void* stream);
+vinp_status vinp_build_lists(vinp_level* lv, int L, void* ws, size_t ws_bytes, void* stream);
+
+/* ---- Alg. 3 onion layers: layer(p) = L_inf distance from p to D, out-of-bounds occluded (R22).
+ * Writes lv->layer; *n_layers_out = max layer (host; synchronises).  ws: >= 16 device bytes. */
+vinp_status vinp_layers(vinp_level* lv, int32_t* n_layers_out, void* ws, void* stream);
+
+/* ---- a5: NNF initialisation ----
+ * Random (Alg. 4; R8): q = sources[(U0 |D~|) >> 32], U0 = Philox(p, 0,
+ * (level<<24)|(1<<16), outer_code).  Upsample (Alg. 4; R21): fine shift =
+ * (2dx, 2dy, dt) of the coarse shift at (x/2, y/2, t); invalid results are re-drawn with stream 3.
+ * Evaluate: (D, n) of the current shift on the current u and K.  All act on target slots
+ * [b, e).  D of init/upsample is left 0 until evaluate. */
+vinp_status vinp_nnf_init_random(const vinp_level* lv, vinp_nnf* nnf, const vinp_params* prm,
+                                 uint32_t outer_code, int32_t b, int32_t e, void* stream);
+vinp_status vinp_nnf_upsample(const vinp_level* coarse, const vinp_nnf* cn, const vinp_level* fine,
+                              vinp_nnf* fn, const vinp_params* prm, int32_t b, int32_t e,
+                              void* stream);
+vinp_status vinp_nnf_evaluate(const vinp_level* lv, vinp_nnf* nnf, const vinp_params* prm, int kb,
+                              int only_layer, int32_t b, int32_t e, unsigned long long* counter,
+                              void* stream);
+
+/* ---- a6: propagation, one Jacobi jump pass (Alg. 1; R2, R5, R6, R25) ----
+ * Candidates in rank order: 0 = in(p); 1..3 = in(p + sign*step*e_x / e_y / e_t) for neighbours in
+ * Omega and H~.  A candidate is evaluated iff q = p + v is in Omega and D~ and v differs from the
+ * incumbent and from every earlier valid candidate; strict improvement wins.  Reads `in`, writes
+ * `out` for slots [b, e).  counter (device, may be NULL) += evaluated candidates. */
+vinp_status vinp_propagate(const vinp_level* lv, const vinp_nnf* in, vinp_nnf* out,
+                           const vinp_params* prm, int step, int sign, int kb, int only_layer,
+                           int32_t b, int32_t e, unsigned long long* counter, void* stream);
+
+/* ---- a7: random search (Eq. 3, Alg. 1; R1, R3, R7) ----
+ * v0 = in(p); for i = 1, 2, ...: R_i = rmax * rho^i (repeated fp64 multiplication) while
+ * R_i >= 1; delta_c = (U_c - 2^31) 2^-31 from Philox(p, pm_iter, (level<<24)|(2<<16)|i,
+ * outer_code); q_i = p + v0 + floor(R_i delta).  Same validity / duplicate / strict rules. */
+vinp_status vinp_random_search(const vinp_level* lv, const vinp_nnf* in, vinp_nnf* out,
+                               const vinp_params* prm, uint32_t outer_code, int pm_iter, int kb,
+                               int only_layer, int32_t b, int32_t e, unsigned long long* counter,
+                               void* stream);
+
+/* ---- a8: ANN search (Alg. 1), single GPU: evaluate, then for k = 1..K: for each step
+ * s in steps: propagate(s, sign = +1 for odd k, -1 for even k); random_search(k).  Uses `b` as the
+ * ping-pong buffer; the result is in `a`. */
+vinp_status vinp_ann_search(const vinp_level* lv, vinp_nnf* a, vinp_nnf* b, const vinp_params* prm,
+                            uint32_t outer_code, int K, const int32_t* steps, int n_steps, int kb,
+                            int only_layer, unsigned long long* counter, void* stream);
+
+/* ---- a9/a10: reconstruction (Eqs. 4-5, Eq. 6, Eq. 11, Eq. 13
+ * P:829-832; R10-R13, R20, R26, R27) ----
+ * For holes[h], h in [hb, he) (and layer(p) == layer_j if layer_j >= 0): contributors q in
+ * N_p cap Omega (with layer(q) < layer_j for an onion layer).  mode VINP_WEIGHTED: sigma^2 = the
+ * ceil(0.75 m)-th smallest d^2_q (exact rationals), weights round(exp(-a_q) 2^36) with
+ * a_q = D_q n_s / (2 n_q D_s); mean over zero-distance contributors if sigma = 0.
+ * VINP_UNWEIGHTED: weights 1.  VINP_BEST_PATCH: copy from argmin d^2_q (ties -> smallest q).
+ * Writes out_rgb[h][3], out_tex[h][2] (fp32; texture in half-grey units) and, if commit != 0,
+ * the u8 working copy floor(x + 0.5) into vox at p. */
+vinp_status vinp_reconstruct(vinp_level* lv, const vinp_nnf* nnf, int mode, int layer_j, int32_t hb,
+                             int32_t he, float* out_rgb, float* out_tex, int commit, void* stream);
+/* Write floor(x + 0.5) of out_rgb/out_tex for holes [hb, he) (layer_j filter as above) into vox. */
+vinp_status vinp_commit(vinp_level* lv, const float* out_rgb, const float* out_tex, int layer_j,
+                        int32_t hb, int32_t he, void* stream);
+
+/* ---- a11: stopping-rule change (Alg. 4, R19): *out (device int64) += sum_i
+ * llrint(|a_i - b_i| 2^20).  e = out / 2^20 / (3|H|). */
+vinp_status vinp_change_l1(const float* a, const float* b, int64_t n, int64_t* out, void* stream);
+
+/* ---- Eq. 1 P:286-289 (diagnostic): *out (device double) = sum_{p in H} D_p / (4 n_p). */
+vinp_status vinp_energy(const vinp_level* lv, const vinp_nnf* nnf, double* out, void* stream);
+
+/* ---- a13: exact NN (definition of Matching): argmin over q in D~ of D(p, q), K = Omega,
+ * ties -> smallest q; target slots [b, e).  ws: vinp_brute_force_ws_bytes. */
+size_t vinp_brute_force_ws_bytes(const vinp_level* lv);
+vinp_status vinp_brute_force(const vinp_level* lv, vinp_nnf* out, const vinp_params* prm, int32_t b,
+                             int32_t e, void* ws, size_t ws_bytes, void* stream);
+
+/* ---- test hooks ----
+ * vinp_patch_ssd: D and n of pairs (p[i], q[i]) with known set kb (q must be in D~).
+ * vinp_philox: out[i][0..3] = Philox4x32-10(ctr[i][0..3], key = seed). */
+vinp_status vinp_patch_ssd(const vinp_level* lv, const int32_t* p, const int32_t* q, int64_t n,
+                           const vinp_params* prm, int kb, uint32_t* D, uint8_t* cnt, void* stream);
+vinp_status vinp_philox(const uint32_t* ctr, int64_t n, uint64_t seed, uint32_t* out, void* stream);
+
+#ifdef __cplusplus
+}
+#endif
+#endif

@@ -503,7 +503,9 @@ void or_reconstruct(or_level* lv, const or_nnf* nnf, int mode, int layer_j, int3
           int32_t q = (int32_t)lin(lv, qx, qy, qt);
           if (layer_j >= 0 && !(lv->layer[q] < layer_j)) continue;
           int32_t s = lv->slot[q];
-          if (s < 0 || nnf->n[s] == 0) continue; /* cannot happen for p in H (q in H~) */
+          if (s < 0) continue; /* cannot happen for p in H (q in H~) */
+          /* distances are only defined after an evaluate (n > 0); UNWEIGHTED does not use them */
+          if (mode != OR_UNWEIGHTED && nnf->n[s] == 0) continue;
           cq[m] = q;
           cs[m] = s;
           ++m;

@@ -1,0 +1,511 @@
+// ann.cu — PatchMatch ANN search on sm_100a: NNF init / upsample / evaluate (a5), Jacobi jump
+// propagation (a6), Philox random search (a7), the Alg. 1 schedule (a8), exact brute force (a13,
+// CUDA-core form), and the SSD / Philox test hooks.
+//
+// Execution model: one warp per target p.  The warp holds the target patch N_p in registers
+// (lane l owns voxels v = l + 32i, i < 4) and evaluates each candidate source patch with one
+// coalesced 8-byte gather per voxel, VABSDIFF4 + IDP.4A per colour / texture word and one
+// REDUX.SUM across the warp (common.cuh).  Candidate generation (neighbour shifts, Philox draws,
+// validity, de-duplication) is spread across lanes, so a candidate costs ~4 loads + 20 ALU ops
+// per lane.  Every pass reads NNF buffer `in` and writes `out` (double buffering): no atomics
+// on the NNF, results independent of scheduling.
+#include <vector>
+
+#include "common.cuh"
+
+namespace vinp {
+
+static inline int nblk(int64_t n, int t) { return (int)((n + t - 1) / t); }
+constexpr int kWarpsPerBlock = 8;
+
+struct LevelArgs {
+  Geo g;
+  const uint64_t* vox;
+  const uint8_t* flags;
+  const uint8_t* layer;
+  const int32_t* slot;
+  const int32_t* targets;
+  const int32_t* sources;
+  int32_t n_sources;
+  int level;
+};
+static LevelArgs args_of(const vinp_level* lv) {
+  return LevelArgs{geo_of(lv), lv->vox,     lv->flags,     lv->layer, lv->slot,
+                   lv->targets, lv->sources, lv->n_sources, lv->level};
+}
+
+__device__ __forceinline__ int lin(const Geo& g, int x, int y, int t) {
+  return t * g.HW + y * g.W + x;
+}
+
+__device__ __forceinline__ void flush_count(unsigned long long* counter, unsigned cnt) {
+  if (counter && cnt) atomicAdd(counter, (unsigned long long)cnt);
+}
+
+// ------------------------------------------------------------------ a5: random init
+__global__ void k_init_random(LevelArgs a, uint64_t* __restrict__ e_out, uint8_t* __restrict__ n_out,
+                              uint64_t seed, uint32_t oc, int32_t b, int32_t e) {
+  int s = b + blockIdx.x * blockDim.x + threadIdx.x;
+  if (s >= e) return;
+  int p = a.targets[s];
+  uint4 u = draw((uint32_t)p, 0, a.level, kStreamInit, 0, oc, seed);
+  int q = a.sources[__umulhi(u.x, (uint32_t)a.n_sources)];
+  e_out[s] = pack_e(0, q);
+  n_out[s] = 0;
+}
+
+// ------------------------------------------------------------------ a5: upsample (+ R21 repair)
+__global__ void k_upsample(LevelArgs c, const uint64_t* __restrict__ ce, LevelArgs f,
+                           uint64_t* __restrict__ fe, uint8_t* __restrict__ fn, uint64_t seed,
+                           int32_t b, int32_t e) {
+  int s = b + blockIdx.x * blockDim.x + threadIdx.x;
+  if (s >= e) return;
+  int p = f.targets[s];
+  int px, py, pt;
+  decode(f.g, p, px, py, pt);
+  int cx = px >> 1, cy = py >> 1;
+  int cs = c.slot[lin(c.g, cx, cy, pt)];
+  int q = -1;
+  if (cs >= 0) {
+    int cq = e_q(ce[cs]);
+    int qx, qy, qt;
+    decode(c.g, cq, qx, qy, qt);
+    int fx = px + 2 * (qx - cx), fy = py + 2 * (qy - cy), ft = pt + (qt - pt);
+    if (is_source(f.g, f.flags, fx, fy, ft)) q = lin(f.g, fx, fy, ft);
+  }
+  if (q < 0) {
+    uint4 u = draw((uint32_t)p, 0, f.level, kStreamRepair, 0, 0, seed);
+    q = f.sources[__umulhi(u.x, (uint32_t)f.n_sources)];
+  }
+  fe[s] = pack_e(0, q);
+  fn[s] = 0;
+}
+
+// ------------------------------------------------------------------ a5: evaluate
+__global__ void __launch_bounds__(256) k_evaluate(LevelArgs a, uint64_t* __restrict__ ee,
+                                                  uint8_t* __restrict__ en, int lambda, int kb,
+                                                  int only_layer, int32_t b, int32_t e,
+                                                  unsigned long long* counter) {
+  int lane = threadIdx.x & 31;
+  int s = b + blockIdx.x * kWarpsPerBlock + (threadIdx.x >> 5);
+  if (s >= e) return;
+  int p = a.targets[s];
+  if (only_layer >= 0 && a.layer[p] != only_layer) return;
+  PatchLanes L;
+  init_lanes(L, a.g, lane);
+  int px, py, pt;
+  decode(a.g, p, px, py, pt);
+  TargetPatch tp;
+  load_target(tp, L, a.g, a.vox, a.layer, kb, p, px, py, pt);
+  int q = e_q(ee[s]);
+  uint32_t D = warp_ssd(tp, L, a.vox, q, lambda);
+  uint32_t n = __reduce_add_sync(kFull, (uint32_t)__popc(tp.mask));
+  if (lane == 0) {
+    ee[s] = pack_e(D, q);
+    en[s] = (uint8_t)n;
+    flush_count(counter, 1);
+  }
+}
+
+// evaluate a list of candidate sources (warp-uniform) against the incumbent, in rank order
+__device__ __forceinline__ void eval_candidates(const TargetPatch& tp, const PatchLanes& L,
+                                                const uint64_t* __restrict__ vox, int lambda,
+                                                unsigned mask, int qlane, uint32_t& bestD,
+                                                int& bestq) {
+  while (mask) {
+    int i0 = __ffs(mask) - 1;
+    mask &= mask - 1;
+    int q0 = __shfl_sync(kFull, qlane, i0);
+    if (mask) {
+      int i1 = __ffs(mask) - 1;
+      mask &= mask - 1;
+      int q1 = __shfl_sync(kFull, qlane, i1);
+      uint32_t D0, D1;
+      warp_ssd2(tp, L, vox, q0, q1, lambda, D0, D1);
+      if (D0 < bestD) { bestD = D0; bestq = q0; }
+      if (D1 < bestD) { bestD = D1; bestq = q1; }
+    } else {
+      uint32_t D0 = warp_ssd(tp, L, vox, q0, lambda);
+      if (D0 < bestD) { bestD = D0; bestq = q0; }
+    }
+  }
+}
+
+// ------------------------------------------------------------------ a6: propagation pass
+__global__ void __launch_bounds__(256) k_propagate(LevelArgs a, const uint64_t* __restrict__ ein,
+                                                   uint64_t* __restrict__ eout, int lambda, int step,
+                                                   int sign, int kb, int only_layer, int32_t b,
+                                                   int32_t e, unsigned long long* counter) {
+  int lane = threadIdx.x & 31;
+  int s = b + blockIdx.x * kWarpsPerBlock + (threadIdx.x >> 5);
+  if (s >= e) return;
+  int p = a.targets[s];
+  uint64_t inc = ein[s];
+  if (only_layer >= 0 && a.layer[p] != only_layer) {
+    if (lane == 0) eout[s] = inc;
+    return;
+  }
+  int px, py, pt;
+  decode(a.g, p, px, py, pt);
+  int q0 = e_q(inc);
+  // lanes 0,1,2: neighbour r = p + sign*step*e_{x,y,t}; candidate q = p + phi(r)
+  int q = -1;
+  if (lane < 3) {
+    int ox = lane == 0 ? sign * step : 0, oy = lane == 1 ? sign * step : 0,
+        ot = lane == 2 ? sign * step : 0;
+    int rx = px + ox, ry = py + oy, rt = pt + ot;
+    if (inside(a.g, rx, ry, rt)) {
+      int rs = __ldg(a.slot + lin(a.g, rx, ry, rt));
+      if (rs >= 0) {
+        int src = e_q(__ldg(reinterpret_cast<const unsigned long long*>(ein) + rs));
+        int sx, sy, st;
+        decode(a.g, src, sx, sy, st);
+        int qx = sx - ox, qy = sy - oy, qt = st - ot;  // q = p + (src - r)
+        if (is_source(a.g, a.flags, qx, qy, qt)) q = lin(a.g, qx, qy, qt);
+      }
+    }
+  }
+  int c0 = __shfl_sync(kFull, q, 0), c1 = __shfl_sync(kFull, q, 1);
+  bool ok = lane < 3 && q >= 0 && q != q0 && !(lane >= 1 && q == c0) && !(lane >= 2 && q == c1);
+  unsigned mask = __ballot_sync(kFull, ok);
+  uint32_t bestD = e_D(inc);
+  int bestq = q0;
+  if (mask) {
+    PatchLanes L;
+    init_lanes(L, a.g, lane);
+    TargetPatch tp;
+    load_target(tp, L, a.g, a.vox, a.layer, kb, p, px, py, pt);
+    eval_candidates(tp, L, a.vox, lambda, mask, q, bestD, bestq);
+  }
+  if (lane == 0) {
+    eout[s] = pack_e(bestD, bestq);
+    flush_count(counter, __popc(mask));
+  }
+}
+
+// ------------------------------------------------------------------ a7: random search pass
+struct Radii {
+  double R[32];
+  int M;
+};
+
+__global__ void __launch_bounds__(256) k_random_search(LevelArgs a, const uint64_t* __restrict__ ein,
+                                                       uint64_t* __restrict__ eout, int lambda,
+                                                       Radii rad, uint64_t seed, uint32_t oc,
+                                                       int pm_iter, int kb, int only_layer, int32_t b,
+                                                       int32_t e, unsigned long long* counter) {
+  int lane = threadIdx.x & 31;
+  int s = b + blockIdx.x * kWarpsPerBlock + (threadIdx.x >> 5);
+  if (s >= e) return;
+  int p = a.targets[s];
+  uint64_t inc = ein[s];
+  if (only_layer >= 0 && a.layer[p] != only_layer) {
+    if (lane == 0) eout[s] = inc;
+    return;
+  }
+  int px, py, pt;
+  decode(a.g, p, px, py, pt);
+  int q0 = e_q(inc);
+  int q0x, q0y, q0t;
+  decode(a.g, q0, q0x, q0y, q0t);
+  int q = -1;
+  if (lane < rad.M) {  // candidate i = lane + 1
+    uint4 u = draw((uint32_t)p, (uint32_t)pm_iter, a.level, kStreamRS, lane + 1, oc, seed);
+    double R = rad.R[lane];
+    int ox = (int)floor(__dmul_rn(R, __dmul_rn((double)u.x - 2147483648.0, 4.656612873077392578125e-10)));
+    int oy = (int)floor(__dmul_rn(R, __dmul_rn((double)u.y - 2147483648.0, 4.656612873077392578125e-10)));
+    int ot = (int)floor(__dmul_rn(R, __dmul_rn((double)u.z - 2147483648.0, 4.656612873077392578125e-10)));
+    int qx = q0x + ox, qy = q0y + oy, qt = q0t + ot;
+    if (is_source(a.g, a.flags, qx, qy, qt)) q = lin(a.g, qx, qy, qt);
+  }
+  bool ok = q >= 0 && q != q0;
+  for (int j = 0; j < rad.M; ++j) {  // duplicates of an earlier valid candidate
+    int qj = __shfl_sync(kFull, q, j);
+    if (j < lane && qj == q) ok = false;
+  }
+  unsigned mask = __ballot_sync(kFull, ok);
+  uint32_t bestD = e_D(inc);
+  int bestq = q0;
+  if (mask) {
+    PatchLanes L;
+    init_lanes(L, a.g, lane);
+    TargetPatch tp;
+    load_target(tp, L, a.g, a.vox, a.layer, kb, p, px, py, pt);
+    eval_candidates(tp, L, a.vox, lambda, mask, q, bestD, bestq);
+  }
+  if (lane == 0) {
+    eout[s] = pack_e(bestD, bestq);
+    flush_count(counter, __popc(mask));
+  }
+}
+
+// ------------------------------------------------------------------ a13: brute force (CUDA cores)
+// One block of 8 warps per target; warp w scans sources i = w, w+8, ... in increasing order and
+// keeps its first minimum; the block then takes the lexicographic min of (D, i).
+__global__ void __launch_bounds__(256) k_brute_force(LevelArgs a, uint64_t* __restrict__ ee,
+                                                     uint8_t* __restrict__ en, int lambda, int32_t b,
+                                                     int32_t e) {
+  int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
+  int s = b + blockIdx.x;
+  if (s >= e) return;
+  int p = a.targets[s];
+  PatchLanes L;
+  init_lanes(L, a.g, lane);
+  int px, py, pt;
+  decode(a.g, p, px, py, pt);
+  TargetPatch tp;
+  load_target(tp, L, a.g, a.vox, a.layer, -1, p, px, py, pt);
+  uint64_t best = ~0ull;  // (D << 32) | i
+  int i = w;
+  for (; i + kWarpsPerBlock < a.n_sources; i += 2 * kWarpsPerBlock) {
+    uint32_t D0, D1;
+    warp_ssd2(tp, L, a.vox, a.sources[i], a.sources[i + kWarpsPerBlock], lambda, D0, D1);
+    uint64_t k0 = ((uint64_t)D0 << 32) | (uint32_t)i;
+    uint64_t k1 = ((uint64_t)D1 << 32) | (uint32_t)(i + kWarpsPerBlock);
+    best = min(best, min(k0, k1));
+  }
+  for (; i < a.n_sources; i += kWarpsPerBlock) {
+    uint32_t D0 = warp_ssd(tp, L, a.vox, a.sources[i], lambda);
+    best = min(best, ((uint64_t)D0 << 32) | (uint32_t)i);
+  }
+  __shared__ unsigned long long red[kWarpsPerBlock];
+  if (lane == 0) red[w] = best;
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    uint64_t m = red[0];
+    for (int k = 1; k < kWarpsPerBlock; ++k) m = min(m, (uint64_t)red[k]);
+    uint32_t n = 0;
+    (void)n;
+    ee[s] = pack_e((uint32_t)(m >> 32), a.sources[(uint32_t)m]);
+  }
+  uint32_t n = __reduce_add_sync(kFull, (uint32_t)__popc(tp.mask));
+  if (threadIdx.x == 0) en[s] = (uint8_t)n;
+}
+
+// ------------------------------------------------------------------ test hooks
+__global__ void k_patch_ssd(LevelArgs a, const int32_t* __restrict__ P, const int32_t* __restrict__ Q,
+                            int64_t n, int lambda, int kb, uint32_t* __restrict__ D,
+                            uint8_t* __restrict__ cnt) {
+  int lane = threadIdx.x & 31;
+  int64_t i = (int64_t)blockIdx.x * kWarpsPerBlock + (threadIdx.x >> 5);
+  if (i >= n) return;
+  PatchLanes L;
+  init_lanes(L, a.g, lane);
+  int p = P[i];
+  int px, py, pt;
+  decode(a.g, p, px, py, pt);
+  TargetPatch tp;
+  load_target(tp, L, a.g, a.vox, a.layer, kb, p, px, py, pt);
+  uint32_t d = warp_ssd(tp, L, a.vox, Q[i], lambda);
+  uint32_t c = __reduce_add_sync(kFull, (uint32_t)__popc(tp.mask));
+  if (lane == 0) {
+    D[i] = d;
+    cnt[i] = (uint8_t)c;
+  }
+}
+
+__global__ void k_philox(const uint4* __restrict__ ctr, int64_t n, uint64_t seed,
+                         uint4* __restrict__ out) {
+  int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (i < n) out[i] = philox(ctr[i], (uint32_t)seed, (uint32_t)(seed >> 32));
+}
+
+static vinp_status check_nnf_args(const vinp_level* lv, const char* who, int32_t b, int32_t e,
+                                  const vinp_params* prm) {
+  vinp_status st = check_level(lv, who);
+  if (st) return st;
+  if (!prm) { set_error("%s: null params", who); return VINP_E_INVALID; }
+  if (prm->lambda < 0 || prm->lambda > 126) {
+    set_error("%s: lambda %d outside [0,126]", who, prm->lambda);
+    return VINP_E_UNSUPPORTED;
+  }
+  if (b < 0 || e > lv->n_targets || b > e) {
+    set_error("%s: slot range [%d,%d) outside [0,%d)", who, b, e, lv->n_targets);
+    return VINP_E_INVALID;
+  }
+  if (!lv->targets || !lv->slot) { set_error("%s: level lists missing", who); return VINP_E_INVALID; }
+  return VINP_OK;
+}
+
+static Radii make_radii(const vinp_level* lv, const vinp_params* prm) {
+  Radii r{};
+  int rmax = prm->rmax > 0 ? prm->rmax : std::max(lv->W, std::max(lv->H, lv->T));
+  double R = (double)rmax;
+  r.M = 0;
+  for (int i = 1; i <= 31; ++i) {
+    R = R * prm->rho;
+    if (!(R >= 1.0)) break;
+    r.R[r.M++] = R;
+  }
+  return r;
+}
+
+}  // namespace vinp
+
+using namespace vinp;
+
+extern "C" {
+
+vinp_status vinp_nnf_init_random(const vinp_level* lv, vinp_nnf* nnf, const vinp_params* prm,
+                                 uint32_t outer_code, int32_t b, int32_t e, void* stream) {
+  vinp_status st = check_nnf_args(lv, "vinp_nnf_init_random", b, e, prm);
+  if (st) return st;
+  VINP_REQUIRE(nnf && nnf->e && nnf->n, "vinp_nnf_init_random: null nnf");
+  if (lv->n_sources <= 0) {
+    set_error("vinp_nnf_init_random: D~ is empty at level %d", lv->level);
+    return VINP_E_NO_SOURCE;
+  }
+  if (e > b) {
+    k_init_random<<<nblk(e - b, 256), 256, 0, S(stream)>>>(args_of(lv), nnf->e, nnf->n, prm->seed,
+                                                           outer_code, b, e);
+    count_launch();
+  }
+  return check_launch("vinp_nnf_init_random");
+}
+
+vinp_status vinp_nnf_upsample(const vinp_level* coarse, const vinp_nnf* cn, const vinp_level* fine,
+                              vinp_nnf* fn, const vinp_params* prm, int32_t b, int32_t e,
+                              void* stream) {
+  vinp_status st = check_nnf_args(fine, "vinp_nnf_upsample", b, e, prm);
+  if (st) return st;
+  st = check_level(coarse, "vinp_nnf_upsample(coarse)");
+  if (st) return st;
+  VINP_REQUIRE(cn && cn->e && fn && fn->e && fn->n && coarse->slot, "vinp_nnf_upsample: null nnf");
+  VINP_REQUIRE(coarse->T == fine->T && coarse->W == (fine->W + 1) / 2 && coarse->H == (fine->H + 1) / 2,
+               "vinp_nnf_upsample: coarse dims must be ceil(fine/2)");
+  if (fine->n_sources <= 0) {
+    set_error("vinp_nnf_upsample: D~ is empty at level %d", fine->level);
+    return VINP_E_NO_SOURCE;
+  }
+  if (e > b) {
+    k_upsample<<<nblk(e - b, 256), 256, 0, S(stream)>>>(args_of(coarse), cn->e, args_of(fine),
+                                                        fn->e, fn->n, prm->seed, b, e);
+    count_launch();
+  }
+  return check_launch("vinp_nnf_upsample");
+}
+
+vinp_status vinp_nnf_evaluate(const vinp_level* lv, vinp_nnf* nnf, const vinp_params* prm, int kb,
+                              int only_layer, int32_t b, int32_t e, unsigned long long* counter,
+                              void* stream) {
+  vinp_status st = check_nnf_args(lv, "vinp_nnf_evaluate", b, e, prm);
+  if (st) return st;
+  VINP_REQUIRE(nnf && nnf->e && nnf->n, "vinp_nnf_evaluate: null nnf");
+  VINP_REQUIRE((kb < 0 && only_layer < 0) || lv->layer, "vinp_nnf_evaluate: layer map required");
+  if (e > b) {
+    k_evaluate<<<nblk(e - b, kWarpsPerBlock), 32 * kWarpsPerBlock, 0, S(stream)>>>(
+        args_of(lv), nnf->e, nnf->n, prm->lambda, kb, only_layer, b, e, counter);
+    count_launch();
+  }
+  return check_launch("vinp_nnf_evaluate");
+}
+
+vinp_status vinp_propagate(const vinp_level* lv, const vinp_nnf* in, vinp_nnf* out,
+                           const vinp_params* prm, int step, int sign, int kb, int only_layer,
+                           int32_t b, int32_t e, unsigned long long* counter, void* stream) {
+  vinp_status st = check_nnf_args(lv, "vinp_propagate", b, e, prm);
+  if (st) return st;
+  VINP_REQUIRE(in && in->e && out && out->e && in->e != out->e, "vinp_propagate: need two buffers");
+  VINP_REQUIRE(step >= 1 && (sign == 1 || sign == -1), "vinp_propagate: bad step/sign");
+  VINP_REQUIRE((kb < 0 && only_layer < 0) || lv->layer, "vinp_propagate: layer map required");
+  if (e > b) {
+    k_propagate<<<nblk(e - b, kWarpsPerBlock), 32 * kWarpsPerBlock, 0, S(stream)>>>(
+        args_of(lv), in->e, out->e, prm->lambda, step, sign, kb, only_layer, b, e, counter);
+    count_launch();
+  }
+  return check_launch("vinp_propagate");
+}
+
+vinp_status vinp_random_search(const vinp_level* lv, const vinp_nnf* in, vinp_nnf* out,
+                               const vinp_params* prm, uint32_t outer_code, int pm_iter, int kb,
+                               int only_layer, int32_t b, int32_t e, unsigned long long* counter,
+                               void* stream) {
+  vinp_status st = check_nnf_args(lv, "vinp_random_search", b, e, prm);
+  if (st) return st;
+  VINP_REQUIRE(in && in->e && out && out->e && in->e != out->e, "vinp_random_search: need two buffers");
+  VINP_REQUIRE(prm->rho > 0 && prm->rho < 1, "vinp_random_search: rho must lie in (0,1)");
+  VINP_REQUIRE((kb < 0 && only_layer < 0) || lv->layer, "vinp_random_search: layer map required");
+  Radii r = make_radii(lv, prm);
+  if (e > b) {
+    k_random_search<<<nblk(e - b, kWarpsPerBlock), 32 * kWarpsPerBlock, 0, S(stream)>>>(
+        args_of(lv), in->e, out->e, prm->lambda, r, prm->seed, outer_code, pm_iter, kb, only_layer,
+        b, e, counter);
+    count_launch();
+  }
+  return check_launch("vinp_random_search");
+}
+
+vinp_status vinp_ann_search(const vinp_level* lv, vinp_nnf* a, vinp_nnf* b, const vinp_params* prm,
+                            uint32_t outer_code, int K, const int32_t* steps, int n_steps, int kb,
+                            int only_layer, unsigned long long* counter, void* stream) {
+  VINP_REQUIRE(a && b && steps && n_steps >= 0 && n_steps <= 16 && K >= 0, "vinp_ann_search: bad args");
+  vinp_status st = vinp_nnf_evaluate(lv, a, prm, kb, only_layer, 0, lv->n_targets, counter, stream);
+  if (st) return st;
+  vinp_nnf* cur = a;
+  vinp_nnf* nxt = b;
+  for (int k = 1; k <= K; ++k) {
+    int sign = (k % 2 == 1) ? 1 : -1;
+    for (int i = 0; i < n_steps; ++i) {
+      st = vinp_propagate(lv, cur, nxt, prm, steps[i], sign, kb, only_layer, 0, lv->n_targets,
+                          counter, stream);
+      if (st) return st;
+      std::swap(cur, nxt);
+    }
+    st = vinp_random_search(lv, cur, nxt, prm, outer_code, k, kb, only_layer, 0, lv->n_targets,
+                            counter, stream);
+    if (st) return st;
+    std::swap(cur, nxt);
+  }
+  if (cur != a && lv->n_targets > 0) {
+    if (cudaMemcpyAsync(a->e, cur->e, sizeof(uint64_t) * lv->n_targets, cudaMemcpyDeviceToDevice,
+                        S(stream)) != cudaSuccess)
+      return check_launch("vinp_ann_search(copy)");
+  }
+  return VINP_OK;
+}
+
+size_t vinp_brute_force_ws_bytes(const vinp_level* lv) { return lv ? 256 : 0; }
+
+vinp_status vinp_brute_force(const vinp_level* lv, vinp_nnf* out, const vinp_params* prm, int32_t b,
+                             int32_t e, void* ws, size_t ws_bytes, void* stream) {
+  vinp_status st = check_nnf_args(lv, "vinp_brute_force", b, e, prm);
+  if (st) return st;
+  VINP_REQUIRE(out && out->e && out->n, "vinp_brute_force: null nnf");
+  (void)ws;
+  (void)ws_bytes;
+  if (lv->n_sources <= 0) {
+    set_error("vinp_brute_force: D~ is empty");
+    return VINP_E_NO_SOURCE;
+  }
+  if (e > b) {
+    k_brute_force<<<e - b, 32 * kWarpsPerBlock, 0, S(stream)>>>(args_of(lv), out->e, out->n,
+                                                                 prm->lambda, b, e);
+    count_launch();
+  }
+  return check_launch("vinp_brute_force");
+}
+
+vinp_status vinp_patch_ssd(const vinp_level* lv, const int32_t* p, const int32_t* q, int64_t n,
+                           const vinp_params* prm, int kb, uint32_t* D, uint8_t* cnt, void* stream) {
+  vinp_status st = check_level(lv, "vinp_patch_ssd");
+  if (st) return st;
+  VINP_REQUIRE(p && q && D && cnt && prm && n >= 0, "vinp_patch_ssd: bad args");
+  VINP_REQUIRE(kb < 0 || lv->layer, "vinp_patch_ssd: layer map required");
+  if (n > 0) {
+    k_patch_ssd<<<nblk(n, kWarpsPerBlock), 32 * kWarpsPerBlock, 0, S(stream)>>>(
+        args_of(lv), p, q, n, prm->lambda, kb, D, cnt);
+    count_launch();
+  }
+  return check_launch("vinp_patch_ssd");
+}
+
+vinp_status vinp_philox(const uint32_t* ctr, int64_t n, uint64_t seed, uint32_t* out, void* stream) {
+  VINP_REQUIRE(ctr && out && n >= 0, "vinp_philox: bad args");
+  if (n > 0) {
+    k_philox<<<nblk(n, 256), 256, 0, S(stream)>>>((const uint4*)ctr, n, seed, (uint4*)out);
+    count_launch();
+  }
+  return check_launch("vinp_philox");
+}
+
+}  // extern "C"

@@ -1,0 +1,196 @@
+// common.cuh — shared device helpers of libvinp (sm_100a).  Not shared with oracle/.
+#pragma once
+#include <cuda_runtime.h>
+#include <stdint.h>
+
+#include <cstdarg>
+#include <cstdio>
+
+#include "vinp.h"
+
+namespace vinp {
+
+constexpr int kPatch = 125;   // 5x5x5
+constexpr int kR = 2;         // patch radius
+constexpr unsigned kFull = 0xffffffffu;
+
+// ---------------------------------------------------------------- host-side error plumbing
+void set_error(const char* fmt, ...);
+vinp_status check_launch(const char* what);
+void count_launch(int n = 1);
+
+#define VINP_REQUIRE(cond, ...)          \
+  do {                                   \
+    if (!(cond)) {                       \
+      ::vinp::set_error(__VA_ARGS__);    \
+      return VINP_E_INVALID;             \
+    }                                    \
+  } while (0)
+
+inline cudaStream_t S(void* s) { return reinterpret_cast<cudaStream_t>(s); }
+
+inline vinp_status check_level(const vinp_level* lv, const char* who) {
+  if (!lv || !lv->vox || !lv->flags) {
+    set_error("%s: null level or buffers", who);
+    return VINP_E_INVALID;
+  }
+  if (lv->W < 1 || lv->H < 1 || lv->T < 1 || (int64_t)lv->W * lv->H * lv->T >= (1ll << 31)) {
+    set_error("%s: bad dims %dx%dx%d", who, lv->W, lv->H, lv->T);
+    return VINP_E_UNSUPPORTED;
+  }
+  return VINP_OK;
+}
+
+// ---------------------------------------------------------------- geometry
+struct Geo {
+  int W, H, T;
+  int HW;
+};
+inline Geo geo_of(const vinp_level* lv) { return Geo{lv->W, lv->H, lv->T, lv->W * lv->H}; }
+
+__device__ __forceinline__ void decode(const Geo& g, int p, int& x, int& y, int& t) {
+  t = p / g.HW;
+  int r = p - t * g.HW;
+  y = r / g.W;
+  x = r - y * g.W;
+}
+
+__device__ __forceinline__ bool inside(const Geo& g, int x, int y, int t) {
+  return (unsigned)x < (unsigned)g.W && (unsigned)y < (unsigned)g.H && (unsigned)t < (unsigned)g.T;
+}
+
+// patch offset index v in [0,125): dx = v%5-2, dy = (v/5)%5-2, dt = v/25-2 (t-major order)
+__device__ __forceinline__ void voff(int v, int& dx, int& dy, int& dt) {
+  dt = v / 25 - 2;
+  int r = v % 25;
+  dy = r / 5 - 2;
+  dx = r % 5 - 2;
+}
+
+// ---------------------------------------------------------------- Philox4x32-10
+__device__ __forceinline__ uint4 philox(uint4 c, uint32_t k0, uint32_t k1) {
+#pragma unroll
+  for (int r = 0; r < 10; ++r) {
+    uint32_t hi0 = __umulhi(0xD2511F53u, c.x), lo0 = 0xD2511F53u * c.x;
+    uint32_t hi1 = __umulhi(0xCD9E8D57u, c.z), lo1 = 0xCD9E8D57u * c.z;
+    c = make_uint4(hi1 ^ c.y ^ k0, lo1, hi0 ^ c.w ^ k1, lo0);
+    k0 += 0x9E3779B9u;
+    k1 += 0xBB67AE85u;
+  }
+  return c;
+}
+enum { kStreamInit = 1, kStreamRS = 2, kStreamRepair = 3 };
+__device__ __forceinline__ uint4 draw(uint32_t p, uint32_t k, int level, int stream, int i,
+                                      uint32_t oc, uint64_t seed) {
+  return philox(make_uint4(p, k, ((uint32_t)level << 24) | ((uint32_t)stream << 16) | (uint32_t)i, oc),
+                (uint32_t)seed, (uint32_t)(seed >> 32));
+}
+
+// ---------------------------------------------------------------- NNF entry packing
+__device__ __forceinline__ uint64_t pack_e(uint32_t D, int32_t q) {
+  return ((uint64_t)D << 32) | (uint32_t)q;
+}
+__device__ __forceinline__ uint32_t e_D(uint64_t e) { return (uint32_t)(e >> 32); }
+__device__ __forceinline__ int32_t e_q(uint64_t e) { return (int32_t)(uint32_t)e; }
+
+// ---------------------------------------------------------------- warp-per-target patch state
+// Lane l owns patch voxels v = l + 32 i, i = 0..3 (v < 125).  off[i] is the linear offset of v,
+// identical for the target patch around p and the source patch around q (same geometry).
+struct PatchLanes {
+  int off[4];
+  int dx[4], dy[4], dt[4];
+  bool live[4];  // v < 125
+};
+__device__ __forceinline__ void init_lanes(PatchLanes& L, const Geo& g, int lane) {
+#pragma unroll
+  for (int i = 0; i < 4; ++i) {
+    int v = lane + 32 * i;
+    L.live[i] = v < kPatch;
+    int dx, dy, dt;
+    voff(L.live[i] ? v : 62, dx, dy, dt);
+    L.dx[i] = dx; L.dy[i] = dy; L.dt[i] = dt;
+    L.off[i] = dt * g.HW + dy * g.W + dx;
+  }
+}
+
+struct TargetPatch {
+  uint32_t c[4], t[4];  // colour / texture words of the target voxels
+  unsigned mask;        // bit i: voxel i in Omega and in K
+};
+
+// K = Omega (kb < 0) or {r : layer(r) < kb}
+__device__ __forceinline__ void load_target(TargetPatch& tp, const PatchLanes& L, const Geo& g,
+                                            const uint64_t* __restrict__ vox,
+                                            const uint8_t* __restrict__ layer, int kb, int p,
+                                            int px, int py, int pt) {
+  tp.mask = 0;
+#pragma unroll
+  for (int i = 0; i < 4; ++i) {
+    tp.c[i] = 0; tp.t[i] = 0;
+    if (L.live[i] && inside(g, px + L.dx[i], py + L.dy[i], pt + L.dt[i])) {
+      int r = p + L.off[i];
+      bool known = kb < 0 || layer[r] < kb;
+      if (known) {
+        uint64_t w = __ldg(reinterpret_cast<const unsigned long long*>(vox) + r);
+        tp.c[i] = (uint32_t)w;
+        tp.t[i] = (uint32_t)(w >> 32);
+        tp.mask |= 1u << i;
+      }
+    }
+  }
+}
+
+__device__ __forceinline__ uint32_t voxel_cost(uint32_t tc, uint32_t tt, uint64_t s, int lambda) {
+  uint32_t dc = __vabsdiffu4(tc, (uint32_t)s);
+  uint32_t dtx = __vabsdiffu4(tt, (uint32_t)(s >> 32));
+  uint32_t cc = __dp4a(dc, dc, 0u);
+  uint32_t tc2 = __dp4a(dtx, dtx, 0u);
+  return 4u * cc + (uint32_t)lambda * tc2;
+}
+
+// D(p, q) for the whole warp (all lanes return the same value).  q must be in D~.
+__device__ __forceinline__ uint32_t warp_ssd(const TargetPatch& tp, const PatchLanes& L,
+                                             const uint64_t* __restrict__ vox, int q, int lambda) {
+  uint32_t acc = 0;
+  const unsigned long long* v = reinterpret_cast<const unsigned long long*>(vox);
+#pragma unroll
+  for (int i = 0; i < 4; ++i) {
+    if (tp.mask & (1u << i)) {
+      uint64_t s = __ldg(v + q + L.off[i]);
+      acc += voxel_cost(tp.c[i], tp.t[i], s, lambda);
+    }
+  }
+  return __reduce_add_sync(kFull, acc);
+}
+
+// Two candidates at once (more loads in flight per warp).
+__device__ __forceinline__ void warp_ssd2(const TargetPatch& tp, const PatchLanes& L,
+                                          const uint64_t* __restrict__ vox, int q0, int q1,
+                                          int lambda, uint32_t& D0, uint32_t& D1) {
+  uint32_t a0 = 0, a1 = 0;
+  const unsigned long long* v = reinterpret_cast<const unsigned long long*>(vox);
+  uint64_t s0[4], s1[4];
+#pragma unroll
+  for (int i = 0; i < 4; ++i) {
+    bool m = tp.mask & (1u << i);
+    s0[i] = m ? __ldg(v + q0 + L.off[i]) : 0ull;
+    s1[i] = m ? __ldg(v + q1 + L.off[i]) : 0ull;
+  }
+#pragma unroll
+  for (int i = 0; i < 4; ++i) {
+    if (tp.mask & (1u << i)) {
+      a0 += voxel_cost(tp.c[i], tp.t[i], s0[i], lambda);
+      a1 += voxel_cost(tp.c[i], tp.t[i], s1[i], lambda);
+    }
+  }
+  D0 = __reduce_add_sync(kFull, a0);
+  D1 = __reduce_add_sync(kFull, a1);
+}
+
+__device__ __forceinline__ bool is_source(const Geo& g, const uint8_t* __restrict__ flags, int x,
+                                          int y, int t) {
+  if (!inside(g, x, y, t)) return false;
+  return (__ldg(flags + (t * g.HW + y * g.W + x)) & 2) != 0;
+}
+
+}  // namespace vinp

@@ -1,0 +1,285 @@
+// reconstruct.cu — patch-vote reconstruction (a9/a10: Eqs. 4-6, 11, 13), commit of the u8
+// working copy, the stopping-rule change (a11) and the Eq. 1 energy diagnostic.
+//
+// One warp per hole pixel p, gathering its <= 125 contributors q in N_p (lane l owns q = p + off_v
+// for v = l + 32i): each lane reads slot[q], the NNF entry of q and the proposed value
+// u(p + phi(q)) = vox[src_q - off_v] — a per-target-pixel gather, no atomics (north_star (c)).
+// sigma_p^2 is selected exactly as the ceil(0.75 m)-th smallest key d^2 = D/n (the key is the
+// fp64 D/n, which orders distinct rationals with n <= 125 exactly) by a 63-step bitwise
+// rank search with REDUX.SUM per step.  Weights are round(exp(-a) 2^36) so that the sums are
+// exact int64 and do not depend on the reduction order (R26).
+#include "common.cuh"
+
+namespace vinp {
+
+static inline int nblk(int64_t n, int t) { return (int)((n + t - 1) / t); }
+constexpr int kWPB = 8;
+
+__device__ __forceinline__ uint64_t shfl_xor64(uint64_t v, int m) {
+  uint32_t lo = __shfl_xor_sync(kFull, (uint32_t)v, m), hi = __shfl_xor_sync(kFull, (uint32_t)(v >> 32), m);
+  return ((uint64_t)hi << 32) | lo;
+}
+__device__ __forceinline__ int64_t warp_sum64(int64_t v) {
+#pragma unroll
+  for (int m = 16; m; m >>= 1) v += (int64_t)shfl_xor64((uint64_t)v, m);
+  return v;
+}
+__device__ __forceinline__ uint64_t warp_min64(uint64_t v) {
+#pragma unroll
+  for (int m = 16; m; m >>= 1) v = min(v, shfl_xor64(v, m));
+  return v;
+}
+
+__device__ __forceinline__ uint8_t round_u8(float x) {
+  return (uint8_t)floor((double)x + 0.5);
+}
+
+struct ReconArgs {
+  Geo g;
+  uint64_t* vox;
+  const uint8_t* layer;
+  const int32_t* slot;
+  const int32_t* holes;
+  const uint64_t* e;
+  const uint8_t* n;
+};
+
+__global__ void __launch_bounds__(256) k_reconstruct(ReconArgs a, int mode, int layer_j, int32_t hb,
+                                                     int32_t he, float* __restrict__ out_rgb,
+                                                     float* __restrict__ out_tex, int commit) {
+  int lane = threadIdx.x & 31;
+  int h = hb + blockIdx.x * kWPB + (threadIdx.x >> 5);
+  if (h >= he) return;
+  int p = a.holes[h];
+  if (layer_j >= 0 && a.layer[p] != layer_j) return;
+  int px, py, pt;
+  decode(a.g, p, px, py, pt);
+  uint64_t key[4];
+  uint32_t Dq[4], nq[4];
+  uint64_t val[4];
+  unsigned valid = 0;
+#pragma unroll
+  for (int i = 0; i < 4; ++i) {
+    int v = lane + 32 * i;
+    key[i] = ~0ull;
+    Dq[i] = 0; nq[i] = 1; val[i] = 0;
+    if (v < kPatch) {
+      int dx, dy, dt;
+      voff(v, dx, dy, dt);
+      if (inside(a.g, px + dx, py + dy, pt + dt)) {
+        int off = dt * a.g.HW + dy * a.g.W + dx;
+        int q = p + off;
+        if (layer_j < 0 || a.layer[q] < layer_j) {
+          int s = __ldg(a.slot + q);
+          if (s >= 0) {
+            uint32_t n = __ldg(a.n + s);
+            if (mode == VINP_UNWEIGHTED || n > 0) {
+              uint64_t e = __ldg(reinterpret_cast<const unsigned long long*>(a.e) + s);
+              Dq[i] = e_D(e);
+              nq[i] = n;
+              val[i] = __ldg(reinterpret_cast<const unsigned long long*>(a.vox) + (e_q(e) - off));
+              if (n > 0) key[i] = (uint64_t)__double_as_longlong((double)Dq[i] / (double)n);
+              valid |= 1u << i;
+            }
+          }
+        }
+      }
+    }
+  }
+  uint32_t m = __reduce_add_sync(kFull, (uint32_t)__popc(valid));
+  if (m == 0) return;
+  int64_t w[4];
+  if (mode == VINP_BEST_PATCH) {
+    uint64_t kmin = min(min(key[0], key[1]), min(key[2], key[3]));
+    kmin = warp_min64(kmin);
+    uint32_t vbest = 0xffffffffu;
+#pragma unroll
+    for (int i = 3; i >= 0; --i)
+      if ((valid >> i & 1) && key[i] == kmin) vbest = lane + 32 * i;
+    vbest = __reduce_min_sync(kFull, vbest);
+#pragma unroll
+    for (int i = 0; i < 4; ++i) w[i] = ((uint32_t)(lane + 32 * i) == vbest) ? 1 : 0;
+  } else if (mode == VINP_UNWEIGHTED) {
+#pragma unroll
+    for (int i = 0; i < 4; ++i) w[i] = (valid >> i) & 1;
+  } else {
+    // sigma^2 key: the r-th smallest key, r = ceil(0.75 m) (nearest rank, R10)
+    uint32_t r = (3 * m + 3) / 4;
+    uint64_t ans = 0;
+    for (int bit = 62; bit >= 0; --bit) {
+      uint64_t T = ans | ((1ull << bit) - 1);
+      uint32_t c = 0;
+#pragma unroll
+      for (int i = 0; i < 4; ++i) c += (valid >> i & 1) && key[i] <= T;
+      c = __reduce_add_sync(kFull, c);
+      if (c < r) ans |= 1ull << bit;
+    }
+    // a representative (D_s, n_s) with key == ans
+    int own = -1;
+#pragma unroll
+    for (int i = 3; i >= 0; --i)
+      if ((valid >> i & 1) && key[i] == ans) own = i;
+    unsigned bal = __ballot_sync(kFull, own >= 0);
+    int src = __ffs(bal) - 1;
+    uint32_t myD = 0, myn = 1;
+#pragma unroll
+    for (int i = 0; i < 4; ++i)
+      if (i == own) { myD = Dq[i]; myn = nq[i]; }
+    uint32_t Ds = __shfl_sync(kFull, myD, src), ns = __shfl_sync(kFull, myn, src);
+#pragma unroll
+    for (int i = 0; i < 4; ++i) {
+      if (!(valid >> i & 1)) { w[i] = 0; continue; }
+      if (Ds == 0) {
+        w[i] = Dq[i] == 0;
+      } else {
+        double an = (double)((uint64_t)Dq[i] * ns);
+        double ad = (double)(2ull * nq[i] * Ds);
+        double aa = __ddiv_rn(an, ad);
+        w[i] = __double2ll_rn(__dmul_rn(exp(-aa), 68719476736.0));
+      }
+    }
+  }
+  int64_t S = 0, N[5] = {0, 0, 0, 0, 0};
+#pragma unroll
+  for (int i = 0; i < 4; ++i) {
+    if (!w[i]) continue;
+    uint64_t x = val[i];
+    S += w[i];
+    N[0] += w[i] * (int64_t)(x & 255);
+    N[1] += w[i] * (int64_t)((x >> 8) & 255);
+    N[2] += w[i] * (int64_t)((x >> 16) & 255);
+    N[3] += w[i] * (int64_t)((x >> 32) & 255);
+    N[4] += w[i] * (int64_t)((x >> 40) & 255);
+  }
+  S = warp_sum64(S);
+#pragma unroll
+  for (int c = 0; c < 5; ++c) N[c] = warp_sum64(N[c]);
+  if (lane < 5) {
+    int64_t Nc = lane == 0 ? N[0] : lane == 1 ? N[1] : lane == 2 ? N[2] : lane == 3 ? N[3] : N[4];
+    float o = (float)__ddiv_rn((double)Nc, (double)S);
+    if (lane < 3) out_rgb[3 * (int64_t)h + lane] = o;
+    else out_tex[2 * (int64_t)h + lane - 3] = o;
+    if (commit) {
+      uint32_t b = round_u8(o);
+      uint32_t sh = lane < 3 ? 8 * lane : 32 + 8 * (lane - 3);
+      uint64_t part = (uint64_t)b << sh;
+      // combine the five bytes in lane 0
+      uint32_t lo = (uint32_t)part, hi = (uint32_t)(part >> 32);
+      lo |= __shfl_down_sync(0x1f, lo, 1) | __shfl_down_sync(0x1f, lo, 2);
+      hi |= __shfl_down_sync(0x1f, hi, 3) | __shfl_down_sync(0x1f, hi, 4);
+      if (lane == 0) a.vox[p] = ((uint64_t)hi << 32) | lo;
+    }
+  }
+}
+
+__global__ void k_commit(Geo g, uint64_t* __restrict__ vox, const uint8_t* __restrict__ layer,
+                         const int32_t* __restrict__ holes, const float* __restrict__ rgb,
+                         const float* __restrict__ tex, int layer_j, int32_t hb, int32_t he) {
+  int h = hb + blockIdx.x * blockDim.x + threadIdx.x;
+  if (h >= he) return;
+  int p = holes[h];
+  if (layer_j >= 0 && layer[p] != layer_j) return;
+  uint64_t w = (uint64_t)round_u8(rgb[3 * (int64_t)h]) | ((uint64_t)round_u8(rgb[3 * (int64_t)h + 1]) << 8) |
+               ((uint64_t)round_u8(rgb[3 * (int64_t)h + 2]) << 16) |
+               ((uint64_t)round_u8(tex[2 * (int64_t)h]) << 32) |
+               ((uint64_t)round_u8(tex[2 * (int64_t)h + 1]) << 40);
+  vox[p] = w;
+}
+
+__global__ void k_change_l1(const float* __restrict__ a, const float* __restrict__ b, int64_t n,
+                            unsigned long long* __restrict__ out) {
+  int64_t acc = 0;
+  for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n;
+       i += (int64_t)gridDim.x * blockDim.x)
+    acc += __double2ll_rn(fabs((double)a[i] - (double)b[i]) * 1048576.0);
+  acc = warp_sum64(acc);
+  __shared__ long long sm[32];
+  int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
+  if (lane == 0) sm[w] = acc;
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    long long s = 0;
+    for (int k = 0; k < (int)(blockDim.x >> 5); ++k) s += sm[k];
+    if (s) atomicAdd(out, (unsigned long long)s);
+  }
+}
+
+// deterministic single-block sum of D/(4n) over H (diagnostic)
+__global__ void k_energy(const int32_t* __restrict__ holes, int32_t nh, const int32_t* __restrict__ slot,
+                         const uint64_t* __restrict__ e, const uint8_t* __restrict__ n,
+                         double* __restrict__ out) {
+  double acc = 0;
+  for (int h = threadIdx.x; h < nh; h += blockDim.x) {
+    int s = slot[holes[h]];
+    if (s >= 0 && n[s]) acc += (double)e_D(e[s]) / (4.0 * n[s]);
+  }
+  __shared__ double sm[1024];
+  sm[threadIdx.x] = acc;
+  __syncthreads();
+  for (int k = blockDim.x / 2; k; k >>= 1) {
+    if ((int)threadIdx.x < k) sm[threadIdx.x] += sm[threadIdx.x + k];
+    __syncthreads();
+  }
+  if (threadIdx.x == 0) *out = sm[0];
+}
+
+}  // namespace vinp
+
+using namespace vinp;
+
+extern "C" {
+
+vinp_status vinp_reconstruct(vinp_level* lv, const vinp_nnf* nnf, int mode, int layer_j, int32_t hb,
+                             int32_t he, float* out_rgb, float* out_tex, int commit, void* stream) {
+  vinp_status st = check_level(lv, "vinp_reconstruct");
+  if (st) return st;
+  VINP_REQUIRE(nnf && nnf->e && nnf->n && out_rgb && out_tex && lv->holes && lv->slot,
+               "vinp_reconstruct: null buffers");
+  VINP_REQUIRE(mode == VINP_WEIGHTED || mode == VINP_UNWEIGHTED || mode == VINP_BEST_PATCH,
+               "vinp_reconstruct: bad mode %d", mode);
+  VINP_REQUIRE(hb >= 0 && he <= lv->n_holes && hb <= he, "vinp_reconstruct: bad hole range");
+  VINP_REQUIRE(layer_j < 0 || lv->layer, "vinp_reconstruct: layer map required");
+  if (he > hb) {
+    ReconArgs a{geo_of(lv), lv->vox, lv->layer, lv->slot, lv->holes, nnf->e, nnf->n};
+    k_reconstruct<<<nblk(he - hb, kWPB), 32 * kWPB, 0, S(stream)>>>(a, mode, layer_j, hb, he, out_rgb,
+                                                                  out_tex, commit);
+    count_launch();
+  }
+  return check_launch("vinp_reconstruct");
+}
+
+vinp_status vinp_commit(vinp_level* lv, const float* out_rgb, const float* out_tex, int layer_j,
+                        int32_t hb, int32_t he, void* stream) {
+  vinp_status st = check_level(lv, "vinp_commit");
+  if (st) return st;
+  VINP_REQUIRE(out_rgb && out_tex && lv->holes, "vinp_commit: null buffers");
+  VINP_REQUIRE(hb >= 0 && he <= lv->n_holes && hb <= he, "vinp_commit: bad hole range");
+  VINP_REQUIRE(layer_j < 0 || lv->layer, "vinp_commit: layer map required");
+  if (he > hb) {
+    k_commit<<<nblk(he - hb, 256), 256, 0, S(stream)>>>(geo_of(lv), lv->vox, lv->layer, lv->holes,
+                                                        out_rgb, out_tex, layer_j, hb, he);
+    count_launch();
+  }
+  return check_launch("vinp_commit");
+}
+
+vinp_status vinp_change_l1(const float* a, const float* b, int64_t n, int64_t* out, void* stream) {
+  VINP_REQUIRE(a && b && out && n >= 0, "vinp_change_l1: bad args");
+  if (n > 0) {
+    int g = (int)std::min<int64_t>(nblk(n, 256), 148 * 8);
+    k_change_l1<<<g, 256, 0, S(stream)>>>(a, b, n, (unsigned long long*)out);
+    count_launch();
+  }
+  return check_launch("vinp_change_l1");
+}
+
+vinp_status vinp_energy(const vinp_level* lv, const vinp_nnf* nnf, double* out, void* stream) {
+  vinp_status st = check_level(lv, "vinp_energy");
+  if (st) return st;
+  VINP_REQUIRE(nnf && nnf->e && nnf->n && out && lv->holes && lv->slot, "vinp_energy: null buffers");
+  k_energy<<<1, 1024, 0, S(stream)>>>(lv->holes, lv->n_holes, lv->slot, nnf->e, nnf->n, out);
+  count_launch();
+  return check_launch("vinp_energy");
+}
+
+}  // extern "C"

@@ -1,0 +1,264 @@
+"""Alg. 4 driver over the libvinp C ABI, without AlignVideo/UnwarpVideo (NEXT #1).
+
+Host logic only: which kernel runs on which level, the onion-peel loop (Alg. 3), the stopping
+rule (R19) and, under torch.distributed, the target-slab partition and the exchanges between
+passes.  Every arithmetic step runs in libvinp's kernels.
+
+Multi-GPU: every rank holds the full pyramid; the sorted target list (and hole list) of a level is
+cut into W contiguous equal-count slabs; after every pass that a later pass reads, the NNF slabs
+are all-gathered; after reconstruction the fp32 hole values are all-gathered and committed on
+every rank; the change e is an exact int64 all-reduce.  Because every pass is a Jacobi pass whose
+candidates are drawn from counter-based Philox streams keyed on the voxel, the result is
+bit-identical for any number of ranks.  The onion peel (coarsest level only) runs replicated.
+"""
+from __future__ import annotations
+
+import time
+from dataclasses import dataclass, field
+from typing import List, Optional, Sequence
+
+import torch
+
+from . import vinp as V
+
+
+@dataclass
+class Config:
+    levels: int = 4
+    pm_iters: int = 10          # PatchMatch iterations per ANN search
+    fixed_outer: int = 0        # >0: exactly this many outer iterations per level (c1)
+    max_outer: int = 20
+    lam: int = 50
+    seed: int = 1
+    steps: Sequence[int] = (8, 4, 2, 1)  # jump-flood steps per PM iteration (R6)
+    rho: float = 0.5
+    tex_half: int = -1          # R15
+    onion: bool = True          # Alg. 3 initialisation at the coarsest level
+
+    def params(self) -> V.Params:
+        return V.Params(lam=self.lam, tex_half=self.tex_half, seed=self.seed, rho=self.rho)
+
+
+class Exchange:
+    """Slab partition + collectives.  World size 1: identity."""
+
+    def __init__(self, group=None):
+        import torch.distributed as dist
+        self.dist = dist if (dist.is_available() and dist.is_initialized()) else None
+        self.group = group
+        self.world = self.dist.get_world_size(group) if self.dist else 1
+        self.rank = self.dist.get_rank(group) if self.dist else 0
+
+    def padded(self, n: int) -> int:
+        return -(-max(n, 1) // self.world) * self.world
+
+    def slab(self, n: int):
+        c = self.padded(n) // self.world
+        return min(n, self.rank * c), min(n, (self.rank + 1) * c)
+
+    def gather(self, t: torch.Tensor, n: int):
+        """All-gather the rank slabs of the first padded(n) rows of t, in place."""
+        if self.world == 1:
+            return
+        c = self.padded(n) // self.world
+        mine = t[self.rank * c:(self.rank + 1) * c].clone()
+        self.dist.all_gather_into_tensor(t[:self.world * c], mine, group=self.group)
+
+    def allreduce_sum(self, t: torch.Tensor):
+        if self.world > 1:
+            self.dist.all_reduce(t, group=self.group)
+
+
+@dataclass
+class LevelState:
+    lv: V.Level
+    a: V.NNF
+    b: V.NNF
+    cur_rgb: torch.Tensor
+    cur_tex: torch.Tensor
+    prev_rgb: torch.Tensor
+    prev_tex: torch.Tensor
+    outer: int = 0
+    ms: float = 0.0
+    patch_updates: int = 0
+
+
+@dataclass
+class Stats:
+    levels: List[dict] = field(default_factory=list)
+    onion_layers: int = 0
+    setup_ms: float = 0.0
+    total_ms: float = 0.0
+
+    @property
+    def patch_updates(self):
+        return sum(l["patch_updates"] for l in self.levels)
+
+
+class Inpainter:
+    """Holds the pyramid of one video in HBM and runs Alg. 4 on it."""
+
+    def __init__(self, W: int, H: int, T: int, cfg: Config, device="cuda", exchange: Exchange = None):
+        self.W, self.H, self.T, self.cfg = W, H, T, cfg
+        self.device = torch.device(device)
+        self.ex = exchange or Exchange()
+        self.prm = cfg.params()
+        self.levels: List[V.Level] = []
+        w, h = W, H
+        for l in range(1, cfg.levels + 1):
+            self.levels.append(V.Level.alloc(w, h, T, l, self.device))
+            w, h = (w + 1) // 2, (h + 1) // 2
+        n1 = W * H * T
+        self.ws = torch.empty(max(V.texture_ws_bytes(self.levels[0]), V.sets_ws_bytes(self.levels[0])) + 256,
+                              dtype=torch.uint8, device=self.device)
+        self.counter = torch.zeros(1, dtype=torch.int64, device=self.device)
+        self.change = torch.zeros(1, dtype=torch.int64, device=self.device)
+        self.states: List[LevelState] = []
+        self.stats = Stats()
+        self.n_layers = 0
+
+    # ------------------------------------------------------------------ setup (a1-a3)
+    def load(self, rgb: torch.Tensor, mask: torch.Tensor):
+        """rgb u8 [T,H,W,3], mask u8 [T,H,W] (nonzero = occluded), on this device."""
+        assert rgb.shape == (self.T, self.H, self.W, 3) and mask.shape == (self.T, self.H, self.W)
+        rgb = rgb.contiguous()
+        mask = mask.contiguous()
+        V.build_pyramid(rgb, mask, self.levels)
+        V.texture_features(self.prm, self.levels, self.ws)
+        counts = V.build_sets(self.levels, self.ws)
+        for lv in self.levels:
+            if lv.n_sources == 0:
+                raise V.VinpError(f"D~ is empty at level {lv.level} (S:237)")
+            lv.alloc_lists()
+        V.build_lists(self.levels, self.ws)
+        self.states = []
+        for lv in self.levels:
+            npad = self.ex.padded(lv.n_targets)
+            hpad = self.ex.padded(lv.n_holes)
+            a = V.NNF.alloc(npad, self.device)
+            b = V.NNF.alloc(npad, self.device, n=a.n)
+            z = lambda k: torch.zeros((hpad, k), dtype=torch.float32, device=self.device)
+            self.states.append(LevelState(lv, a, b, z(3), z(2), z(3), z(2)))
+        top = self.levels[-1]
+        top.layer = torch.empty(top.N, dtype=torch.uint8, device=self.device)
+        self.n_layers = V.layers(top, self.ws)
+        self.stats.onion_layers = self.n_layers
+        return counts
+
+    # ------------------------------------------------------------------ ANN search (a5-a8)
+    def ann_search(self, st: LevelState, outer_code: int, kb=-1, only_layer=-1, replicated=False):
+        lv, prm, cfg = st.lv, self.prm, self.cfg
+        n = lv.n_targets
+        b, e = (0, n) if replicated else self.ex.slab(n)
+        gather = (lambda t: None) if replicated else (lambda t: self.ex.gather(t, n))
+        V.nnf_evaluate(lv, st.a, prm, kb, only_layer, b, e, self.counter)
+        gather(st.a.e)
+        gather(st.a.n)
+        for k in range(1, cfg.pm_iters + 1):
+            sign = 1 if k % 2 == 1 else -1
+            for s in cfg.steps:
+                V.propagate(lv, st.a, st.b, prm, s, sign, kb, only_layer, b, e, self.counter)
+                st.a, st.b = st.b, st.a
+                gather(st.a.e)
+            V.random_search(lv, st.a, st.b, prm, outer_code, k, kb, only_layer, b, e, self.counter)
+            st.a, st.b = st.b, st.a
+            gather(st.a.e)
+
+    def reconstruct(self, st: LevelState, mode: int, layer_j=-1, replicated=False):
+        lv = st.lv
+        n = lv.n_holes
+        hb, he = (0, n) if replicated else self.ex.slab(n)
+        V.reconstruct(lv, st.a, mode, st.cur_rgb, st.cur_tex, layer_j, hb, he, commit=True)
+        if not replicated and self.ex.world > 1:
+            self.ex.gather(st.cur_rgb, n)
+            self.ex.gather(st.cur_tex, n)
+            V.commit(lv, st.cur_rgb, st.cur_tex, layer_j, 0, n)
+
+    # ------------------------------------------------------------------ Alg. 3 onion peel
+    def onion_peel(self):
+        st = self.states[-1]
+        V.nnf_init_random(st.lv, st.a, self.prm, 0)  # phi^L <- Random
+        for j in range(0, self.n_layers + 1):
+            kb = max(j, 1)
+            self.ann_search(st, V.ONION | j, kb=kb, only_layer=j, replicated=True)
+            if j >= 1:
+                self.reconstruct(st, V.WEIGHTED, layer_j=j, replicated=True)
+
+    # ------------------------------------------------------------------ Alg. 4
+    def run(self, timing=True) -> Stats:
+        cfg = self.cfg
+        L = cfg.levels
+        ev = lambda: torch.cuda.Event(enable_timing=True)
+        self.stats.levels = [dict(level=l, outer=0, patch_updates=0, ms=0.0) for l in range(1, L + 1)]
+        t_all0 = ev(); t_all0.record()
+        marks = {}
+        self.counter.zero_()
+        e0 = ev(); e0.record()
+        if cfg.onion:
+            self.onion_peel()
+        else:
+            st = self.states[-1]
+            V.nnf_init_random(st.lv, st.a, self.prm, 0)
+        pu_prev = 0
+        for l in range(L, 0, -1):
+            st = self.states[l - 1]
+            lv = st.lv
+            k = 0
+            while True:
+                st.prev_rgb.copy_(st.cur_rgb)
+                st.prev_tex.copy_(st.cur_tex)
+                self.ann_search(st, k)
+                self.reconstruct(st, V.WEIGHTED)
+                self.change.zero_()
+                hb, he = self.ex.slab(lv.n_holes)
+                V.change_l1(st.cur_rgb[hb:he], st.prev_rgb[hb:he], self.change)
+                self.ex.allreduce_sum(self.change)
+                k += 1
+                if cfg.fixed_outer > 0:
+                    if k >= cfg.fixed_outer:
+                        break
+                else:
+                    e_fixed = int(self.change.item())  # the one host sync per outer iteration
+                    if 10 * e_fixed <= 3 * lv.n_holes * (1 << 20) or k >= cfg.max_outer:
+                        break
+            if l == 1:
+                self.reconstruct(st, V.BEST_PATCH)  # Eq. 6
+            else:
+                f = self.states[l - 2]
+                fb, fe = self.ex.slab(f.lv.n_targets)
+                V.nnf_upsample(lv, st.a, f.lv, f.a, self.prm, fb, fe)
+                self.ex.gather(f.a.e, f.lv.n_targets)
+                self.ex.gather(f.a.n, f.lv.n_targets)
+                self.reconstruct(f, V.UNWEIGHTED)  # R20
+            e1 = ev(); e1.record()
+            marks[l] = (e0, e1)
+            self.stats.levels[l - 1]["outer"] = k
+            e0 = e1
+        t_all1 = ev(); t_all1.record()
+        if timing:
+            torch.cuda.synchronize()
+            for l, (a, b) in marks.items():
+                self.stats.levels[l - 1]["ms"] = a.elapsed_time(b)
+            self.stats.total_ms = t_all0.elapsed_time(t_all1)
+        pu = self.counter.clone()
+        self.ex.allreduce_sum(pu)
+        self.stats.total_patch_updates = int(pu.item())
+        return self.stats
+
+    def output(self, rgb_in: torch.Tensor) -> torch.Tensor:
+        """Final video: input outside H, the best-patch u8 values inside H (device tensor)."""
+        lv = self.levels[0]
+        vb = lv.vox.view(torch.uint8).view(self.T, self.H, self.W, 8)[..., :3]
+        m = (lv.flags.view(self.T, self.H, self.W) & 1).bool()
+        return torch.where(m[..., None], vb, rgb_in)
+
+
+def inpaint(rgb: torch.Tensor, mask: torch.Tensor, cfg: Config, device="cuda", exchange=None):
+    """Convenience: whole Alg. 4 on one video.  rgb/mask may live on the host (copied in)."""
+    T, H, W, _ = rgb.shape
+    ip = Inpainter(W, H, T, cfg, device, exchange)
+    rgb_d = rgb.to(device, non_blocking=True)
+    mask_d = mask.to(device, non_blocking=True)
+    ip.load(rgb_d, mask_d)
+    stats = ip.run()
+    return ip.output(rgb_d), stats, ip

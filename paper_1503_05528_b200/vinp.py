@@ -1,0 +1,330 @@
+"""Thin ctypes binding of libvinp.so (include/vinp.h).  Argument marshalling only: every step of
+the inpainting path runs in the library's sm_100a kernels.  Device memory is owned by torch
+tensors; calls are enqueued on torch's current CUDA stream.
+
+There is no fallback: if libvinp.so is missing or fails to load, import raises.
+"""
+from __future__ import annotations
+
+import ctypes as C
+import os
+from dataclasses import dataclass, field
+from typing import Optional
+
+import torch
+
+HERE = os.path.dirname(os.path.abspath(__file__))
+LIB_PATH = os.path.join(HERE, "libvinp.so")
+
+WEIGHTED, UNWEIGHTED, BEST_PATCH = 0, 1, 2
+ONION = 0x80000000  # outer_code marker for onion layer j: ONION | j
+
+
+class VinpError(RuntimeError):
+    pass
+
+
+class _Level(C.Structure):
+    _fields_ = [("W", C.c_int32), ("H", C.c_int32), ("T", C.c_int32), ("level", C.c_int32),
+                ("vox", C.c_void_p), ("flags", C.c_void_p), ("layer", C.c_void_p),
+                ("slot", C.c_void_p),
+                ("targets", C.c_void_p), ("n_targets", C.c_int32),
+                ("holes", C.c_void_p), ("n_holes", C.c_int32),
+                ("sources", C.c_void_p), ("n_sources", C.c_int32)]
+
+
+class _NNF(C.Structure):
+    _fields_ = [("e", C.c_void_p), ("n", C.c_void_p)]
+
+
+class _Params(C.Structure):
+    _fields_ = [("lambda_", C.c_int32), ("tex_half", C.c_int32), ("seed", C.c_uint64),
+                ("rho", C.c_double), ("rmax", C.c_int32)]
+
+
+def _load():
+    if not os.path.exists(LIB_PATH):
+        raise VinpError(f"{LIB_PATH} is missing: run `python -m paper_1503_05528_b200.build` "
+                        "(there is no CPU fallback)")
+    lib = C.CDLL(LIB_PATH)
+    P, I, I32, I64, U32, U64 = C.c_void_p, C.c_int, C.c_int32, C.c_int64, C.c_uint32, C.c_uint64
+    sigs = {
+        "vinp_last_error": (C.c_char_p, []),
+        "vinp_version": (I, []),
+        "vinp_launch_count": (U64, []),
+        "vinp_build_pyramid": (I, [P, P, P, I, P]),
+        "vinp_texture_ws_bytes": (C.c_size_t, [P]),
+        "vinp_texture_features": (I, [P, P, I, P, C.c_size_t, P]),
+        "vinp_sets_ws_bytes": (C.c_size_t, [P]),
+        "vinp_build_sets": (I, [P, I, P, P, C.c_size_t, P]),
+        "vinp_build_lists": (I, [P, I, P, C.c_size_t, P]),
+        "vinp_layers": (I, [P, P, P, P]),
+        "vinp_nnf_init_random": (I, [P, P, P, U32, I32, I32, P]),
+        "vinp_nnf_upsample": (I, [P, P, P, P, P, I32, I32, P]),
+        "vinp_nnf_evaluate": (I, [P, P, P, I, I, I32, I32, P, P]),
+        "vinp_propagate": (I, [P, P, P, P, I, I, I, I, I32, I32, P, P]),
+        "vinp_random_search": (I, [P, P, P, P, U32, I, I, I, I32, I32, P, P]),
+        "vinp_ann_search": (I, [P, P, P, P, U32, I, P, I, I, I, P, P]),
+        "vinp_reconstruct": (I, [P, P, I, I, I32, I32, P, P, I, P]),
+        "vinp_commit": (I, [P, P, P, I, I32, I32, P]),
+        "vinp_change_l1": (I, [P, P, I64, P, P]),
+        "vinp_energy": (I, [P, P, P, P]),
+        "vinp_brute_force_ws_bytes": (C.c_size_t, [P]),
+        "vinp_brute_force": (I, [P, P, P, I32, I32, P, C.c_size_t, P]),
+        "vinp_patch_ssd": (I, [P, P, P, I64, P, I, P, P, P]),
+        "vinp_philox": (I, [P, I64, U64, P, P]),
+    }
+    for name, (res, args) in sigs.items():
+        f = getattr(lib, name)
+        f.restype = res
+        f.argtypes = args
+    return lib
+
+
+_lib = _load()
+EXPORTED = [
+    "vinp_last_error", "vinp_version", "vinp_launch_count", "vinp_build_pyramid",
+    "vinp_texture_ws_bytes", "vinp_texture_features", "vinp_sets_ws_bytes", "vinp_build_sets",
+    "vinp_build_lists", "vinp_layers", "vinp_nnf_init_random", "vinp_nnf_upsample",
+    "vinp_nnf_evaluate", "vinp_propagate", "vinp_random_search", "vinp_ann_search",
+    "vinp_reconstruct", "vinp_commit", "vinp_change_l1", "vinp_energy",
+    "vinp_brute_force_ws_bytes", "vinp_brute_force", "vinp_patch_ssd", "vinp_philox"]
+
+
+def _check(rc: int, what: str):
+    if rc != 0:
+        msg = _lib.vinp_last_error()
+        raise VinpError(f"{what} failed ({rc}): {msg.decode() if msg else ''}")
+
+
+def _ptr(t: Optional[torch.Tensor]):
+    return None if t is None else t.data_ptr()
+
+
+def _stream():
+    return C.c_void_p(torch.cuda.current_stream().cuda_stream)
+
+
+def launch_count() -> int:
+    return int(_lib.vinp_launch_count())
+
+
+@dataclass
+class Params:
+    lam: int = 50
+    tex_half: int = -1
+    seed: int = 1
+    rho: float = 0.5
+    rmax: int = -1
+
+    def struct(self):
+        return _Params(self.lam, self.tex_half, self.seed, self.rho, self.rmax)
+
+
+@dataclass
+class Level:
+    """One pyramid level in HBM (layout: include/vinp.h)."""
+    W: int
+    H: int
+    T: int
+    level: int
+    device: torch.device
+    vox: torch.Tensor = None
+    flags: torch.Tensor = None
+    layer: Optional[torch.Tensor] = None
+    slot: Optional[torch.Tensor] = None
+    targets: Optional[torch.Tensor] = None
+    holes: Optional[torch.Tensor] = None
+    sources: Optional[torch.Tensor] = None
+    n_targets: int = 0
+    n_holes: int = 0
+    n_sources: int = 0
+    _s: object = field(default=None, repr=False)
+
+    @classmethod
+    def alloc(cls, W, H, T, level, device):
+        lv = cls(W, H, T, level, torch.device(device))
+        N = W * H * T
+        lv.vox = torch.zeros(N, dtype=torch.int64, device=device)
+        lv.flags = torch.zeros(N, dtype=torch.uint8, device=device)
+        return lv
+
+    @property
+    def N(self):
+        return self.W * self.H * self.T
+
+    @property
+    def rmax(self):
+        return max(self.W, self.H, self.T)
+
+    def struct(self):
+        s = _Level(self.W, self.H, self.T, self.level, _ptr(self.vox), _ptr(self.flags),
+                   _ptr(self.layer), _ptr(self.slot), _ptr(self.targets), self.n_targets,
+                   _ptr(self.holes), self.n_holes, _ptr(self.sources), self.n_sources)
+        self._s = s
+        return C.byref(s)
+
+    def alloc_lists(self):
+        d = self.device
+        self.targets = torch.empty(max(self.n_targets, 1), dtype=torch.int32, device=d)
+        self.holes = torch.empty(max(self.n_holes, 1), dtype=torch.int32, device=d)
+        self.sources = torch.empty(max(self.n_sources, 1), dtype=torch.int32, device=d)
+        self.slot = torch.empty(self.N, dtype=torch.int32, device=d)
+
+
+@dataclass
+class NNF:
+    e: torch.Tensor
+    n: torch.Tensor
+    _s: object = field(default=None, repr=False)
+
+    @classmethod
+    def alloc(cls, n_slots, device, n=None):
+        e = torch.zeros(max(n_slots, 1), dtype=torch.int64, device=device)
+        if n is None:
+            n = torch.zeros(max(n_slots, 1), dtype=torch.uint8, device=device)
+        return cls(e, n)
+
+    def struct(self):
+        self._s = _NNF(_ptr(self.e), _ptr(self.n))
+        return C.byref(self._s)
+
+
+def _levels_array(levels):
+    arr = (_Level * len(levels))()
+    for i, lv in enumerate(levels):
+        lv.struct()
+        arr[i] = lv._s
+    return arr
+
+
+def _sync_back(levels, arr):
+    for i, lv in enumerate(levels):
+        lv.n_targets, lv.n_holes, lv.n_sources = arr[i].n_targets, arr[i].n_holes, arr[i].n_sources
+
+
+# ----------------------------------------------------------------------------- calls
+def build_pyramid(rgb: torch.Tensor, mask: torch.Tensor, levels):
+    arr = _levels_array(levels)
+    _check(_lib.vinp_build_pyramid(_ptr(rgb), _ptr(mask), arr, len(levels), _stream()),
+           "vinp_build_pyramid")
+
+
+def texture_features(prm: Params, levels, ws: torch.Tensor):
+    arr = _levels_array(levels)
+    _check(_lib.vinp_texture_features(C.byref(prm.struct()), arr, len(levels), _ptr(ws),
+                                      ws.numel() * ws.element_size(), _stream()),
+           "vinp_texture_features")
+
+
+def texture_ws_bytes(lv1: Level) -> int:
+    return int(_lib.vinp_texture_ws_bytes(lv1.struct()))
+
+
+def sets_ws_bytes(lv1: Level) -> int:
+    return int(_lib.vinp_sets_ws_bytes(lv1.struct()))
+
+
+def build_sets(levels, ws: torch.Tensor):
+    arr = _levels_array(levels)
+    counts = (C.c_int32 * (3 * len(levels)))()
+    _check(_lib.vinp_build_sets(arr, len(levels), counts, _ptr(ws), ws.numel(), _stream()),
+           "vinp_build_sets")
+    _sync_back(levels, arr)
+    return [tuple(counts[3 * i:3 * i + 3]) for i in range(len(levels))]
+
+
+def build_lists(levels, ws: torch.Tensor):
+    arr = _levels_array(levels)
+    _check(_lib.vinp_build_lists(arr, len(levels), _ptr(ws), ws.numel(), _stream()),
+           "vinp_build_lists")
+
+
+def layers(lv: Level, ws: torch.Tensor) -> int:
+    n = C.c_int32(0)
+    _check(_lib.vinp_layers(lv.struct(), C.byref(n), _ptr(ws), _stream()), "vinp_layers")
+    return n.value
+
+
+def nnf_init_random(lv, nnf, prm, outer_code, b=0, e=None):
+    e = lv.n_targets if e is None else e
+    _check(_lib.vinp_nnf_init_random(lv.struct(), nnf.struct(), C.byref(prm.struct()), outer_code,
+                                     b, e, _stream()), "vinp_nnf_init_random")
+
+
+def nnf_upsample(coarse, cn, fine, fn, prm, b=0, e=None):
+    e = fine.n_targets if e is None else e
+    _check(_lib.vinp_nnf_upsample(coarse.struct(), cn.struct(), fine.struct(), fn.struct(),
+                                  C.byref(prm.struct()), b, e, _stream()), "vinp_nnf_upsample")
+
+
+def nnf_evaluate(lv, nnf, prm, kb=-1, only_layer=-1, b=0, e=None, counter=None):
+    e = lv.n_targets if e is None else e
+    _check(_lib.vinp_nnf_evaluate(lv.struct(), nnf.struct(), C.byref(prm.struct()), kb, only_layer,
+                                  b, e, _ptr(counter), _stream()), "vinp_nnf_evaluate")
+
+
+def propagate(lv, nin, nout, prm, step, sign, kb=-1, only_layer=-1, b=0, e=None, counter=None):
+    e = lv.n_targets if e is None else e
+    _check(_lib.vinp_propagate(lv.struct(), nin.struct(), nout.struct(), C.byref(prm.struct()), step,
+                               sign, kb, only_layer, b, e, _ptr(counter), _stream()),
+           "vinp_propagate")
+
+
+def random_search(lv, nin, nout, prm, outer_code, pm_iter, kb=-1, only_layer=-1, b=0, e=None,
+                  counter=None):
+    e = lv.n_targets if e is None else e
+    _check(_lib.vinp_random_search(lv.struct(), nin.struct(), nout.struct(), C.byref(prm.struct()),
+                                   outer_code, pm_iter, kb, only_layer, b, e, _ptr(counter),
+                                   _stream()), "vinp_random_search")
+
+
+def ann_search(lv, a, b, prm, outer_code, K, steps=(8, 4, 2, 1), kb=-1, only_layer=-1, counter=None):
+    st = (C.c_int32 * len(steps))(*steps)
+    _check(_lib.vinp_ann_search(lv.struct(), a.struct(), b.struct(), C.byref(prm.struct()), outer_code,
+                                K, st, len(steps), kb, only_layer, _ptr(counter), _stream()),
+           "vinp_ann_search")
+
+
+def reconstruct(lv, nnf, mode, out_rgb, out_tex, layer_j=-1, hb=0, he=None, commit=True):
+    he = lv.n_holes if he is None else he
+    _check(_lib.vinp_reconstruct(lv.struct(), nnf.struct(), mode, layer_j, hb, he, _ptr(out_rgb),
+                                 _ptr(out_tex), int(commit), _stream()), "vinp_reconstruct")
+
+
+def commit(lv, out_rgb, out_tex, layer_j=-1, hb=0, he=None):
+    he = lv.n_holes if he is None else he
+    _check(_lib.vinp_commit(lv.struct(), _ptr(out_rgb), _ptr(out_tex), layer_j, hb, he, _stream()),
+           "vinp_commit")
+
+
+def change_l1(a, b, out):
+    _check(_lib.vinp_change_l1(_ptr(a), _ptr(b), a.numel(), _ptr(out), _stream()), "vinp_change_l1")
+
+
+def energy(lv, nnf, out):
+    _check(_lib.vinp_energy(lv.struct(), nnf.struct(), _ptr(out), _stream()), "vinp_energy")
+
+
+def brute_force(lv, nnf, prm, b=0, e=None, ws=None):
+    e = lv.n_targets if e is None else e
+    nbytes = int(_lib.vinp_brute_force_ws_bytes(lv.struct()))
+    if ws is None or ws.numel() < nbytes:
+        ws = torch.empty(max(nbytes, 1), dtype=torch.uint8, device=lv.device)
+    _check(_lib.vinp_brute_force(lv.struct(), nnf.struct(), C.byref(prm.struct()), b, e, _ptr(ws),
+                                 ws.numel(), _stream()), "vinp_brute_force")
+
+
+def patch_ssd(lv, p, q, prm, kb=-1):
+    n = p.numel()
+    D = torch.empty(n, dtype=torch.int32, device=lv.device)
+    cnt = torch.empty(n, dtype=torch.uint8, device=lv.device)
+    _check(_lib.vinp_patch_ssd(lv.struct(), _ptr(p), _ptr(q), n, C.byref(prm.struct()), kb, _ptr(D),
+                               _ptr(cnt), _stream()), "vinp_patch_ssd")
+    return D, cnt
+
+
+def philox(ctr: torch.Tensor, seed: int):
+    out = torch.empty_like(ctr)
+    _check(_lib.vinp_philox(_ptr(ctr), ctr.shape[0], seed, _ptr(out), _stream()), "vinp_philox")
+    return out
