@@ -9,7 +9,7 @@ import pytest
 import torch
 
 from gen.synth import generate, random_volume
-from tests import _bridge as B
+import _bridge as B
 
 pytestmark = pytest.mark.gpu
 
