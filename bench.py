@@ -209,6 +209,7 @@ def main():
     ip.load(v, m)
     stats = ip.run(timing=True)
     levels = [{"level": l["level"], "outer": l["outer"], "s": l["ms"] / 1000.0} for l in stats.levels]
+    levels[-1]["onion_s"] = stats.onion_ms / 1000.0
 
     # dominant-kernel roofline: one instrumented step with events around every pass
     roof = measure_roofline(ip, v, m, dev)
@@ -285,7 +286,7 @@ def measure_roofline(ip, v, m, dev):
             s0.record()
             f(*a, **k)
             s1.record()
-            rec.append((name, s0, s1, c0, ip.counter.clone(), nt_fn(*a, **k)))
+            rec.append((name, s0, s1, c0, ip.counter.clone(), nt_fn(*a, **k), a[0].level))
         setattr(V, name, g)
 
     # slot range [b, e) of each call, from its positional arguments (see paper_1503_05528_b200/vinp.py)
@@ -294,14 +295,17 @@ def measure_roofline(ip, v, m, dev):
     wrap("nnf_evaluate", lambda lv, *a, **k: (a[4], a[5]))
     wrap("reconstruct", lambda lv, *a, **k: (a[5], a[6]))
     try:
+        ip.native = False  # one C-ABI call per pass so that every launch is timed
         ip.load(v, m)
         ip.run(timing=False)
         torch.cuda.synchronize()
     finally:
+        ip.native = True
         for k2, f in orig.items():
             setattr(V, k2, f)
     agg = {}
-    for name, s0, s1, c0, c1, (b, e) in rec:
+    per_level = {}
+    for name, s0, s1, c0, c1, (b, e), lvl in rec:
         ms = s0.elapsed_time(s1)
         pu = int(c1.item() - c0.item())
         slots = e - b
@@ -309,11 +313,12 @@ def measure_roofline(ip, v, m, dev):
             by = B_HOLE * slots
         else:
             by = B_PU * pu + B_TP * slots
-        a = agg.setdefault(name, {"ms": 0.0, "bytes": 0, "launches": 0, "pu": 0})
-        a["ms"] += ms
-        a["bytes"] += by
-        a["launches"] += 1
-        a["pu"] += pu
+        for a in (agg.setdefault(name, {"ms": 0.0, "bytes": 0, "launches": 0, "pu": 0}),
+                  per_level.setdefault(f"{name}@l{lvl}", {"ms": 0.0, "bytes": 0, "launches": 0, "pu": 0})):
+            a["ms"] += ms
+            a["bytes"] += by
+            a["launches"] += 1
+            a["pu"] += pu
     tot = sum(a["ms"] for a in agg.values())
     dom = max(agg, key=lambda k: agg[k]["ms"])
     a = agg[dom]
@@ -329,7 +334,10 @@ def measure_roofline(ip, v, m, dev):
     return {"kernel": f"vinp_{dom}", "bound": "hbm", "achieved": round(achieved, 1), "peak": peak,
             "peak_kind": kind, "unit": "GB/s", "frac": round(achieved / peak, 4),
             "traffic": traffic, "bytes_per_launch": a["bytes"] / a["launches"],
-            "avg_launch_ms": a["ms"] / a["launches"], "kernels": kernels}
+            "avg_launch_ms": a["ms"] / a["launches"], "kernels": kernels,
+            "by_level": {k: {"ms": round(x["ms"], 2), "GB/s": round(x["bytes"] / (x["ms"] / 1000) / 1e9, 1),
+                             "launches": x["launches"], "patch_updates": x["pu"]}
+                         for k, x in sorted(per_level.items())}}
 
 
 if __name__ == "__main__":

@@ -172,6 +172,18 @@ vinp_status vinp_reconstruct(vinp_level* lv, const vinp_nnf* nnf, int mode, int 
 vinp_status vinp_commit(vinp_level* lv, const float* out_rgb, const float* out_tex, int layer_j,
                         int32_t hb, int32_t he, void* stream);
 
+/* ---- a12: onion-peel initialisation (Alg. 3; Eqs. 12-13; R22), coarsest level, after
+ * vinp_layers and vinp_nnf_init_random on `a`: for j = 0..n_layers: ANN search (as vinp_ann_search,
+ * K iterations, outer code 0x80000000|j) over the targets with layer(p) == j and known set
+ * K = {layer < max(j,1)}; then for j >= 1 the weighted reconstruction (Eq. 13) of the holes of
+ * layer j, committed to the working copy.  Layer-j index lists are built once in ws
+ * (vinp_onion_ws_bytes); synchronises once.  Result NNF in `a`; `b` is scratch. */
+size_t vinp_onion_ws_bytes(const vinp_level* lv);
+vinp_status vinp_onion_peel(vinp_level* lv, vinp_nnf* a, vinp_nnf* b, const vinp_params* prm, int K,
+                            const int32_t* steps, int n_steps, int n_layers, float* out_rgb,
+                            float* out_tex, unsigned long long* counter, void* ws, size_t ws_bytes,
+                            void* stream);
+
 /* ---- a11: stopping-rule change (Alg. 4, R19): *out (device int64) += sum_i
  * llrint(|a_i - b_i| 2^20).  e = out / 2^20 / (3|H|). */
 vinp_status vinp_change_l1(const float* a, const float* b, int64_t n, int64_t* out, void* stream);

@@ -27,28 +27,33 @@ def _stale() -> bool:
     return any(os.path.getmtime(d) > t for d in deps)
 
 
-def build(force: bool = False, verbose: bool = False) -> str:
-    if not force and not _stale():
+def build(force: bool = False, verbose: bool = False, defines=(), out=None) -> str:
+    """defines/out: variant builds for A/B timing (tools/); the product uses the defaults."""
+    lib = out or LIB
+    if not force and not defines and not _stale():
         return LIB
     objs = []
     log = []
     for src in sources():
-        obj = os.path.join(HERE, "csrc", os.path.basename(src)[:-3] + ".o")
-        cmd = [NVCC, *ARCH, *FLAGS, "-I", os.path.join(ROOT, "include"), "-c", src, "-o", obj]
+        tag = "" if not defines else "_" + os.path.basename(lib)[:-3]
+        obj = os.path.join(HERE, "csrc", os.path.basename(src)[:-3] + tag + ".o")
+        cmd = [NVCC, *ARCH, *FLAGS, *["-D" + d for d in defines], "-I", os.path.join(ROOT, "include"),
+               "-c", src, "-o", obj]
         r = subprocess.run(cmd, capture_output=True, text=True)
         log.append(r.stderr)
         if r.returncode != 0:
-            raise RuntimeError(f"nvcc failed on {src}:\n{r.stderr[-4000:]}")
+            errs = [l for l in r.stderr.splitlines() if "error" in l.lower()]
+            raise RuntimeError(f"nvcc failed on {src}:\n" + "\n".join(errs[:20] or [r.stderr[-4000:]]))
         objs.append(obj)
-    cmd = [NVCC, *ARCH, "-shared", "-o", LIB, *objs, "-lcudart"]
+    cmd = [NVCC, *ARCH, "-shared", "-o", lib, *objs, "-lcudart"]
     r = subprocess.run(cmd, capture_output=True, text=True)
     if r.returncode != 0:
         raise RuntimeError(f"link failed:\n{r.stderr[-4000:]}")
-    with open(os.path.join(HERE, "csrc", "ptxas.log"), "w") as f:
+    with open(os.path.join(HERE, "csrc", "ptxas.log" if not defines else f"ptxas{tag}.log"), "w") as f:
         f.write("\n".join(log))
     if verbose:
         print("\n".join(log))
-    return LIB
+    return lib
 
 
 if __name__ == "__main__":

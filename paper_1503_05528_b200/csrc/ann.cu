@@ -81,162 +81,307 @@ __global__ void k_upsample(LevelArgs c, const uint64_t* __restrict__ ce, LevelAr
   fn[s] = 0;
 }
 
+#ifndef VINP_MINB
+#define VINP_MINB 3
+#endif
+#ifndef VINP_GROUP
+#define VINP_GROUP 8
+#endif
+
+// ------------------------------------------------------------------ thread-per-target SSD
+// Used where candidates are spatially coherent (evaluate, propagation): lane l of a warp owns
+// target slot s0 + l, and consecutive slots are x-adjacent voxels, whose candidate sources are
+// usually x-adjacent too.  Each of the 125 gathers of a patch is then one coalesced warp load of
+// ~32 adjacent 8-byte voxels (2-3 L1 lines), addressed as row pointer + immediate offset.
+// Exact partial-distance elimination after every frame of 25 voxels (SPEC: early abort that
+// changes no comparison): a lane drops its candidate once the partial sum reaches `thr`.
+// `full` = 1: every voxel of N_p is in Omega and K (interior target, K = Omega).
+template <bool ABORT>
+__device__ __forceinline__ uint32_t thread_ssd(const LevelArgs& a, int p, int px, int py, int pt,
+                                               int q, int lambda, int kb, bool full, uint32_t thr,
+                                               bool& alive) {
+  const unsigned long long* v = reinterpret_cast<const unsigned long long*>(a.vox);
+  uint32_t accc = 0, acct = 0;
+#pragma unroll 1
+  for (int dt = -2; dt <= 2; ++dt) {
+#pragma unroll
+    for (int dy = -2; dy <= 2; ++dy) {
+      int ro = dt * a.g.HW + dy * a.g.W;
+      const unsigned long long* tr = v + (p + ro);
+      const unsigned long long* sr = v + (q + ro);
+      if (full) {
+        uint64_t t0 = __ldg(tr - 2), t1 = __ldg(tr - 1), t2 = __ldg(tr), t3 = __ldg(tr + 1), t4 = __ldg(tr + 2);
+        uint64_t s0 = __ldg(sr - 2), s1 = __ldg(sr - 1), s2 = __ldg(sr), s3 = __ldg(sr + 1), s4 = __ldg(sr + 2);
+#define VINP_ACC(T, S)                                                        \
+  {                                                                           \
+    uint32_t dc = __vabsdiffu4((uint32_t)(T), (uint32_t)(S));                 \
+    uint32_t dx_ = __vabsdiffu4((uint32_t)((T) >> 32), (uint32_t)((S) >> 32)); \
+    accc = __dp4a(dc, dc, accc);                                              \
+    acct = __dp4a(dx_, dx_, acct);                                            \
+  }
+        VINP_ACC(t0, s0) VINP_ACC(t1, s1) VINP_ACC(t2, s2) VINP_ACC(t3, s3) VINP_ACC(t4, s4)
+      } else {
+#pragma unroll
+        for (int dx = -2; dx <= 2; ++dx) {
+          if (!inside(a.g, px + dx, py + dy, pt + dt)) continue;
+          if (kb >= 0 && !(a.layer[p + ro + dx] < kb)) continue;
+          uint64_t t = __ldg(tr + dx), s = __ldg(sr + dx);
+          VINP_ACC(t, s)
+        }
+      }
+#undef VINP_ACC
+    }
+    if (ABORT) {
+      uint32_t part = 4u * accc + (uint32_t)lambda * acct;
+      if (part >= thr) alive = false;
+      if (!__any_sync(__activemask(), alive)) break;
+      if (!alive) break;
+    }
+  }
+  return 4u * accc + (uint32_t)lambda * acct;
+}
+
 // ------------------------------------------------------------------ a5: evaluate
 __global__ void __launch_bounds__(256) k_evaluate(LevelArgs a, uint64_t* __restrict__ ee,
                                                   uint8_t* __restrict__ en, int lambda, int kb,
                                                   int only_layer, int32_t b, int32_t e,
+                                                  const int32_t* __restrict__ list,
                                                   unsigned long long* counter) {
-  int lane = threadIdx.x & 31;
-  int s = b + blockIdx.x * kWarpsPerBlock + (threadIdx.x >> 5);
-  if (s >= e) return;
-  int p = a.targets[s];
-  if (only_layer >= 0 && a.layer[p] != only_layer) return;
-  PatchLanes L;
-  init_lanes(L, a.g, lane);
-  int px, py, pt;
-  decode(a.g, p, px, py, pt);
-  TargetPatch tp;
-  load_target(tp, L, a.g, a.vox, a.layer, kb, p, px, py, pt);
-  int q = e_q(ee[s]);
-  uint32_t D = warp_ssd(tp, L, a.vox, q, lambda);
-  uint32_t n = __reduce_add_sync(kFull, (uint32_t)__popc(tp.mask));
-  if (lane == 0) {
+  int idx = b + blockIdx.x * blockDim.x + threadIdx.x;
+  bool act = idx < e;
+  int s = act ? (list ? __ldg(list + idx) : idx) : 0;
+  int p = act ? __ldg(a.targets + s) : 0;
+  act = act && (only_layer < 0 || a.layer[p] == only_layer);
+  unsigned cnt = 0;
+  if (act) {
+    int px, py, pt;
+    decode(a.g, p, px, py, pt);
+    int q = e_q(ee[s]);
+    bool full = kb < 0 && px >= 2 && px < a.g.W - 2 && py >= 2 && py < a.g.H - 2 && pt >= 2 && pt < a.g.T - 2;
+    bool alive = true;
+    uint32_t D = thread_ssd<false>(a, p, px, py, pt, q, lambda, kb, full, 0, alive);
+    int n = 0;
+    if (full) {
+      n = 125;
+    } else {
+      for (int dt = -2; dt <= 2; ++dt)
+        for (int dy = -2; dy <= 2; ++dy)
+          for (int dx = -2; dx <= 2; ++dx)
+            if (inside(a.g, px + dx, py + dy, pt + dt) &&
+                (kb < 0 || a.layer[p + dt * a.g.HW + dy * a.g.W + dx] < kb))
+              ++n;
+    }
     ee[s] = pack_e(D, q);
     en[s] = (uint8_t)n;
-    flush_count(counter, 1);
+    cnt = 1;
   }
-}
-
-// evaluate a list of candidate sources (warp-uniform) against the incumbent, in rank order
-__device__ __forceinline__ void eval_candidates(const TargetPatch& tp, const PatchLanes& L,
-                                                const uint64_t* __restrict__ vox, int lambda,
-                                                unsigned mask, int qlane, uint32_t& bestD,
-                                                int& bestq) {
-  while (mask) {
-    int i0 = __ffs(mask) - 1;
-    mask &= mask - 1;
-    int q0 = __shfl_sync(kFull, qlane, i0);
-    if (mask) {
-      int i1 = __ffs(mask) - 1;
-      mask &= mask - 1;
-      int q1 = __shfl_sync(kFull, qlane, i1);
-      uint32_t D0, D1;
-      warp_ssd2(tp, L, vox, q0, q1, lambda, D0, D1);
-      if (D0 < bestD) { bestD = D0; bestq = q0; }
-      if (D1 < bestD) { bestD = D1; bestq = q1; }
-    } else {
-      uint32_t D0 = warp_ssd(tp, L, vox, q0, lambda);
-      if (D0 < bestD) { bestD = D0; bestq = q0; }
-    }
-  }
+  cnt = __reduce_add_sync(kFull, cnt);
+  if ((threadIdx.x & 31) == 0) flush_count(counter, cnt);
 }
 
 // ------------------------------------------------------------------ a6: propagation pass
+// Lane = target (thread-per-target, coherent candidates).  Candidates of rank 1..3 are evaluated
+// one rank at a time by all lanes that have one, each against the running best of its own target
+// (strict improvement in rank order, R25).
 __global__ void __launch_bounds__(256) k_propagate(LevelArgs a, const uint64_t* __restrict__ ein,
                                                    uint64_t* __restrict__ eout, int lambda, int step,
                                                    int sign, int kb, int only_layer, int32_t b,
-                                                   int32_t e, unsigned long long* counter) {
-  int lane = threadIdx.x & 31;
-  int s = b + blockIdx.x * kWarpsPerBlock + (threadIdx.x >> 5);
-  if (s >= e) return;
-  int p = a.targets[s];
-  uint64_t inc = ein[s];
-  if (only_layer >= 0 && a.layer[p] != only_layer) {
-    if (lane == 0) eout[s] = inc;
-    return;
-  }
-  int px, py, pt;
-  decode(a.g, p, px, py, pt);
+                                                   int32_t e, const int32_t* __restrict__ list,
+                                                   unsigned long long* counter) {
+  int idx = b + blockIdx.x * blockDim.x + threadIdx.x;
+  bool have = idx < e;
+  int s = have ? (list ? __ldg(list + idx) : idx) : 0;
+  int p = have ? __ldg(a.targets + s) : 0;
+  uint64_t inc = have ? __ldg(reinterpret_cast<const unsigned long long*>(ein) + s) : 0ull;
+  bool act = have && (only_layer < 0 || a.layer[p] == only_layer);
+  int q[3] = {-1, -1, -1};
+  int px = 0, py = 0, pt = 0;
   int q0 = e_q(inc);
-  // lanes 0,1,2: neighbour r = p + sign*step*e_{x,y,t}; candidate q = p + phi(r)
-  int q = -1;
-  if (lane < 3) {
-    int ox = lane == 0 ? sign * step : 0, oy = lane == 1 ? sign * step : 0,
-        ot = lane == 2 ? sign * step : 0;
-    int rx = px + ox, ry = py + oy, rt = pt + ot;
-    if (inside(a.g, rx, ry, rt)) {
-      int rs = __ldg(a.slot + lin(a.g, rx, ry, rt));
-      if (rs >= 0) {
-        int src = e_q(__ldg(reinterpret_cast<const unsigned long long*>(ein) + rs));
-        int sx, sy, st;
-        decode(a.g, src, sx, sy, st);
-        int qx = sx - ox, qy = sy - oy, qt = st - ot;  // q = p + (src - r)
-        if (is_source(a.g, a.flags, qx, qy, qt)) q = lin(a.g, qx, qy, qt);
+  if (act) {
+    decode(a.g, p, px, py, pt);
+#pragma unroll
+    for (int c = 0; c < 3; ++c) {
+      int ox = c == 0 ? sign * step : 0, oy = c == 1 ? sign * step : 0, ot = c == 2 ? sign * step : 0;
+      int rx = px + ox, ry = py + oy, rt = pt + ot;
+      if (inside(a.g, rx, ry, rt)) {
+        int rs = __ldg(a.slot + lin(a.g, rx, ry, rt));
+        if (rs >= 0) {
+          int src = e_q(__ldg(reinterpret_cast<const unsigned long long*>(ein) + rs));
+          int sx, sy, st;
+          decode(a.g, src, sx, sy, st);
+          int qx = sx - ox, qy = sy - oy, qt = st - ot;  // q = p + (src - r)
+          if (is_source(a.g, a.flags, qx, qy, qt)) q[c] = lin(a.g, qx, qy, qt);
+        }
       }
     }
+    if (q[0] == q0) q[0] = -1;
+    if (q[1] == q0 || q[1] == q[0]) q[1] = -1;
+    if (q[2] == q0 || q[2] == q[0] || q[2] == q[1]) q[2] = -1;
   }
-  int c0 = __shfl_sync(kFull, q, 0), c1 = __shfl_sync(kFull, q, 1);
-  bool ok = lane < 3 && q >= 0 && q != q0 && !(lane >= 1 && q == c0) && !(lane >= 2 && q == c1);
-  unsigned mask = __ballot_sync(kFull, ok);
   uint32_t bestD = e_D(inc);
   int bestq = q0;
-  if (mask) {
-    PatchLanes L;
-    init_lanes(L, a.g, lane);
-    TargetPatch tp;
-    load_target(tp, L, a.g, a.vox, a.layer, kb, p, px, py, pt);
-    eval_candidates(tp, L, a.vox, lambda, mask, q, bestD, bestq);
+  unsigned cnt = 0;
+  bool full = act && kb < 0 && px >= 2 && px < a.g.W - 2 && py >= 2 && py < a.g.H - 2 && pt >= 2 &&
+              pt < a.g.T - 2;
+  bool allfull = __all_sync(kFull, full || !act);
+#pragma unroll
+  for (int c = 0; c < 3; ++c) {
+    bool mine = act && q[c] >= 0;
+    if (!__any_sync(kFull, mine)) continue;
+    if (mine) {
+      bool alive = true;
+      uint32_t D = allfull ? thread_ssd<true>(a, p, px, py, pt, q[c], lambda, kb, true, bestD, alive)
+                           : thread_ssd<true>(a, p, px, py, pt, q[c], lambda, kb, full, bestD, alive);
+      if (alive && D < bestD) {
+        bestD = D;
+        bestq = q[c];
+      }
+      ++cnt;
+    }
   }
-  if (lane == 0) {
-    eout[s] = pack_e(bestD, bestq);
-    flush_count(counter, __popc(mask));
-  }
+  if (have) eout[s] = pack_e(bestD, bestq);
+  cnt = __reduce_add_sync(kFull, cnt);
+  if ((threadIdx.x & 31) == 0) flush_count(counter, cnt);
 }
 
 // ------------------------------------------------------------------ a7: random search pass
+// Candidates are incoherent (independent Philox offsets per voxel), so the evaluation is
+// warp-cooperative: lane l holds voxel l + 32k of the target patch, every gather of a candidate
+// is one warp load of 32 consecutive patch voxels (~8 L1 lines), and a group of up to G candidates
+// of one target has all its gathers in flight.  Exact partial-distance elimination after each
+// chunk of 32 voxels against the best distance at the start of the group.
+__device__ __forceinline__ uint64_t shfl64(uint64_t v, int src) {
+  uint32_t lo = __shfl_sync(kFull, (uint32_t)v, src), hi = __shfl_sync(kFull, (uint32_t)(v >> 32), src);
+  return ((uint64_t)hi << 32) | lo;
+}
+
+template <int G>
+__device__ __forceinline__ void eval_group(const LevelArgs& a, const PatchLanes& L, unsigned tmask,
+                                           int lambda, int pi, const int* cand, int i, int base,
+                                           int k, uint32_t& bestD, int& bestq, uint32_t (&tw)[4][2],
+                                           unsigned& tloaded) {
+  const unsigned long long* v = reinterpret_cast<const unsigned long long*>(a.vox);
+  int q[G];
+  uint32_t part[G];
+#pragma unroll
+  for (int c = 0; c < G; ++c) {
+    q[c] = c < k ? cand[(base + c) * 32 + i] : 0;
+    part[c] = 0;
+  }
+  unsigned alive = (1u << k) - 1;
+  uint32_t thr = bestD;
+#pragma unroll
+  for (int ch = 0; ch < 4; ++ch) {
+    if (!alive) break;  // warp-uniform
+    bool m = (tmask >> ch) & 1;
+    if (!((tloaded >> ch) & 1)) {  // target chunk, loaded on first use
+      uint64_t w = m ? __ldg(v + pi + L.off[ch]) : 0ull;
+      tw[ch][0] = (uint32_t)w;
+      tw[ch][1] = (uint32_t)(w >> 32);
+      tloaded |= 1u << ch;
+    }
+    uint64_t sv[G];
+#pragma unroll
+    for (int c = 0; c < G; ++c) sv[c] = (m && ((alive >> c) & 1)) ? __ldg(v + q[c] + L.off[ch]) : 0ull;
+#pragma unroll
+    for (int c = 0; c < G; ++c) {
+      if ((alive >> c) & 1) {
+        uint32_t x = m ? voxel_cost(tw[ch][0], tw[ch][1], sv[c], lambda) : 0u;
+        part[c] += __reduce_add_sync(kFull, x);
+        if (part[c] >= thr) alive &= ~(1u << c);
+      }
+    }
+  }
+#pragma unroll
+  for (int c = 0; c < G; ++c)
+    if (((alive >> c) & 1) && part[c] < bestD) {
+      bestD = part[c];
+      bestq = q[c];
+    }
+}
+
+template <int NC>
+__device__ __forceinline__ void phase2(const LevelArgs& a, int lane, int lambda, int kb, int p,
+                                       uint64_t inc, const int* cand, int ncand, uint64_t& result,
+                                       unsigned& cnt) {
+  constexpr int G = NC < VINP_GROUP ? NC : VINP_GROUP;
+  result = inc;
+  unsigned work = __ballot_sync(kFull, ncand != 0);
+  if (!work) return;
+  PatchLanes L;
+  init_lanes(L, a.g, lane);
+  while (work) {
+    int i = __ffs(work) - 1;
+    work &= work - 1;
+    int pi = __shfl_sync(kFull, p, i);
+    int ni = __shfl_sync(kFull, ncand, i);
+    uint64_t inci = shfl64(inc, i);
+    int px, py, pt;
+    decode(a.g, pi, px, py, pt);
+    unsigned tmask = 0;  // per-lane validity of the 4 owned target voxels (Omega and K)
+#pragma unroll
+    for (int ch = 0; ch < 4; ++ch)
+      if (L.live[ch] && inside(a.g, px + L.dx[ch], py + L.dy[ch], pt + L.dt[ch]) &&
+          (kb < 0 || a.layer[pi + L.off[ch]] < kb))
+        tmask |= 1u << ch;
+    uint32_t bestD = e_D(inci);
+    int bestq = e_q(inci);
+    uint32_t tw[4][2];
+    unsigned tloaded = 0;
+    for (int base = 0; base < ni; base += G)
+      eval_group<G>(a, L, tmask, lambda, pi, cand, i, base, min(G, ni - base), bestD, bestq, tw, tloaded);
+    if (lane == i) result = pack_e(bestD, bestq);
+    cnt += ni;
+  }
+}
+
 struct Radii {
   double R[32];
   int M;
 };
 
-__global__ void __launch_bounds__(256) k_random_search(LevelArgs a, const uint64_t* __restrict__ ein,
-                                                       uint64_t* __restrict__ eout, int lambda,
-                                                       Radii rad, uint64_t seed, uint32_t oc,
-                                                       int pm_iter, int kb, int only_layer, int32_t b,
-                                                       int32_t e, unsigned long long* counter) {
+template <int NC, int WPB>
+__global__ void __launch_bounds__(32 * WPB, VINP_MINB * 8 / WPB) k_random_search(
+    LevelArgs a, const uint64_t* __restrict__ ein, uint64_t* __restrict__ eout, int lambda, Radii rad,
+    uint64_t seed, uint32_t oc, int pm_iter, int kb, int only_layer, int32_t b, int32_t e,
+    const int32_t* __restrict__ list, unsigned long long* counter) {
   int lane = threadIdx.x & 31;
-  int s = b + blockIdx.x * kWarpsPerBlock + (threadIdx.x >> 5);
-  if (s >= e) return;
-  int p = a.targets[s];
-  uint64_t inc = ein[s];
-  if (only_layer >= 0 && a.layer[p] != only_layer) {
-    if (lane == 0) eout[s] = inc;
-    return;
+  int i0 = b + (blockIdx.x * WPB + (threadIdx.x >> 5)) * 32;
+  if (i0 >= e) return;
+  int idx = i0 + lane;
+  bool have = idx < e;
+  int s = have ? (list ? __ldg(list + idx) : idx) : 0;
+  int p = have ? __ldg(a.targets + s) : 0;
+  uint64_t inc = have ? __ldg(reinterpret_cast<const unsigned long long*>(ein) + s) : 0ull;
+  bool act = have && (only_layer < 0 || a.layer[p] == only_layer);
+  __shared__ int s_cand[WPB][NC * 32];
+  int* cand = s_cand[threadIdx.x >> 5];
+  int nc = 0;
+  if (act) {
+    int q0 = e_q(inc);
+    int q0x, q0y, q0t;
+    decode(a.g, q0, q0x, q0y, q0t);
+    for (int i = 0; i < rad.M; ++i) {  // candidate i + 1 of Eq. 3
+      uint4 u = draw((uint32_t)p, (uint32_t)pm_iter, a.level, kStreamRS, i + 1, oc, seed);
+      double R = rad.R[i];
+      int ox = (int)floor(__dmul_rn(R, __dmul_rn((double)u.x - 2147483648.0, 4.656612873077392578125e-10)));
+      int oy = (int)floor(__dmul_rn(R, __dmul_rn((double)u.y - 2147483648.0, 4.656612873077392578125e-10)));
+      int ot = (int)floor(__dmul_rn(R, __dmul_rn((double)u.z - 2147483648.0, 4.656612873077392578125e-10)));
+      int qx = q0x + ox, qy = q0y + oy, qt = q0t + ot;
+      if (is_source(a.g, a.flags, qx, qy, qt)) {
+        int qq = lin(a.g, qx, qy, qt);
+        bool dup = qq == q0;
+        for (int j = 0; j < nc; ++j) dup |= (cand[j * 32 + lane] == qq);
+        if (!dup) cand[(nc++) * 32 + lane] = qq;
+      }
+    }
   }
-  int px, py, pt;
-  decode(a.g, p, px, py, pt);
-  int q0 = e_q(inc);
-  int q0x, q0y, q0t;
-  decode(a.g, q0, q0x, q0y, q0t);
-  int q = -1;
-  if (lane < rad.M) {  // candidate i = lane + 1
-    uint4 u = draw((uint32_t)p, (uint32_t)pm_iter, a.level, kStreamRS, lane + 1, oc, seed);
-    double R = rad.R[lane];
-    int ox = (int)floor(__dmul_rn(R, __dmul_rn((double)u.x - 2147483648.0, 4.656612873077392578125e-10)));
-    int oy = (int)floor(__dmul_rn(R, __dmul_rn((double)u.y - 2147483648.0, 4.656612873077392578125e-10)));
-    int ot = (int)floor(__dmul_rn(R, __dmul_rn((double)u.z - 2147483648.0, 4.656612873077392578125e-10)));
-    int qx = q0x + ox, qy = q0y + oy, qt = q0t + ot;
-    if (is_source(a.g, a.flags, qx, qy, qt)) q = lin(a.g, qx, qy, qt);
-  }
-  bool ok = q >= 0 && q != q0;
-  for (int j = 0; j < rad.M; ++j) {  // duplicates of an earlier valid candidate
-    int qj = __shfl_sync(kFull, q, j);
-    if (j < lane && qj == q) ok = false;
-  }
-  unsigned mask = __ballot_sync(kFull, ok);
-  uint32_t bestD = e_D(inc);
-  int bestq = q0;
-  if (mask) {
-    PatchLanes L;
-    init_lanes(L, a.g, lane);
-    TargetPatch tp;
-    load_target(tp, L, a.g, a.vox, a.layer, kb, p, px, py, pt);
-    eval_candidates(tp, L, a.vox, lambda, mask, q, bestD, bestq);
-  }
-  if (lane == 0) {
-    eout[s] = pack_e(bestD, bestq);
-    flush_count(counter, __popc(mask));
-  }
+  __syncwarp();
+  uint64_t res;
+  unsigned cnt = 0;
+  phase2<NC>(a, lane, lambda, kb, p, inc, cand, nc, res, cnt);
+  if (have) eout[s] = res;
+  if (lane == 0) flush_count(counter, cnt);
 }
 
 // ------------------------------------------------------------------ a13: brute force (CUDA cores)
@@ -332,9 +477,10 @@ static Radii make_radii(const vinp_level* lv, const vinp_params* prm) {
   int rmax = prm->rmax > 0 ? prm->rmax : std::max(lv->W, std::max(lv->H, lv->T));
   double R = (double)rmax;
   r.M = 0;
-  for (int i = 1; i <= 31; ++i) {
+  for (int i = 1; i <= 32; ++i) {
     R = R * prm->rho;
     if (!(R >= 1.0)) break;
+    if (r.M == 32) { r.M = -1; break; }
     r.R[r.M++] = R;
   }
   return r;
@@ -385,54 +531,100 @@ vinp_status vinp_nnf_upsample(const vinp_level* coarse, const vinp_nnf* cn, cons
   return check_launch("vinp_nnf_upsample");
 }
 
-vinp_status vinp_nnf_evaluate(const vinp_level* lv, vinp_nnf* nnf, const vinp_params* prm, int kb,
-                              int only_layer, int32_t b, int32_t e, unsigned long long* counter,
-                              void* stream) {
-  vinp_status st = check_nnf_args(lv, "vinp_nnf_evaluate", b, e, prm);
+}  // extern "C"
+
+namespace vinp {
+vinp_status launch_evaluate(const vinp_level* lv, vinp_nnf* nnf, const vinp_params* prm, int kb,
+                            int only_layer, int32_t b, int32_t e, const int32_t* list,
+                            unsigned long long* counter, void* stream) {
+  vinp_status st = check_nnf_args(lv, "vinp_nnf_evaluate", list ? 0 : b, list ? 0 : e, prm);
   if (st) return st;
   VINP_REQUIRE(nnf && nnf->e && nnf->n, "vinp_nnf_evaluate: null nnf");
   VINP_REQUIRE((kb < 0 && only_layer < 0) || lv->layer, "vinp_nnf_evaluate: layer map required");
   if (e > b) {
-    k_evaluate<<<nblk(e - b, kWarpsPerBlock), 32 * kWarpsPerBlock, 0, S(stream)>>>(
-        args_of(lv), nnf->e, nnf->n, prm->lambda, kb, only_layer, b, e, counter);
+    k_evaluate<<<nblk(e - b, 256), 256, 0, S(stream)>>>(
+        args_of(lv), nnf->e, nnf->n, prm->lambda, kb, only_layer, b, e, list, counter);
     count_launch();
   }
   return check_launch("vinp_nnf_evaluate");
 }
-
-vinp_status vinp_propagate(const vinp_level* lv, const vinp_nnf* in, vinp_nnf* out,
-                           const vinp_params* prm, int step, int sign, int kb, int only_layer,
-                           int32_t b, int32_t e, unsigned long long* counter, void* stream) {
-  vinp_status st = check_nnf_args(lv, "vinp_propagate", b, e, prm);
+vinp_status launch_propagate(const vinp_level* lv, const vinp_nnf* in, vinp_nnf* out,
+                             const vinp_params* prm, int step, int sign, int kb, int only_layer,
+                             int32_t b, int32_t e, const int32_t* list, unsigned long long* counter,
+                             void* stream) {
+  vinp_status st = check_nnf_args(lv, "vinp_propagate", list ? 0 : b, list ? 0 : e, prm);
   if (st) return st;
   VINP_REQUIRE(in && in->e && out && out->e && in->e != out->e, "vinp_propagate: need two buffers");
   VINP_REQUIRE(step >= 1 && (sign == 1 || sign == -1), "vinp_propagate: bad step/sign");
   VINP_REQUIRE((kb < 0 && only_layer < 0) || lv->layer, "vinp_propagate: layer map required");
   if (e > b) {
-    k_propagate<<<nblk(e - b, kWarpsPerBlock), 32 * kWarpsPerBlock, 0, S(stream)>>>(
-        args_of(lv), in->e, out->e, prm->lambda, step, sign, kb, only_layer, b, e, counter);
+    k_propagate<<<nblk(e - b, 256), 256, 0, S(stream)>>>(
+        args_of(lv), in->e, out->e, prm->lambda, step, sign, kb, only_layer, b, e, list, counter);
     count_launch();
   }
   return check_launch("vinp_propagate");
 }
+}  // namespace vinp
 
-vinp_status vinp_random_search(const vinp_level* lv, const vinp_nnf* in, vinp_nnf* out,
-                               const vinp_params* prm, uint32_t outer_code, int pm_iter, int kb,
-                               int only_layer, int32_t b, int32_t e, unsigned long long* counter,
-                               void* stream) {
-  vinp_status st = check_nnf_args(lv, "vinp_random_search", b, e, prm);
+extern "C" {
+vinp_status vinp_nnf_evaluate(const vinp_level* lv, vinp_nnf* nnf, const vinp_params* prm, int kb,
+                              int only_layer, int32_t b, int32_t e, unsigned long long* counter,
+                              void* stream) {
+  return launch_evaluate(lv, nnf, prm, kb, only_layer, b, e, nullptr, counter, stream);
+}
+
+vinp_status vinp_propagate(const vinp_level* lv, const vinp_nnf* in, vinp_nnf* out,
+                           const vinp_params* prm, int step, int sign, int kb, int only_layer,
+                           int32_t b, int32_t e, unsigned long long* counter, void* stream) {
+  return launch_propagate(lv, in, out, prm, step, sign, kb, only_layer, b, e, nullptr, counter, stream);
+}
+
+}  // extern "C"
+
+namespace vinp {
+vinp_status launch_random_search(const vinp_level* lv, const vinp_nnf* in, vinp_nnf* out,
+                                 const vinp_params* prm, uint32_t outer_code, int pm_iter, int kb,
+                                 int only_layer, int32_t b, int32_t e, const int32_t* list,
+                                 unsigned long long* counter, void* stream) {
+  vinp_status st = check_nnf_args(lv, "vinp_random_search", list ? 0 : b, list ? 0 : e, prm);
   if (st) return st;
   VINP_REQUIRE(in && in->e && out && out->e && in->e != out->e, "vinp_random_search: need two buffers");
   VINP_REQUIRE(prm->rho > 0 && prm->rho < 1, "vinp_random_search: rho must lie in (0,1)");
   VINP_REQUIRE((kb < 0 && only_layer < 0) || lv->layer, "vinp_random_search: layer map required");
   Radii r = make_radii(lv, prm);
+  if (r.M < 0) {
+    set_error("vinp_random_search: more than 31 random-search radii (rho too close to 1)");
+    return VINP_E_UNSUPPORTED;
+  }
   if (e > b) {
-    k_random_search<<<nblk(e - b, kWarpsPerBlock), 32 * kWarpsPerBlock, 0, S(stream)>>>(
-        args_of(lv), in->e, out->e, prm->lambda, r, prm->seed, outer_code, pm_iter, kb, only_layer,
-        b, e, counter);
+    cudaStream_t cs = S(stream);
+    LevelArgs la = args_of(lv);
+#define VINP_RS(NC, WPB)                                                                          \
+  k_random_search<NC, WPB><<<nblk(e - b, 32 * WPB), 32 * WPB, 0, cs>>>(                          \
+      la, in->e, out->e, prm->lambda, r, prm->seed, outer_code, pm_iter, kb, only_layer, b, e, list, \
+      counter)
+    if (r.M <= 8)
+      VINP_RS(8, 8);
+    else if (r.M <= 12)
+      VINP_RS(12, 8);
+    else if (r.M <= 16)
+      VINP_RS(16, 4);
+    else
+      VINP_RS(32, 2);
+#undef VINP_RS
     count_launch();
   }
   return check_launch("vinp_random_search");
+}
+}  // namespace vinp
+
+extern "C" {
+vinp_status vinp_random_search(const vinp_level* lv, const vinp_nnf* in, vinp_nnf* out,
+                               const vinp_params* prm, uint32_t outer_code, int pm_iter, int kb,
+                               int only_layer, int32_t b, int32_t e, unsigned long long* counter,
+                               void* stream) {
+  return launch_random_search(lv, in, out, prm, outer_code, pm_iter, kb, only_layer, b, e, nullptr,
+                              counter, stream);
 }
 
 vinp_status vinp_ann_search(const vinp_level* lv, vinp_nnf* a, vinp_nnf* b, const vinp_params* prm,

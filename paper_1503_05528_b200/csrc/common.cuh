@@ -41,6 +41,22 @@ inline vinp_status check_level(const vinp_level* lv, const char* who) {
   return VINP_OK;
 }
 
+// internal launchers with an optional index list (list[i] = slot / hole index, i in [b, e))
+vinp_status launch_evaluate(const vinp_level* lv, vinp_nnf* nnf, const vinp_params* prm, int kb,
+                            int only_layer, int32_t b, int32_t e, const int32_t* list,
+                            unsigned long long* counter, void* stream);
+vinp_status launch_propagate(const vinp_level* lv, const vinp_nnf* in, vinp_nnf* out,
+                             const vinp_params* prm, int step, int sign, int kb, int only_layer,
+                             int32_t b, int32_t e, const int32_t* list, unsigned long long* counter,
+                             void* stream);
+vinp_status launch_random_search(const vinp_level* lv, const vinp_nnf* in, vinp_nnf* out,
+                                 const vinp_params* prm, uint32_t outer_code, int pm_iter, int kb,
+                                 int only_layer, int32_t b, int32_t e, const int32_t* list,
+                                 unsigned long long* counter, void* stream);
+vinp_status launch_reconstruct(vinp_level* lv, const vinp_nnf* nnf, int mode, int layer_j, int32_t hb,
+                               int32_t he, const int32_t* list, float* out_rgb, float* out_tex,
+                               int commit, void* stream);
+
 // ---------------------------------------------------------------- geometry
 struct Geo {
   int W, H, T;
@@ -185,6 +201,27 @@ __device__ __forceinline__ void warp_ssd2(const TargetPatch& tp, const PatchLane
   }
   D0 = __reduce_add_sync(kFull, a0);
   D1 = __reduce_add_sync(kFull, a1);
+}
+
+// N candidates at once (N*4 gathers in flight per lane).
+template <int N>
+__device__ __forceinline__ void warp_ssdN(const TargetPatch& tp, const PatchLanes& L,
+                                          const uint64_t* __restrict__ vox, const int* q, int lambda,
+                                          uint32_t* D) {
+  const unsigned long long* v = reinterpret_cast<const unsigned long long*>(vox);
+  uint64_t s[N][4];
+#pragma unroll
+  for (int c = 0; c < N; ++c)
+#pragma unroll
+    for (int i = 0; i < 4; ++i) s[c][i] = (tp.mask & (1u << i)) ? __ldg(v + q[c] + L.off[i]) : 0ull;
+#pragma unroll
+  for (int c = 0; c < N; ++c) {
+    uint32_t a = 0;
+#pragma unroll
+    for (int i = 0; i < 4; ++i)
+      if (tp.mask & (1u << i)) a += voxel_cost(tp.c[i], tp.t[i], s[c][i], lambda);
+    D[c] = __reduce_add_sync(kFull, a);
+  }
 }
 
 __device__ __forceinline__ bool is_source(const Geo& g, const uint8_t* __restrict__ flags, int x,

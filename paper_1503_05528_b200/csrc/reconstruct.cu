@@ -5,9 +5,11 @@
 // for v = l + 32i): each lane reads slot[q], the NNF entry of q and the proposed value
 // u(p + phi(q)) = vox[src_q - off_v] — a per-target-pixel gather, no atomics (north_star (c)).
 // sigma_p^2 is selected exactly as the ceil(0.75 m)-th smallest key d^2 = D/n (the key is the
-// fp64 D/n, which orders distinct rationals with n <= 125 exactly) by a 63-step bitwise
-// rank search with REDUX.SUM per step.  Weights are round(exp(-a) 2^36) so that the sums are
-// exact int64 and do not depend on the reduction order (R26).
+// fp64 D/n, which orders distinct rationals with n <= 125 exactly) by a bitwise rank search with
+// one REDUX.SUM per bit: on the high 32 key bits from the first bit where the warp's keys differ,
+// and on the low 32 bits only if the selected high half is shared by unequal keys.  Weights are
+// round(exp(-a) 2^36) so that the sums are exact integers, independent of reduction order (R26);
+// they are summed as two 23-bit halves with REDUX.SUM.
 #include "common.cuh"
 
 namespace vinp {
@@ -23,6 +25,13 @@ __device__ __forceinline__ int64_t warp_sum64(int64_t v) {
 #pragma unroll
   for (int m = 16; m; m >>= 1) v += (int64_t)shfl_xor64((uint64_t)v, m);
   return v;
+}
+// exact warp sum of non-negative values < 2^46 (two 23-bit halves, each < 2^28 summed)
+__device__ __forceinline__ int64_t warp_sum46(int64_t v) {
+  uint32_t lo = (uint32_t)(v & 0x7fffff), hi = (uint32_t)(v >> 23);
+  lo = __reduce_add_sync(kFull, lo);
+  hi = __reduce_add_sync(kFull, hi);
+  return ((int64_t)hi << 23) + lo;
 }
 __device__ __forceinline__ uint64_t warp_min64(uint64_t v) {
 #pragma unroll
@@ -45,11 +54,13 @@ struct ReconArgs {
 };
 
 __global__ void __launch_bounds__(256) k_reconstruct(ReconArgs a, int mode, int layer_j, int32_t hb,
-                                                     int32_t he, float* __restrict__ out_rgb,
+                                                     int32_t he, const int32_t* __restrict__ list,
+                                                     float* __restrict__ out_rgb,
                                                      float* __restrict__ out_tex, int commit) {
   int lane = threadIdx.x & 31;
-  int h = hb + blockIdx.x * kWPB + (threadIdx.x >> 5);
-  if (h >= he) return;
+  int idx = hb + blockIdx.x * kWPB + (threadIdx.x >> 5);
+  if (idx >= he) return;
+  int h = list ? __ldg(list + idx) : idx;
   int p = a.holes[h];
   if (layer_j >= 0 && a.layer[p] != layer_j) return;
   int px, py, pt;
@@ -103,22 +114,58 @@ __global__ void __launch_bounds__(256) k_reconstruct(ReconArgs a, int mode, int 
 #pragma unroll
     for (int i = 0; i < 4; ++i) w[i] = (valid >> i) & 1;
   } else {
-    // sigma^2 key: the r-th smallest key, r = ceil(0.75 m) (nearest rank, R10)
+    // sigma^2 key: the r-th smallest key, r = ceil(0.75 m) (nearest rank, R10).  The key is the
+    // fp64 bit pattern of D/n (positive, so unsigned order = numeric order).  Rank search on the
+    // high 32 bits first, from the highest bit where the keys differ; only when keys sharing the
+    // selected high half differ in their low half is the low half searched as well.
     uint32_t r = (3 * m + 3) / 4;
-    uint64_t ans = 0;
-    for (int bit = 62; bit >= 0; --bit) {
-      uint64_t T = ans | ((1ull << bit) - 1);
+    uint32_t hi[4], lo[4];
+#pragma unroll
+    for (int i = 0; i < 4; ++i) {
+      hi[i] = (uint32_t)(key[i] >> 32);
+      lo[i] = (uint32_t)key[i];
+    }
+    uint32_t hmin = __reduce_min_sync(kFull, min(min(hi[0], hi[1]), min(hi[2], hi[3])));
+    uint32_t hmax = __reduce_max_sync(kFull, max(max((valid & 1) ? hi[0] : 0u, (valid & 2) ? hi[1] : 0u),
+                                                 max((valid & 4) ? hi[2] : 0u, (valid & 8) ? hi[3] : 0u)));
+    uint32_t ans = hmin & ~((hmax ^ hmin) ? (0xffffffffu >> __clz(hmax ^ hmin)) : 0u);
+    for (int bit = 31 - (hmax ^ hmin ? __clz(hmax ^ hmin) : 32); bit >= 0; --bit) {
+      uint32_t T = ans | ((1u << bit) - 1);
       uint32_t c = 0;
 #pragma unroll
-      for (int i = 0; i < 4; ++i) c += (valid >> i & 1) && key[i] <= T;
+      for (int i = 0; i < 4; ++i) c += hi[i] <= T;  // invalid keys are ~0: never counted (T < ~0)
       c = __reduce_add_sync(kFull, c);
-      if (c < r) ans |= 1ull << bit;
+      if (c < r) ans |= 1u << bit;
     }
-    // a representative (D_s, n_s) with key == ans
+    // keys whose high half equals ans: resolve the low half if they are not all equal
+    uint32_t below = 0, lmin = 0xffffffffu, lmax = 0;
+#pragma unroll
+    for (int i = 0; i < 4; ++i) {
+      below += hi[i] < ans;
+      if (hi[i] == ans && (valid >> i & 1)) { lmin = min(lmin, lo[i]); lmax = max(lmax, lo[i]); }
+    }
+    below = __reduce_add_sync(kFull, below);
+    lmin = __reduce_min_sync(kFull, lmin);
+    lmax = __reduce_max_sync(kFull, lmax);
+    uint32_t lans = lmin;
+    if (lmin != lmax) {
+      uint32_t r2 = r - below;
+      lans = lmin & ~(0xffffffffu >> __clz(lmax ^ lmin));
+      for (int bit = 31 - __clz(lmax ^ lmin); bit >= 0; --bit) {
+        uint32_t T = lans | ((1u << bit) - 1);
+        uint32_t c = 0;
+#pragma unroll
+        for (int i = 0; i < 4; ++i) c += (hi[i] == ans && (valid >> i & 1) && lo[i] <= T);
+        c = __reduce_add_sync(kFull, c);
+        if (c < r2) lans |= 1u << bit;
+      }
+    }
+    uint64_t kans = ((uint64_t)ans << 32) | lans;
+    // a representative (D_s, n_s) with key == kans (equal keys are equal rationals)
     int own = -1;
 #pragma unroll
     for (int i = 3; i >= 0; --i)
-      if ((valid >> i & 1) && key[i] == ans) own = i;
+      if ((valid >> i & 1) && key[i] == kans) own = i;
     unsigned bal = __ballot_sync(kFull, own >= 0);
     int src = __ffs(bal) - 1;
     uint32_t myD = 0, myn = 1;
@@ -139,6 +186,7 @@ __global__ void __launch_bounds__(256) k_reconstruct(ReconArgs a, int mode, int 
       }
     }
   }
+  // exact sums: per-lane partials (< 2^46) split into two 23-bit halves, each summed by REDUX
   int64_t S = 0, N[5] = {0, 0, 0, 0, 0};
 #pragma unroll
   for (int i = 0; i < 4; ++i) {
@@ -151,9 +199,9 @@ __global__ void __launch_bounds__(256) k_reconstruct(ReconArgs a, int mode, int 
     N[3] += w[i] * (int64_t)((x >> 32) & 255);
     N[4] += w[i] * (int64_t)((x >> 40) & 255);
   }
-  S = warp_sum64(S);
+  S = warp_sum46(S);
 #pragma unroll
-  for (int c = 0; c < 5; ++c) N[c] = warp_sum64(N[c]);
+  for (int c = 0; c < 5; ++c) N[c] = warp_sum46(N[c]);
   if (lane < 5) {
     int64_t Nc = lane == 0 ? N[0] : lane == 1 ? N[1] : lane == 2 ? N[2] : lane == 3 ? N[3] : N[4];
     float o = (float)__ddiv_rn((double)Nc, (double)S);
@@ -229,23 +277,34 @@ using namespace vinp;
 
 extern "C" {
 
-vinp_status vinp_reconstruct(vinp_level* lv, const vinp_nnf* nnf, int mode, int layer_j, int32_t hb,
-                             int32_t he, float* out_rgb, float* out_tex, int commit, void* stream) {
+}  // extern "C"
+
+namespace vinp {
+vinp_status launch_reconstruct(vinp_level* lv, const vinp_nnf* nnf, int mode, int layer_j, int32_t hb,
+                               int32_t he, const int32_t* list, float* out_rgb, float* out_tex,
+                               int commit, void* stream) {
   vinp_status st = check_level(lv, "vinp_reconstruct");
   if (st) return st;
   VINP_REQUIRE(nnf && nnf->e && nnf->n && out_rgb && out_tex && lv->holes && lv->slot,
                "vinp_reconstruct: null buffers");
   VINP_REQUIRE(mode == VINP_WEIGHTED || mode == VINP_UNWEIGHTED || mode == VINP_BEST_PATCH,
                "vinp_reconstruct: bad mode %d", mode);
-  VINP_REQUIRE(hb >= 0 && he <= lv->n_holes && hb <= he, "vinp_reconstruct: bad hole range");
+  VINP_REQUIRE(hb >= 0 && (list || he <= lv->n_holes) && hb <= he, "vinp_reconstruct: bad hole range");
   VINP_REQUIRE(layer_j < 0 || lv->layer, "vinp_reconstruct: layer map required");
   if (he > hb) {
     ReconArgs a{geo_of(lv), lv->vox, lv->layer, lv->slot, lv->holes, nnf->e, nnf->n};
-    k_reconstruct<<<nblk(he - hb, kWPB), 32 * kWPB, 0, S(stream)>>>(a, mode, layer_j, hb, he, out_rgb,
-                                                                  out_tex, commit);
+    k_reconstruct<<<nblk(he - hb, kWPB), 32 * kWPB, 0, S(stream)>>>(a, mode, layer_j, hb, he, list,
+                                                                  out_rgb, out_tex, commit);
     count_launch();
   }
   return check_launch("vinp_reconstruct");
+}
+}  // namespace vinp
+
+extern "C" {
+vinp_status vinp_reconstruct(vinp_level* lv, const vinp_nnf* nnf, int mode, int layer_j, int32_t hb,
+                             int32_t he, float* out_rgb, float* out_tex, int commit, void* stream) {
+  return launch_reconstruct(lv, nnf, mode, layer_j, hb, he, nullptr, out_rgb, out_tex, commit, stream);
 }
 
 vinp_status vinp_commit(vinp_level* lv, const float* out_rgb, const float* out_tex, int layer_j,

@@ -89,6 +89,7 @@ class Stats:
     onion_layers: int = 0
     setup_ms: float = 0.0
     total_ms: float = 0.0
+    onion_ms: float = 0.0
 
     @property
     def patch_updates(self):
@@ -116,6 +117,7 @@ class Inpainter:
         self.states: List[LevelState] = []
         self.stats = Stats()
         self.n_layers = 0
+        self.native = True  # False: every pass through its own C-ABI call (per-launch timing)
 
     # ------------------------------------------------------------------ setup (a1-a3)
     def load(self, rgb: torch.Tensor, mask: torch.Tensor):
@@ -149,7 +151,11 @@ class Inpainter:
     def ann_search(self, st: LevelState, outer_code: int, kb=-1, only_layer=-1, replicated=False):
         lv, prm, cfg = st.lv, self.prm, self.cfg
         n = lv.n_targets
-        b, e = (0, n) if replicated else self.ex.slab(n)
+        if self.native and (replicated or self.ex.world == 1):  # Alg. 1 in one native call
+            V.ann_search(lv, st.a, st.b, prm, outer_code, cfg.pm_iters, tuple(cfg.steps), kb, only_layer,
+                         self.counter)
+            return
+        b, e = self.ex.slab(n)
         gather = (lambda t: None) if replicated else (lambda t: self.ex.gather(t, n))
         V.nnf_evaluate(lv, st.a, prm, kb, only_layer, b, e, self.counter)
         gather(st.a.e)
@@ -176,8 +182,16 @@ class Inpainter:
 
     # ------------------------------------------------------------------ Alg. 3 onion peel
     def onion_peel(self):
+        """Alg. 3, replicated on every rank: one native call (per-layer index lists, all passes)."""
         st = self.states[-1]
         V.nnf_init_random(st.lv, st.a, self.prm, 0)  # phi^L <- Random (P:977)
+        V.onion_peel(st.lv, st.a, st.b, self.prm, self.cfg.pm_iters, self.n_layers, st.cur_rgb,
+                     st.cur_tex, tuple(self.cfg.steps), self.counter)
+
+    def onion_peel_stepwise(self):
+        """The same Alg. 3 through the per-pass C-ABI calls (only_layer filter); reference path."""
+        st = self.states[-1]
+        V.nnf_init_random(st.lv, st.a, self.prm, 0)
         for j in range(0, self.n_layers + 1):
             kb = max(j, 1)
             self.ann_search(st, V.ONION | j, kb=kb, only_layer=j, replicated=True)
@@ -195,10 +209,11 @@ class Inpainter:
         self.counter.zero_()
         e0 = ev(); e0.record()
         if cfg.onion:
-            self.onion_peel()
+            self.onion_peel() if self.native else self.onion_peel_stepwise()
         else:
             st = self.states[-1]
             V.nnf_init_random(st.lv, st.a, self.prm, 0)
+        e_on = ev(); e_on.record()
         pu_prev = 0
         for l in range(L, 0, -1):
             st = self.states[l - 1]
@@ -240,6 +255,7 @@ class Inpainter:
             for l, (a, b) in marks.items():
                 self.stats.levels[l - 1]["ms"] = a.elapsed_time(b)
             self.stats.total_ms = t_all0.elapsed_time(t_all1)
+            self.stats.onion_ms = t_all0.elapsed_time(e_on)
         pu = self.counter.clone()
         self.ex.allreduce_sum(pu)
         self.stats.total_patch_updates = int(pu.item())

@@ -14,7 +14,7 @@ from typing import Optional
 import torch
 
 HERE = os.path.dirname(os.path.abspath(__file__))
-LIB_PATH = os.path.join(HERE, "libvinp.so")
+LIB_PATH = os.environ.get("VINP_LIB_PATH") or os.path.join(HERE, "libvinp.so")  # override: A/B dev builds
 
 WEIGHTED, UNWEIGHTED, BEST_PATCH = 0, 1, 2
 ONION = 0x80000000  # outer_code marker for onion layer j: ONION | j
@@ -65,6 +65,8 @@ def _load():
         "vinp_propagate": (I, [P, P, P, P, I, I, I, I, I32, I32, P, P]),
         "vinp_random_search": (I, [P, P, P, P, U32, I, I, I, I32, I32, P, P]),
         "vinp_ann_search": (I, [P, P, P, P, U32, I, P, I, I, I, P, P]),
+        "vinp_onion_ws_bytes": (C.c_size_t, [P]),
+        "vinp_onion_peel": (I, [P, P, P, P, I, P, I, I, P, P, P, P, C.c_size_t, P]),
         "vinp_reconstruct": (I, [P, P, I, I, I32, I32, P, P, I, P]),
         "vinp_commit": (I, [P, P, P, I, I32, I32, P]),
         "vinp_change_l1": (I, [P, P, I64, P, P]),
@@ -87,6 +89,7 @@ EXPORTED = [
     "vinp_texture_ws_bytes", "vinp_texture_features", "vinp_sets_ws_bytes", "vinp_build_sets",
     "vinp_build_lists", "vinp_layers", "vinp_nnf_init_random", "vinp_nnf_upsample",
     "vinp_nnf_evaluate", "vinp_propagate", "vinp_random_search", "vinp_ann_search",
+    "vinp_onion_ws_bytes", "vinp_onion_peel",
     "vinp_reconstruct", "vinp_commit", "vinp_change_l1", "vinp_energy",
     "vinp_brute_force_ws_bytes", "vinp_brute_force", "vinp_patch_ssd", "vinp_philox"]
 
@@ -284,6 +287,16 @@ def ann_search(lv, a, b, prm, outer_code, K, steps=(8, 4, 2, 1), kb=-1, only_lay
     _check(_lib.vinp_ann_search(lv.struct(), a.struct(), b.struct(), C.byref(prm.struct()), outer_code,
                                 K, st, len(steps), kb, only_layer, _ptr(counter), _stream()),
            "vinp_ann_search")
+
+
+def onion_peel(lv, a, b, prm, K, n_layers, out_rgb, out_tex, steps=(8, 4, 2, 1), counter=None, ws=None):
+    nbytes = int(_lib.vinp_onion_ws_bytes(lv.struct()))
+    if ws is None or ws.numel() < nbytes:
+        ws = torch.empty(nbytes, dtype=torch.uint8, device=lv.device)
+    st = (C.c_int32 * len(steps))(*steps)
+    _check(_lib.vinp_onion_peel(lv.struct(), a.struct(), b.struct(), C.byref(prm.struct()), K, st,
+                                len(steps), n_layers, _ptr(out_rgb), _ptr(out_tex), _ptr(counter),
+                                _ptr(ws), ws.numel(), _stream()), "vinp_onion_peel")
 
 
 def reconstruct(lv, nnf, mode, out_rgb, out_tex, layer_j=-1, hb=0, he=None, commit=True):

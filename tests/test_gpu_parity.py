@@ -326,3 +326,23 @@ def test_pipeline_two_levels_end_to_end(orc):
     ref, st = orc.inpaint(v.numpy(), m.numpy(), 2, pm_iters=3, max_outer=4)
     assert [l["outer"] for l in stats.levels] == st["outer_iters"]
     assert np.array_equal(out.cpu().numpy(), ref)
+
+
+def test_native_onion_peel_equals_stepwise(V):
+    """vinp_onion_peel (per-layer lists, one call) == the per-pass only_layer path, bit for bit."""
+    from paper_1503_05528_b200 import Config, Inpainter
+    v, m, _ = generate("c2")
+    T, H, W, _ = v.shape
+    res = []
+    for native in (True, False):
+        ip = Inpainter(W, H, T, Config(levels=2, pm_iters=3), "cuda")
+        ip.load(v.cuda(), m.cuda())
+        ip.counter.zero_()
+        (ip.onion_peel if native else ip.onion_peel_stepwise)()
+        st = ip.states[-1]
+        torch.cuda.synchronize()
+        res.append((st.a.e.clone(), st.a.n.clone(), st.cur_rgb.clone(), st.cur_tex.clone(),
+                    st.lv.vox.clone(), int(ip.counter.item())))
+    for x, y in zip(res[0][:5], res[1][:5]):
+        assert torch.equal(x, y)
+    assert res[0][5] == res[1][5]

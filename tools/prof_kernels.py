@@ -1,0 +1,69 @@
+"""Per-kernel timing of the level-1 PatchMatch passes on a bench config (default c5), for ncu.
+
+Loads the config, runs `--warm` PatchMatch iterations at level 1 from random init (to reach a
+representative NNF), then times one evaluate + one PM iteration (J propagation passes + one
+random search) + one weighted reconstruction with CUDA events and prints per-kernel ms and
+model GB/s.  Under ncu, select the timed launches with e.g.
+  ncu -k regex:k_random_search -s <warm> -c 1 python tools/prof_kernels.py
+"""
+import argparse
+import json
+import os
+import sys
+
+import torch
+
+ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+sys.path.insert(0, ROOT)
+
+from gen.synth import CONFIGS, generate  # noqa: E402
+from paper_1503_05528_b200 import Config, Inpainter, vinp as V  # noqa: E402
+
+
+def main():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--config", default="c5")
+    ap.add_argument("--warm", type=int, default=3)
+    ap.add_argument("--level", type=int, default=1)
+    args = ap.parse_args()
+    c = CONFIGS[args.config]
+    v, m, _ = generate(args.config, device="cuda")
+    ip = Inpainter(c.W, c.H, c.T, Config(levels=c.levels, lam=c.lam, seed=c.seed), "cuda")
+    ip.load(v, m)
+    st = ip.states[args.level - 1]
+    lv = st.lv
+    V.nnf_init_random(lv, st.a, ip.prm, 0)
+    V.ann_search(lv, st.a, st.b, ip.prm, 0, args.warm)
+    torch.cuda.synchronize()
+    cnt = torch.zeros(1, dtype=torch.int64, device="cuda")
+    res = []
+
+    def timed(name, fn, slots, per_slot=29):
+        cnt.zero_()
+        a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        a.record()
+        fn()
+        b.record()
+        torch.cuda.synchronize()
+        ms = a.elapsed_time(b)
+        pu = int(cnt.item())
+        by = 625 * pu + per_slot * slots
+        res.append(dict(kernel=name, ms=round(ms, 3), patch_updates=pu, model_GBps=round(by / ms / 1e6, 1),
+                        pu_per_s=round(pu / ms * 1e3 / 1e9, 3)))
+
+    n = lv.n_targets
+    timed("evaluate", lambda: V.nnf_evaluate(lv, st.a, ip.prm, counter=cnt), n)
+    k = args.warm + 1
+    sign = 1 if k % 2 else -1
+    for s in (8, 4, 2, 1):
+        timed(f"propagate_s{s}", lambda: V.propagate(lv, st.a, st.b, ip.prm, s, sign, counter=cnt), n)
+        st.a, st.b = st.b, st.a
+    timed("random_search", lambda: V.random_search(lv, st.a, st.b, ip.prm, 0, k, counter=cnt), n)
+    st.a, st.b = st.b, st.a
+    nh = lv.n_holes
+    timed("reconstruct", lambda: V.reconstruct(lv, st.a, V.WEIGHTED, st.cur_rgb, st.cur_tex), nh, 662)
+    print(json.dumps(dict(config=args.config, level=args.level, targets=n, holes=nh, kernels=res)))
+
+
+if __name__ == "__main__":
+    main()
