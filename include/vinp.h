@@ -134,7 +134,7 @@ vinp_status vinp_nnf_evaluate(const vinp_level* lv, vinp_nnf* nnf, const vinp_pa
 
 /* ---- a6: propagation, one Jacobi jump pass (Alg. 1; R2, R5, R6, R25) ----
  * Candidates in rank order: 0 = in(p); 1..3 = in(p + sign*step*e_x / e_y / e_t) for neighbours in
- * Omega and H~.  A candidate is evaluated iff q = p + v is in Omega and D~ and v differs from the
+ * Omega and H~ (sign = 0: 1..6 = the -step then the +step neighbours).  A candidate is evaluated iff q = p + v is in Omega and D~ and v differs from the
  * incumbent and from every earlier valid candidate; strict improvement wins.  Reads `in`, writes
  * `out` for slots [b, e).  counter (device, may be NULL) += evaluated candidates. */
 vinp_status vinp_propagate(const vinp_level* lv, const vinp_nnf* in, vinp_nnf* out,
@@ -151,11 +151,13 @@ vinp_status vinp_random_search(const vinp_level* lv, const vinp_nnf* in, vinp_nn
                                void* stream);
 
 /* ---- a8: ANN search (Alg. 1), single GPU: evaluate, then for k = 1..K: for each step
- * s in steps: propagate(s, sign = +1 for odd k, -1 for even k); random_search(k).  Uses `b` as the
- * ping-pong buffer; the result is in `a`. */
+ * s in steps: propagate(s, sign); random_search(k).  sign_policy 0: sign = +1 for odd k, -1 for
+ * even k (Alg. 1's alternation, R5); 1: sign = 0 (both directions) on every pass (R6).  Uses `b`
+ * as the ping-pong buffer; the result is in `a`. */
 vinp_status vinp_ann_search(const vinp_level* lv, vinp_nnf* a, vinp_nnf* b, const vinp_params* prm,
-                            uint32_t outer_code, int K, const int32_t* steps, int n_steps, int kb,
-                            int only_layer, unsigned long long* counter, void* stream);
+                            uint32_t outer_code, int K, const int32_t* steps, int n_steps,
+                            int sign_policy, int kb, int only_layer, unsigned long long* counter,
+                            void* stream);
 
 /* ---- a9/a10: reconstruction (Eqs. 4-5, Eq. 6, Eq. 11, Eq. 13
  * P:829-832; R10-R13, R20, R26, R27) ----
@@ -180,7 +182,7 @@ vinp_status vinp_commit(vinp_level* lv, const float* out_rgb, const float* out_t
  * (vinp_onion_ws_bytes); synchronises once.  Result NNF in `a`; `b` is scratch. */
 size_t vinp_onion_ws_bytes(const vinp_level* lv);
 vinp_status vinp_onion_peel(vinp_level* lv, vinp_nnf* a, vinp_nnf* b, const vinp_params* prm, int K,
-                            const int32_t* steps, int n_steps, int n_layers, float* out_rgb,
+                            const int32_t* steps, int n_steps, int sign_policy, int n_layers, float* out_rgb,
                             float* out_tex, unsigned long long* counter, void* ws, size_t ws_bytes,
                             void* stream);
 

@@ -367,7 +367,8 @@ static void copy_entry(const or_nnf* in, or_nnf* out, int32_t s) {
 
 /* ------------------------------------------------------------------------------------------
  * a6  Propagation, P:371-386 / Alg. 1, as one Jacobi jump pass (R6): candidates in
- * rank order 0 = incumbent phi_in(p); 1,2,3 = phi_in(p + sign*step*e_x / e_y / e_t), each only if
+ * rank order 0 = incumbent phi_in(p); 1,2,3 = phi_in(p + sign*step*e_x / e_y / e_t) (sign = 0:
+ * 1..6 = the -step then the +step neighbours), each only if
  * that neighbour is in Omega and in H~.  A candidate is evaluated only if p+v is in Omega and in
  * D~ (R2) and v differs from the incumbent and from every earlier valid candidate; it replaces the
  * best if its distance is strictly smaller (R25).  Returns the number of evaluated candidates.
@@ -382,14 +383,19 @@ int64_t or_propagate(const or_level* lv, const or_nnf* in, or_nnf* out, int lamb
     if (!in_layer(lv, p, only_layer)) continue;
     int px, py, pt;
     coords(lv, p, &px, &py, &pt);
-    int seen[4][3];
+    int seen[7][3];
     int nseen = 0;
     seen[nseen][0] = in->dx[s]; seen[nseen][1] = in->dy[s]; seen[nseen][2] = in->dt[s]; ++nseen;
     uint32_t bestD = in->D[s];
-    for (int a = 0; a < 3; ++a) {
-      int rx = px + (a == 0 ? sign * step : 0);
-      int ry = py + (a == 1 ? sign * step : 0);
-      int rt = pt + (a == 2 ? sign * step : 0);
+    /* sign = +1 / -1: the 3 neighbours p + sign*step*e_{x,y,t}; sign = 0 ("both", R6): the 6
+     * neighbours p - step*e_{x,y,t} then p + step*e_{x,y,t}, in that rank order */
+    int nc = sign == 0 ? 6 : 3;
+    for (int a = 0; a < nc; ++a) {
+      int sg = sign != 0 ? sign : (a < 3 ? -1 : 1);
+      int ax = a % 3;
+      int rx = px + (ax == 0 ? sg * step : 0);
+      int ry = py + (ax == 1 ? sg * step : 0);
+      int rt = pt + (ax == 2 ? sg * step : 0);
       if (!inside(lv, rx, ry, rt)) continue;
       int32_t rs = lv->slot[lin(lv, rx, ry, rt)];
       if (rs < 0) continue; /* neighbour not in H~ */
@@ -659,7 +665,8 @@ static void copy_nnf(const or_nnf* a, or_nnf* b, int32_t n) {
 }
 
 /* ANN search, Alg. 1 with R3/R5/R6: evaluate; for k = 1..K: for s in steps: propagate(s, sigma_k)
- * with sigma_k = +1 for odd k and -1 for even k; random_search(k).  Result in w->a. */
+ * with sigma_k = +1 for odd k and -1 for even k (sign_policy 0) or 0 = both directions
+ * (sign_policy 1); random_search(k).  Result in w->a. */
 static int64_t ann_search(or_work* w, const or_params* prm, int level, uint32_t oc, int kb, int ol) {
   or_level* lv = &w->lv;
   int32_t n = lv->n_targets;
@@ -667,7 +674,7 @@ static int64_t ann_search(or_work* w, const or_params* prm, int level, uint32_t 
   if (lv->T > rmax) rmax = lv->T;
   int64_t cnt = or_nnf_evaluate(lv, &w->a, prm->lambda, kb, ol, 0, n);
   for (int k = 1; k <= prm->pm_iters; ++k) {
-    int sign = (k % 2 == 1) ? 1 : -1;
+    int sign = prm->sign_policy ? 0 : ((k % 2 == 1) ? 1 : -1);
     for (int i = 0; i < prm->n_steps; ++i) {
       cnt += or_propagate(lv, &w->a, &w->b, prm->lambda, prm->steps[i], sign, kb, ol, 0, n);
       copy_nnf(&w->b, &w->a, n);

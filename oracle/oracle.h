@@ -83,7 +83,7 @@ int64_t or_brute_force(const or_level* lv, or_nnf* out, int lambda, int32_t b, i
 
 /* Whole Alg. 4 (without alignment) on host buffers; returns 0 on success. */
 typedef struct {
-  int levels, pm_iters, fixed_outer, max_outer, lambda, tex_half, n_steps;
+  int levels, pm_iters, fixed_outer, max_outer, lambda, tex_half, n_steps, sign_policy;
   int steps[8];
   uint64_t seed;
   double rho;

@@ -46,7 +46,7 @@ class OrNNF(C.Structure):
 class OrParams(C.Structure):
     _fields_ = [("levels", C.c_int), ("pm_iters", C.c_int), ("fixed_outer", C.c_int),
                 ("max_outer", C.c_int), ("lambda_", C.c_int), ("tex_half", C.c_int),
-                ("n_steps", C.c_int), ("steps", C.c_int * 8), ("seed", C.c_uint64),
+                ("n_steps", C.c_int), ("sign_policy", C.c_int), ("steps", C.c_int * 8), ("seed", C.c_uint64),
                 ("rho", C.c_double)]
 
 
@@ -260,12 +260,12 @@ WEIGHTED, UNWEIGHTED, BEST_PATCH = 0, 1, 2
 
 
 def ann_search(lv, a: NNF, lam, seed, level, outer_code, pm_iters, steps=(8, 4, 2, 1), rho=0.5,
-               kb=-1, ol=-1):
+               kb=-1, ol=-1, sign_policy=0):
     """Alg. 1 schedule (R3/R5/R6), same as or_inpaint's internal ann_search; result in ``a``."""
     b = a.copy()
     cnt = evaluate(lv, a, lam, kb, ol)
     for k in range(1, pm_iters + 1):
-        sign = 1 if k % 2 == 1 else -1
+        sign = 0 if sign_policy else (1 if k % 2 == 1 else -1)
         for s in steps:
             cnt += propagate(lv, a, b, lam, s, sign, kb, ol)
             a, b = b, a
@@ -275,11 +275,11 @@ def ann_search(lv, a: NNF, lam, seed, level, outer_code, pm_iters, steps=(8, 4, 
 
 
 def inpaint(rgb, occ, levels, pm_iters=10, fixed_outer=0, max_outer=20, lam=50, seed=1,
-            steps=(8, 4, 2, 1), rho=0.5, tex_half=-1):
+            steps=(8, 4, 2, 1), rho=0.5, tex_half=-1, sign_policy=0):
     T, H, W, _ = rgb.shape
     prm = OrParams()
     prm.levels, prm.pm_iters, prm.fixed_outer, prm.max_outer = levels, pm_iters, fixed_outer, max_outer
-    prm.lambda_, prm.tex_half, prm.n_steps = lam, tex_half, len(steps)
+    prm.lambda_, prm.tex_half, prm.n_steps, prm.sign_policy = lam, tex_half, len(steps), sign_policy
     for i, s in enumerate(steps):
         prm.steps[i] = s
     prm.seed, prm.rho = seed, rho

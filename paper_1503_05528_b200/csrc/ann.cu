@@ -194,14 +194,21 @@ __global__ void __launch_bounds__(256) k_propagate(LevelArgs a, const uint64_t* 
   int p = have ? __ldg(a.targets + s) : 0;
   uint64_t inc = have ? __ldg(reinterpret_cast<const unsigned long long*>(ein) + s) : 0ull;
   bool act = have && (only_layer < 0 || a.layer[p] == only_layer);
-  int q[3] = {-1, -1, -1};
+  // sign = +1 / -1: neighbours p + sign*step*e_{x,y,t}; sign = 0 ("both"): p - step*e_{x,y,t}
+  // then p + step*e_{x,y,t} (rank order 1..6)
+  constexpr int NCMAX = 6;
+  const int nc = sign == 0 ? 6 : 3;
+  int q[NCMAX] = {-1, -1, -1, -1, -1, -1};
   int px = 0, py = 0, pt = 0;
   int q0 = e_q(inc);
   if (act) {
     decode(a.g, p, px, py, pt);
 #pragma unroll
-    for (int c = 0; c < 3; ++c) {
-      int ox = c == 0 ? sign * step : 0, oy = c == 1 ? sign * step : 0, ot = c == 2 ? sign * step : 0;
+    for (int c = 0; c < NCMAX; ++c) {
+      if (c >= nc) break;
+      int sg = sign != 0 ? sign : (c < 3 ? -1 : 1);
+      int ax = c % 3;
+      int ox = ax == 0 ? sg * step : 0, oy = ax == 1 ? sg * step : 0, ot = ax == 2 ? sg * step : 0;
       int rx = px + ox, ry = py + oy, rt = pt + ot;
       if (inside(a.g, rx, ry, rt)) {
         int rs = __ldg(a.slot + lin(a.g, rx, ry, rt));
@@ -214,9 +221,14 @@ __global__ void __launch_bounds__(256) k_propagate(LevelArgs a, const uint64_t* 
         }
       }
     }
-    if (q[0] == q0) q[0] = -1;
-    if (q[1] == q0 || q[1] == q[0]) q[1] = -1;
-    if (q[2] == q0 || q[2] == q[0] || q[2] == q[1]) q[2] = -1;
+    // keep a candidate only if it differs from the incumbent and every earlier valid candidate
+#pragma unroll
+    for (int c = NCMAX - 1; c >= 0; --c) {
+      bool dup = q[c] == q0;
+#pragma unroll
+      for (int c2 = 0; c2 < c; ++c2) dup |= (q[c2] == q[c]);
+      if (dup) q[c] = -1;
+    }
   }
   uint32_t bestD = e_D(inc);
   int bestq = q0;
@@ -225,7 +237,7 @@ __global__ void __launch_bounds__(256) k_propagate(LevelArgs a, const uint64_t* 
               pt < a.g.T - 2;
   bool allfull = __all_sync(kFull, full || !act);
 #pragma unroll
-  for (int c = 0; c < 3; ++c) {
+  for (int c = 0; c < NCMAX; ++c) {
     bool mine = act && q[c] >= 0;
     if (!__any_sync(kFull, mine)) continue;
     if (mine) {
@@ -385,11 +397,14 @@ __global__ void __launch_bounds__(32 * WPB, VINP_MINB * 8 / WPB) k_random_search
 }
 
 // ------------------------------------------------------------------ a13: brute force (CUDA cores)
-// One block of 8 warps per target; warp w scans sources i = w, w+8, ... in increasing order and
-// keeps its first minimum; the block then takes the lexicographic min of (D, i).
+// One block of 8 warps per target; warp w scans sources i = w, w+8, ... in increasing order, 8 at a
+// time with all gathers of a 32-voxel chunk in flight, and keeps its first minimum (strict <).
+// Exact partial-distance elimination: a source whose partial sum reaches the warp's best so far
+// cannot become the (first) minimum.  The block then takes the lexicographic min of (D, i).
 __global__ void __launch_bounds__(256) k_brute_force(LevelArgs a, uint64_t* __restrict__ ee,
                                                      uint8_t* __restrict__ en, int lambda, int32_t b,
                                                      int32_t e) {
+  constexpr int G = 8;
   int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
   int s = b + blockIdx.x;
   if (s >= e) return;
@@ -400,31 +415,55 @@ __global__ void __launch_bounds__(256) k_brute_force(LevelArgs a, uint64_t* __re
   decode(a.g, p, px, py, pt);
   TargetPatch tp;
   load_target(tp, L, a.g, a.vox, a.layer, -1, p, px, py, pt);
-  uint64_t best = ~0ull;  // (D << 32) | i
-  int i = w;
-  for (; i + kWarpsPerBlock < a.n_sources; i += 2 * kWarpsPerBlock) {
-    uint32_t D0, D1;
-    warp_ssd2(tp, L, a.vox, a.sources[i], a.sources[i + kWarpsPerBlock], lambda, D0, D1);
-    uint64_t k0 = ((uint64_t)D0 << 32) | (uint32_t)i;
-    uint64_t k1 = ((uint64_t)D1 << 32) | (uint32_t)(i + kWarpsPerBlock);
-    best = min(best, min(k0, k1));
-  }
-  for (; i < a.n_sources; i += kWarpsPerBlock) {
-    uint32_t D0 = warp_ssd(tp, L, a.vox, a.sources[i], lambda);
-    best = min(best, ((uint64_t)D0 << 32) | (uint32_t)i);
+  const unsigned long long* v = reinterpret_cast<const unsigned long long*>(a.vox);
+  uint32_t bestD = 0xffffffffu;
+  int bestI = 0x7fffffff;
+  for (int i0 = w; i0 < a.n_sources; i0 += G * kWarpsPerBlock) {
+    int q[G];
+    uint32_t part[G];
+    unsigned alive = 0;
+#pragma unroll
+    for (int c = 0; c < G; ++c) {
+      int i = i0 + c * kWarpsPerBlock;
+      bool ok = i < a.n_sources;
+      q[c] = ok ? __ldg(a.sources + i) : 0;
+      part[c] = 0;
+      alive |= (unsigned)ok << c;
+    }
+    uint32_t thr = bestD;
+#pragma unroll
+    for (int ch = 0; ch < 4; ++ch) {
+      if (!alive) break;
+      bool m = (tp.mask >> ch) & 1;
+      uint64_t sv[G];
+#pragma unroll
+      for (int c = 0; c < G; ++c) sv[c] = (m && ((alive >> c) & 1)) ? __ldg(v + q[c] + L.off[ch]) : 0ull;
+#pragma unroll
+      for (int c = 0; c < G; ++c) {
+        if ((alive >> c) & 1) {
+          uint32_t x = m ? voxel_cost(tp.c[ch], tp.t[ch], sv[c], lambda) : 0u;
+          part[c] += __reduce_add_sync(kFull, x);
+          if (part[c] >= thr) alive &= ~(1u << c);
+        }
+      }
+    }
+#pragma unroll
+    for (int c = 0; c < G; ++c)
+      if (((alive >> c) & 1) && part[c] < bestD) {
+        bestD = part[c];
+        bestI = i0 + c * kWarpsPerBlock;
+      }
   }
   __shared__ unsigned long long red[kWarpsPerBlock];
-  if (lane == 0) red[w] = best;
+  if (lane == 0) red[w] = ((uint64_t)bestD << 32) | (uint32_t)bestI;
   __syncthreads();
-  if (threadIdx.x == 0) {
-    uint64_t m = red[0];
-    for (int k = 1; k < kWarpsPerBlock; ++k) m = min(m, (uint64_t)red[k]);
-    uint32_t n = 0;
-    (void)n;
-    ee[s] = pack_e((uint32_t)(m >> 32), a.sources[(uint32_t)m]);
-  }
   uint32_t n = __reduce_add_sync(kFull, (uint32_t)__popc(tp.mask));
-  if (threadIdx.x == 0) en[s] = (uint8_t)n;
+  if (threadIdx.x == 0) {
+    uint64_t mn = red[0];
+    for (int k = 1; k < kWarpsPerBlock; ++k) mn = min(mn, (uint64_t)red[k]);
+    ee[s] = pack_e((uint32_t)(mn >> 32), a.sources[(uint32_t)mn]);
+    en[s] = (uint8_t)n;
+  }
 }
 
 // ------------------------------------------------------------------ test hooks
@@ -555,7 +594,7 @@ vinp_status launch_propagate(const vinp_level* lv, const vinp_nnf* in, vinp_nnf*
   vinp_status st = check_nnf_args(lv, "vinp_propagate", list ? 0 : b, list ? 0 : e, prm);
   if (st) return st;
   VINP_REQUIRE(in && in->e && out && out->e && in->e != out->e, "vinp_propagate: need two buffers");
-  VINP_REQUIRE(step >= 1 && (sign == 1 || sign == -1), "vinp_propagate: bad step/sign");
+  VINP_REQUIRE(step >= 1 && sign >= -1 && sign <= 1, "vinp_propagate: bad step/sign");
   VINP_REQUIRE((kb < 0 && only_layer < 0) || lv->layer, "vinp_propagate: layer map required");
   if (e > b) {
     k_propagate<<<nblk(e - b, 256), 256, 0, S(stream)>>>(
@@ -628,15 +667,17 @@ vinp_status vinp_random_search(const vinp_level* lv, const vinp_nnf* in, vinp_nn
 }
 
 vinp_status vinp_ann_search(const vinp_level* lv, vinp_nnf* a, vinp_nnf* b, const vinp_params* prm,
-                            uint32_t outer_code, int K, const int32_t* steps, int n_steps, int kb,
-                            int only_layer, unsigned long long* counter, void* stream) {
+                            uint32_t outer_code, int K, const int32_t* steps, int n_steps,
+                            int sign_policy, int kb, int only_layer, unsigned long long* counter,
+                            void* stream) {
+  VINP_REQUIRE(sign_policy == 0 || sign_policy == 1, "vinp_ann_search: bad sign_policy");
   VINP_REQUIRE(a && b && steps && n_steps >= 0 && n_steps <= 16 && K >= 0, "vinp_ann_search: bad args");
   vinp_status st = vinp_nnf_evaluate(lv, a, prm, kb, only_layer, 0, lv->n_targets, counter, stream);
   if (st) return st;
   vinp_nnf* cur = a;
   vinp_nnf* nxt = b;
   for (int k = 1; k <= K; ++k) {
-    int sign = (k % 2 == 1) ? 1 : -1;
+    int sign = sign_policy ? 0 : ((k % 2 == 1) ? 1 : -1);
     for (int i = 0; i < n_steps; ++i) {
       st = vinp_propagate(lv, cur, nxt, prm, steps[i], sign, kb, only_layer, 0, lv->n_targets,
                           counter, stream);

@@ -147,7 +147,7 @@ size_t vinp_onion_ws_bytes(const vinp_level* lv) {
 }
 
 vinp_status vinp_onion_peel(vinp_level* lv, vinp_nnf* a, vinp_nnf* b, const vinp_params* prm, int K,
-                            const int32_t* steps, int n_steps, int n_layers, float* out_rgb,
+                            const int32_t* steps, int n_steps, int sign_policy, int n_layers, float* out_rgb,
                             float* out_tex, unsigned long long* counter, void* ws, size_t ws_bytes,
                             void* stream) {
   vinp_status st = check_level(lv, "vinp_onion_peel");
@@ -199,7 +199,7 @@ vinp_status vinp_onion_peel(vinp_level* lv, vinp_nnf* a, vinp_nnf* b, const vinp
       st = launch_evaluate(lv, cur, prm, kb, j, tb, te, tlist, counter, stream);
       if (st) return st;
       for (int k = 1; k <= K; ++k) {
-        int sign = (k % 2 == 1) ? 1 : -1;
+        int sign = sign_policy ? 0 : ((k % 2 == 1) ? 1 : -1);
         for (int i = 0; i < n_steps; ++i) {
           st = launch_propagate(lv, cur, nxt, prm, steps[i], sign, kb, j, tb, te, tlist, counter, stream);
           if (st) return st;

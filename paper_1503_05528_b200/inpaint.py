@@ -31,6 +31,7 @@ class Config:
     lam: int = 50
     seed: int = 1
     steps: Sequence[int] = (8, 4, 2, 1)  # jump-flood steps per PM iteration (R6)
+    sign_policy: int = 0        # 0: Alg. 1 alternation (R5); 1: both directions every pass (R6)
     rho: float = 0.5
     tex_half: int = -1          # R15
     onion: bool = True          # Alg. 3 initialisation at the coarsest level
@@ -99,7 +100,11 @@ class Stats:
 class Inpainter:
     """Holds the pyramid of one video in HBM and runs Alg. 4 on it."""
 
-    def __init__(self, W: int, H: int, T: int, cfg: Config, device="cuda", exchange: Exchange = None):
+    def __init__(self, W: int, H: int, T: int, cfg: Config, device="cuda", exchange: Exchange = None,
+                 ops=None):
+        """ops: the kernel module (default: the libvinp binding).  Tests substitute an oracle-backed
+        module with the same call signatures to exercise the multi-rank logic on CPU (gloo)."""
+        self.V = ops or V
         self.W, self.H, self.T, self.cfg = W, H, T, cfg
         self.device = torch.device(device)
         self.ex = exchange or Exchange()
@@ -110,7 +115,7 @@ class Inpainter:
             self.levels.append(V.Level.alloc(w, h, T, l, self.device))
             w, h = (w + 1) // 2, (h + 1) // 2
         n1 = W * H * T
-        self.ws = torch.empty(max(V.texture_ws_bytes(self.levels[0]), V.sets_ws_bytes(self.levels[0])) + 256,
+        self.ws = torch.empty(max(self.V.texture_ws_bytes(self.levels[0]), self.V.sets_ws_bytes(self.levels[0])) + 256,
                               dtype=torch.uint8, device=self.device)
         self.counter = torch.zeros(1, dtype=torch.int64, device=self.device)
         self.change = torch.zeros(1, dtype=torch.int64, device=self.device)
@@ -125,14 +130,14 @@ class Inpainter:
         assert rgb.shape == (self.T, self.H, self.W, 3) and mask.shape == (self.T, self.H, self.W)
         rgb = rgb.contiguous()
         mask = mask.contiguous()
-        V.build_pyramid(rgb, mask, self.levels)
-        V.texture_features(self.prm, self.levels, self.ws)
-        counts = V.build_sets(self.levels, self.ws)
+        self.V.build_pyramid(rgb, mask, self.levels)
+        self.V.texture_features(self.prm, self.levels, self.ws)
+        counts = self.V.build_sets(self.levels, self.ws)
         for lv in self.levels:
             if lv.n_sources == 0:
                 raise V.VinpError(f"D~ is empty at level {lv.level} (S:237)")
             lv.alloc_lists()
-        V.build_lists(self.levels, self.ws)
+        self.V.build_lists(self.levels, self.ws)
         self.states = []
         for lv in self.levels:
             npad = self.ex.padded(lv.n_targets)
@@ -143,7 +148,7 @@ class Inpainter:
             self.states.append(LevelState(lv, a, b, z(3), z(2), z(3), z(2)))
         top = self.levels[-1]
         top.layer = torch.empty(top.N, dtype=torch.uint8, device=self.device)
-        self.n_layers = V.layers(top, self.ws)
+        self.n_layers = self.V.layers(top, self.ws)
         self.stats.onion_layers = self.n_layers
         return counts
 
@@ -152,21 +157,21 @@ class Inpainter:
         lv, prm, cfg = st.lv, self.prm, self.cfg
         n = lv.n_targets
         if self.native and (replicated or self.ex.world == 1):  # Alg. 1 in one native call
-            V.ann_search(lv, st.a, st.b, prm, outer_code, cfg.pm_iters, tuple(cfg.steps), kb, only_layer,
-                         self.counter)
+            self.V.ann_search(lv, st.a, st.b, prm, outer_code, cfg.pm_iters, tuple(cfg.steps), kb, only_layer,
+                              self.counter, sign_policy=cfg.sign_policy)
             return
         b, e = self.ex.slab(n)
         gather = (lambda t: None) if replicated else (lambda t: self.ex.gather(t, n))
-        V.nnf_evaluate(lv, st.a, prm, kb, only_layer, b, e, self.counter)
+        self.V.nnf_evaluate(lv, st.a, prm, kb, only_layer, b, e, self.counter)
         gather(st.a.e)
         gather(st.a.n)
         for k in range(1, cfg.pm_iters + 1):
-            sign = 1 if k % 2 == 1 else -1
+            sign = 0 if cfg.sign_policy else (1 if k % 2 == 1 else -1)
             for s in cfg.steps:
-                V.propagate(lv, st.a, st.b, prm, s, sign, kb, only_layer, b, e, self.counter)
+                self.V.propagate(lv, st.a, st.b, prm, s, sign, kb, only_layer, b, e, self.counter)
                 st.a, st.b = st.b, st.a
                 gather(st.a.e)
-            V.random_search(lv, st.a, st.b, prm, outer_code, k, kb, only_layer, b, e, self.counter)
+            self.V.random_search(lv, st.a, st.b, prm, outer_code, k, kb, only_layer, b, e, self.counter)
             st.a, st.b = st.b, st.a
             gather(st.a.e)
 
@@ -174,24 +179,24 @@ class Inpainter:
         lv = st.lv
         n = lv.n_holes
         hb, he = (0, n) if replicated else self.ex.slab(n)
-        V.reconstruct(lv, st.a, mode, st.cur_rgb, st.cur_tex, layer_j, hb, he, commit=True)
+        self.V.reconstruct(lv, st.a, mode, st.cur_rgb, st.cur_tex, layer_j, hb, he, commit=True)
         if not replicated and self.ex.world > 1:
             self.ex.gather(st.cur_rgb, n)
             self.ex.gather(st.cur_tex, n)
-            V.commit(lv, st.cur_rgb, st.cur_tex, layer_j, 0, n)
+            self.V.commit(lv, st.cur_rgb, st.cur_tex, layer_j, 0, n)
 
     # ------------------------------------------------------------------ Alg. 3 onion peel
     def onion_peel(self):
         """Alg. 3, replicated on every rank: one native call (per-layer index lists, all passes)."""
         st = self.states[-1]
-        V.nnf_init_random(st.lv, st.a, self.prm, 0)  # phi^L <- Random (P:977)
-        V.onion_peel(st.lv, st.a, st.b, self.prm, self.cfg.pm_iters, self.n_layers, st.cur_rgb,
-                     st.cur_tex, tuple(self.cfg.steps), self.counter)
+        self.V.nnf_init_random(st.lv, st.a, self.prm, 0)  # phi^L <- Random (P:977)
+        self.V.onion_peel(st.lv, st.a, st.b, self.prm, self.cfg.pm_iters, self.n_layers, st.cur_rgb,
+                          st.cur_tex, tuple(self.cfg.steps), self.counter, sign_policy=self.cfg.sign_policy)
 
     def onion_peel_stepwise(self):
         """The same Alg. 3 through the per-pass C-ABI calls (only_layer filter); reference path."""
         st = self.states[-1]
-        V.nnf_init_random(st.lv, st.a, self.prm, 0)
+        self.V.nnf_init_random(st.lv, st.a, self.prm, 0)
         for j in range(0, self.n_layers + 1):
             kb = max(j, 1)
             self.ann_search(st, V.ONION | j, kb=kb, only_layer=j, replicated=True)
@@ -202,7 +207,14 @@ class Inpainter:
     def run(self, timing=True) -> Stats:
         cfg = self.cfg
         L = cfg.levels
-        ev = lambda: torch.cuda.Event(enable_timing=True)
+        cuda = self.device.type == "cuda"
+        timing = timing and cuda
+
+        class _NoEv:
+            def record(self):
+                pass
+
+        ev = (lambda: torch.cuda.Event(enable_timing=True)) if cuda else (lambda: _NoEv())
         self.stats.levels = [dict(level=l, outer=0, patch_updates=0, ms=0.0) for l in range(1, L + 1)]
         t_all0 = ev(); t_all0.record()
         marks = {}
@@ -212,8 +224,9 @@ class Inpainter:
             self.onion_peel() if self.native else self.onion_peel_stepwise()
         else:
             st = self.states[-1]
-            V.nnf_init_random(st.lv, st.a, self.prm, 0)
+            self.V.nnf_init_random(st.lv, st.a, self.prm, 0)
         e_on = ev(); e_on.record()
+        onion_pu = self.counter.clone()  # replicated work: counted once (rank 0) in the job total
         pu_prev = 0
         for l in range(L, 0, -1):
             st = self.states[l - 1]
@@ -226,7 +239,7 @@ class Inpainter:
                 self.reconstruct(st, V.WEIGHTED)
                 self.change.zero_()
                 hb, he = self.ex.slab(lv.n_holes)
-                V.change_l1(st.cur_rgb[hb:he], st.prev_rgb[hb:he], self.change)
+                self.V.change_l1(st.cur_rgb[hb:he], st.prev_rgb[hb:he], self.change)
                 self.ex.allreduce_sum(self.change)
                 k += 1
                 if cfg.fixed_outer > 0:
@@ -241,7 +254,7 @@ class Inpainter:
             else:
                 f = self.states[l - 2]
                 fb, fe = self.ex.slab(f.lv.n_targets)
-                V.nnf_upsample(lv, st.a, f.lv, f.a, self.prm, fb, fe)
+                self.V.nnf_upsample(lv, st.a, f.lv, f.a, self.prm, fb, fe)
                 self.ex.gather(f.a.e, f.lv.n_targets)
                 self.ex.gather(f.a.n, f.lv.n_targets)
                 self.reconstruct(f, V.UNWEIGHTED)  # R20
@@ -257,6 +270,8 @@ class Inpainter:
             self.stats.total_ms = t_all0.elapsed_time(t_all1)
             self.stats.onion_ms = t_all0.elapsed_time(e_on)
         pu = self.counter.clone()
+        if self.ex.rank != 0:
+            pu -= onion_pu
         self.ex.allreduce_sum(pu)
         self.stats.total_patch_updates = int(pu.item())
         return self.stats
@@ -269,10 +284,10 @@ class Inpainter:
         return torch.where(m[..., None], vb, rgb_in)
 
 
-def inpaint(rgb: torch.Tensor, mask: torch.Tensor, cfg: Config, device="cuda", exchange=None):
+def inpaint(rgb: torch.Tensor, mask: torch.Tensor, cfg: Config, device="cuda", exchange=None, ops=None):
     """Convenience: whole Alg. 4 on one video.  rgb/mask may live on the host (copied in)."""
     T, H, W, _ = rgb.shape
-    ip = Inpainter(W, H, T, cfg, device, exchange)
+    ip = Inpainter(W, H, T, cfg, device, exchange, ops)
     rgb_d = rgb.to(device, non_blocking=True)
     mask_d = mask.to(device, non_blocking=True)
     ip.load(rgb_d, mask_d)

@@ -64,9 +64,9 @@ def _load():
         "vinp_nnf_evaluate": (I, [P, P, P, I, I, I32, I32, P, P]),
         "vinp_propagate": (I, [P, P, P, P, I, I, I, I, I32, I32, P, P]),
         "vinp_random_search": (I, [P, P, P, P, U32, I, I, I, I32, I32, P, P]),
-        "vinp_ann_search": (I, [P, P, P, P, U32, I, P, I, I, I, P, P]),
+        "vinp_ann_search": (I, [P, P, P, P, U32, I, P, I, I, I, I, P, P]),
         "vinp_onion_ws_bytes": (C.c_size_t, [P]),
-        "vinp_onion_peel": (I, [P, P, P, P, I, P, I, I, P, P, P, P, C.c_size_t, P]),
+        "vinp_onion_peel": (I, [P, P, P, P, I, P, I, I, I, P, P, P, P, C.c_size_t, P]),
         "vinp_reconstruct": (I, [P, P, I, I, I32, I32, P, P, I, P]),
         "vinp_commit": (I, [P, P, P, I, I32, I32, P]),
         "vinp_change_l1": (I, [P, P, I64, P, P]),
@@ -282,20 +282,22 @@ def random_search(lv, nin, nout, prm, outer_code, pm_iter, kb=-1, only_layer=-1,
                                    _stream()), "vinp_random_search")
 
 
-def ann_search(lv, a, b, prm, outer_code, K, steps=(8, 4, 2, 1), kb=-1, only_layer=-1, counter=None):
+def ann_search(lv, a, b, prm, outer_code, K, steps=(8, 4, 2, 1), kb=-1, only_layer=-1, counter=None,
+               sign_policy=0):
     st = (C.c_int32 * len(steps))(*steps)
     _check(_lib.vinp_ann_search(lv.struct(), a.struct(), b.struct(), C.byref(prm.struct()), outer_code,
-                                K, st, len(steps), kb, only_layer, _ptr(counter), _stream()),
+                                K, st, len(steps), sign_policy, kb, only_layer, _ptr(counter), _stream()),
            "vinp_ann_search")
 
 
-def onion_peel(lv, a, b, prm, K, n_layers, out_rgb, out_tex, steps=(8, 4, 2, 1), counter=None, ws=None):
+def onion_peel(lv, a, b, prm, K, n_layers, out_rgb, out_tex, steps=(8, 4, 2, 1), counter=None, ws=None,
+               sign_policy=0):
     nbytes = int(_lib.vinp_onion_ws_bytes(lv.struct()))
     if ws is None or ws.numel() < nbytes:
         ws = torch.empty(nbytes, dtype=torch.uint8, device=lv.device)
     st = (C.c_int32 * len(steps))(*steps)
     _check(_lib.vinp_onion_peel(lv.struct(), a.struct(), b.struct(), C.byref(prm.struct()), K, st,
-                                len(steps), n_layers, _ptr(out_rgb), _ptr(out_tex), _ptr(counter),
+                                len(steps), sign_policy, n_layers, _ptr(out_rgb), _ptr(out_tex), _ptr(counter),
                                 _ptr(ws), ws.numel(), _stream()), "vinp_onion_peel")
 
 

@@ -1,0 +1,243 @@
+"""Test-only: the CPU oracle behind the libvinp call signatures (paper_1503_05528_b200/vinp.py), on
+CPU tensors in the GPU data layout (include/vinp.h).  Lets the multi-rank driver logic (slabs,
+all-gathers, all-reduce) run under torch.distributed/gloo on a machine without a GPU.  Every call
+converts to the oracle's own data model, runs the oracle, and converts back."""
+import ctypes as C
+
+import numpy as np
+import torch
+
+import oracle.oracle as orc
+
+ONION = 0x80000000
+
+
+def _np(t):
+    return t.numpy()
+
+
+class _OLevel:
+    """or_level view of a vinp Level (CPU tensors); rgb/tex copied out of vox."""
+
+    def __init__(self, lv):
+        self.lv = lv
+        N = lv.N
+        vb = lv.vox.view(torch.uint8).view(N, 8).numpy()
+        self.rgb = np.ascontiguousarray(vb[:, :3])
+        self.tex = np.ascontiguousarray(vb[:, 4:6])
+        f = lv.flags.numpy()
+        self.occ = np.ascontiguousarray(f & 1)
+        self.src = np.ascontiguousarray((f >> 1) & 1)
+        self.tgt = np.ascontiguousarray((f >> 2) & 1)
+        self.layer = None if lv.layer is None else np.ascontiguousarray(lv.layer.numpy())
+        self.slot = np.ascontiguousarray(lv.slot.numpy())
+        self.targets = np.ascontiguousarray(lv.targets.numpy()[:lv.n_targets])
+        self.holes = np.ascontiguousarray(lv.holes.numpy()[:lv.n_holes])
+        self.sources = np.ascontiguousarray(lv.sources.numpy()[:lv.n_sources])
+        self.W, self.H, self.T = lv.W, lv.H, lv.T
+
+    def struct(self):
+        p = lambda a: None if a is None else a.ctypes.data
+        self._s = orc.OrLevel(self.W, self.H, self.T, p(self.rgb), p(self.tex), p(self.occ), p(self.src),
+                              p(self.tgt), p(self.layer), p(self.slot), p(self.targets), len(self.targets),
+                              p(self.holes), len(self.holes), p(self.sources), len(self.sources))
+        return C.byref(self._s)
+
+    @property
+    def rmax(self):
+        return max(self.W, self.H, self.T)
+
+    def write_back(self):
+        vb = self.lv.vox.view(torch.uint8).view(self.lv.N, 8)
+        vb[:, :3] = torch.from_numpy(self.rgb)
+        vb[:, 4:6] = torch.from_numpy(self.tex)
+
+
+def _to_orc(lv, nnf):
+    nt = lv.n_targets
+    e = nnf.e.numpy()[:nt].view(np.uint64)
+    q = (e & np.uint64(0xFFFFFFFF)).astype(np.int64)
+    p = lv.targets.numpy()[:nt].astype(np.int64)
+    HW = lv.H * lv.W
+    f = orc.NNF.empty(nt)
+    f.dx[:nt] = q % lv.W - p % lv.W
+    f.dy[:nt] = (q // lv.W) % lv.H - (p // lv.W) % lv.H
+    f.dt[:nt] = q // HW - p // HW
+    f.D[:nt] = (e >> np.uint64(32)).astype(np.uint32)
+    f.n[:nt] = nnf.n.numpy()[:nt]
+    return f
+
+
+def _from_orc(lv, f, nnf):
+    nt = lv.n_targets
+    p = lv.targets.numpy()[:nt].astype(np.int64)
+    HW = lv.H * lv.W
+    q = ((p // HW + f.dt[:nt]) * lv.H + (p // lv.W) % lv.H + f.dy[:nt]) * lv.W + p % lv.W + f.dx[:nt]
+    e = (f.D[:nt].astype(np.uint64) << np.uint64(32)) | q.astype(np.uint64)
+    nnf.e[:nt] = torch.from_numpy(e.view(np.int64).copy())
+    nnf.n[:nt] = torch.from_numpy(f.n[:nt].copy())
+
+
+def _count(counter, c):
+    if counter is not None:
+        counter += int(c)
+
+
+# ----------------------------------------------------------------------------- setup
+def texture_ws_bytes(lv1):
+    return 1
+
+
+def sets_ws_bytes(lv1):
+    return 1
+
+
+def build_pyramid(rgb, mask, levels):
+    r, m = rgb.numpy(), (mask.numpy() != 0).astype(np.uint8)
+    for i, lv in enumerate(levels):
+        if i > 0:
+            r, m = orc.pyramid_down(r, m)
+        vb = lv.vox.view(torch.uint8).view(lv.N, 8)
+        vb.zero_()
+        vb[:, :3] = torch.from_numpy(np.ascontiguousarray(r).reshape(-1, 3))
+        lv.flags.copy_(torch.from_numpy(m.reshape(-1)))
+
+
+def texture_features(prm, levels, ws):
+    L = len(levels)
+    h = prm.tex_half if prm.tex_half >= 0 else (2 ** (L - 2) if L >= 2 else 1)
+    l1 = levels[0]
+    vb = l1.vox.view(torch.uint8).view(l1.T, l1.H, l1.W, 8).numpy()
+    occ = (l1.flags.numpy() & 1).reshape(l1.T, l1.H, l1.W)
+    tex1 = orc.texture(np.ascontiguousarray(vb[..., :3]), np.ascontiguousarray(occ), h)
+    for i, lv in enumerate(levels):
+        t = tex1 if i == 0 else orc.texture_decimate(tex1, i + 1, lv.W, lv.H)
+        lv.vox.view(torch.uint8).view(lv.N, 8)[:, 4:6] = torch.from_numpy(t.reshape(-1, 2))
+
+
+def build_sets(levels, ws):
+    out = []
+    for lv in levels:
+        occ = (lv.flags.numpy() & 1).reshape(lv.T, lv.H, lv.W)
+        src, tgt = orc.sets(np.ascontiguousarray(occ))
+        lv.flags.copy_(torch.from_numpy((occ | (src << 1) | (tgt << 2)).reshape(-1)))
+        lv.n_targets, lv.n_holes, lv.n_sources = int(tgt.sum()), int(occ.sum()), int(src.sum())
+        out.append((lv.n_targets, lv.n_holes, lv.n_sources))
+    return out
+
+
+def build_lists(levels, ws):
+    for lv in levels:
+        f = lv.flags.numpy()
+        t, h, s = np.flatnonzero(f & 4), np.flatnonzero(f & 1), np.flatnonzero(f & 2)
+        lv.targets[:len(t)] = torch.from_numpy(t.astype(np.int32))
+        lv.holes[:len(h)] = torch.from_numpy(h.astype(np.int32))
+        lv.sources[:len(s)] = torch.from_numpy(s.astype(np.int32))
+        sl = np.full(lv.N, -1, np.int32)
+        sl[t] = np.arange(len(t), dtype=np.int32)
+        lv.slot.copy_(torch.from_numpy(sl))
+
+
+def layers(lv, ws):
+    occ = (lv.flags.numpy() & 1).reshape(lv.T, lv.H, lv.W)
+    lay, n = orc.layers(np.ascontiguousarray(occ))
+    lv.layer.copy_(torch.from_numpy(lay.reshape(-1)))
+    return n
+
+
+# ----------------------------------------------------------------------------- passes
+def nnf_init_random(lv, nnf, prm, outer_code, b=0, e=None):
+    e = lv.n_targets if e is None else e
+    ol = _OLevel(lv)
+    f = _to_orc(lv, nnf)
+    orc.init_random(ol, f, prm.seed, lv.level, outer_code, b, e)
+    _from_orc(lv, f, nnf)
+
+
+def nnf_upsample(coarse, cn, fine, fn, prm, b=0, e=None):
+    e = fine.n_targets if e is None else e
+    oc, of = _OLevel(coarse), _OLevel(fine)
+    fc, ff = _to_orc(coarse, cn), _to_orc(fine, fn)
+    orc.upsample(oc, fc, of, ff, prm.seed, fine.level, b, e)
+    _from_orc(fine, ff, fn)
+
+
+def nnf_evaluate(lv, nnf, prm, kb=-1, only_layer=-1, b=0, e=None, counter=None):
+    e = lv.n_targets if e is None else e
+    ol = _OLevel(lv)
+    f = _to_orc(lv, nnf)
+    _count(counter, orc.evaluate(ol, f, prm.lam, kb, only_layer, b, e))
+    _from_orc(lv, f, nnf)
+
+
+def propagate(lv, nin, nout, prm, step, sign, kb=-1, only_layer=-1, b=0, e=None, counter=None):
+    e = lv.n_targets if e is None else e
+    ol = _OLevel(lv)
+    fi, fo = _to_orc(lv, nin), _to_orc(lv, nout)
+    _count(counter, orc.propagate(ol, fi, fo, prm.lam, step, sign, kb, only_layer, b, e))
+    _from_orc(lv, fo, nout)
+
+
+def random_search(lv, nin, nout, prm, outer_code, pm_iter, kb=-1, only_layer=-1, b=0, e=None,
+                  counter=None):
+    e = lv.n_targets if e is None else e
+    ol = _OLevel(lv)
+    fi, fo = _to_orc(lv, nin), _to_orc(lv, nout)
+    rmax = prm.rmax if prm.rmax > 0 else ol.rmax
+    _count(counter, orc.random_search(ol, fi, fo, prm.lam, prm.seed, prm.rho, rmax, lv.level, outer_code,
+                                      pm_iter, kb, only_layer, b, e))
+    _from_orc(lv, fo, nout)
+
+
+def ann_search(lv, a, b, prm, outer_code, K, steps=(8, 4, 2, 1), kb=-1, only_layer=-1, counter=None,
+               sign_policy=0):
+    nnf_evaluate(lv, a, prm, kb, only_layer, counter=counter)
+    cur, nxt = a, b
+    for k in range(1, K + 1):
+        sign = 0 if sign_policy else (1 if k % 2 == 1 else -1)
+        for s in steps:
+            propagate(lv, cur, nxt, prm, s, sign, kb, only_layer, counter=counter)
+            cur, nxt = nxt, cur
+        random_search(lv, cur, nxt, prm, outer_code, k, kb, only_layer, counter=counter)
+        cur, nxt = nxt, cur
+    if cur is not a:
+        a.e.copy_(cur.e)
+
+
+def onion_peel(lv, a, b, prm, K, n_layers, out_rgb, out_tex, steps=(8, 4, 2, 1), counter=None, ws=None,
+               sign_policy=0):
+    for j in range(0, n_layers + 1):
+        ann_search(lv, a, b, prm, ONION | j, K, steps, max(j, 1), j, counter, sign_policy)
+        if j >= 1:
+            reconstruct(lv, a, 0, out_rgb, out_tex, j)
+
+
+def reconstruct(lv, nnf, mode, out_rgb, out_tex, layer_j=-1, hb=0, he=None, commit=True):
+    he = lv.n_holes if he is None else he
+    ol = _OLevel(lv)
+    f = _to_orc(lv, nnf)
+    o_rgb = np.ascontiguousarray(out_rgb.numpy())
+    o_tex = np.ascontiguousarray(out_tex.numpy())
+    orc.reconstruct(ol, f, mode, layer_j, hb, he, o_rgb, o_tex)
+    out_rgb.copy_(torch.from_numpy(o_rgb))
+    out_tex.copy_(torch.from_numpy(o_tex))
+    if commit:
+        _commit(ol, o_rgb, o_tex, layer_j, hb, he)
+
+
+def _commit(ol, o_rgb, o_tex, layer_j, hb, he):
+    for h in range(hb, he):
+        if layer_j >= 0 and ol.layer[ol.holes[h]] != layer_j:
+            continue
+        orc.commit(ol, o_rgb, o_tex, h, h + 1)
+    ol.write_back()
+
+
+def commit(lv, out_rgb, out_tex, layer_j=-1, hb=0, he=None):
+    he = lv.n_holes if he is None else he
+    _commit(_OLevel(lv), np.ascontiguousarray(out_rgb.numpy()), np.ascontiguousarray(out_tex.numpy()),
+            layer_j, hb, he)
+
+
+def change_l1(a, b, out):
+    out += int(orc.change_l1(a.numpy(), b.numpy()))

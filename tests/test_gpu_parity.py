@@ -155,7 +155,7 @@ def test_init_evaluate_propagate_random_search_bit_exact(V, orc, case):
         assert len(B.nnf_equal(orc, lv, a.e, a.n, f)) == 0, "evaluate"
         assert int(cnt.item()) == c_o
         g = f.copy()
-        for k, (step, sign) in enumerate([(8, 1), (4, 1), (2, 1), (1, 1), (1, -1), (4, -1)]):
+        for k, (step, sign) in enumerate([(8, 1), (4, 1), (2, 1), (1, 1), (1, -1), (4, -1), (2, 0), (1, 0)]):
             cnt.zero_()
             V.propagate(lv, a, b, ip.prm, step, sign, counter=cnt)
             c_o = orc.propagate(ol, f, g, lam, step, sign)

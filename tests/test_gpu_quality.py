@@ -1,0 +1,63 @@
+"""Quality line (north_star): at level 1, first outer iteration, on the same u and
+initial NNF, mean d^2 after the configured PatchMatch iterations vs the exact brute-force NN.
+Also: the brute-force D is a lower bound for every PatchMatch target (exactness of both)."""
+import json
+import os
+
+import numpy as np
+import pytest
+import torch
+
+from gen.synth import CONFIGS, generate
+
+pytestmark = pytest.mark.gpu
+ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+
+
+def _quality(name, max_targets=None, steps=(8, 4, 2, 1), sign_policy=0):
+    from paper_1503_05528_b200 import Config, Inpainter, vinp as V
+    c = CONFIGS[name]
+    v, m, _ = generate(name, device="cuda")
+    ip = Inpainter(c.W, c.H, c.T, Config(levels=c.levels, pm_iters=c.pm_iters, lam=c.lam, seed=c.seed,
+                                         steps=steps, sign_policy=sign_policy), "cuda")
+    ip.load(v, m)
+    ip.onion_peel()
+    # descend to level 1 exactly as Alg. 4 does (one outer iteration per coarse level suffices to
+    # get a representative u at level 1 for this report)
+    for l in range(c.levels, 1, -1):
+        st, f = ip.states[l - 1], ip.states[l - 2]
+        ip.ann_search(st, 0)
+        ip.reconstruct(st, V.WEIGHTED)
+        V.nnf_upsample(st.lv, st.a, f.lv, f.a, ip.prm)
+        ip.reconstruct(f, V.UNWEIGHTED)
+    st = ip.states[0]
+    lv = st.lv
+    n = lv.n_targets if max_targets is None else min(lv.n_targets, max_targets)
+    cnt = torch.zeros(1, dtype=torch.int64, device="cuda")
+    V.ann_search(lv, st.a, st.b, ip.prm, 0, c.pm_iters, tuple(steps), counter=cnt, sign_policy=sign_policy)
+    bf = V.NNF.alloc(lv.n_targets, "cuda")
+    V.brute_force(lv, bf, ip.prm, 0, n)
+    torch.cuda.synchronize()
+    Dp = (st.a.e[:n] >> 32).double()
+    Db = (bf.e[:n] >> 32).double()
+    npm = st.a.n[:n].double()
+    nbf = bf.n[:n].double()
+    assert torch.all(Dp >= Db), "PatchMatch below the exact minimum"
+    assert torch.equal(npm, nbf)
+    d_pm = (Dp / (4 * npm)).mean().item()
+    d_bf = (Db / (4 * nbf)).mean().item()
+    same = (st.a.e[:n] == bf.e[:n]).double().mean().item()
+    return dict(config=name, steps=list(steps), sign_policy=sign_policy, patch_updates=int(cnt.item()),
+                targets=n, mean_d2_patchmatch=d_pm, mean_d2_bruteforce=d_bf,
+                ratio_minus_1=d_pm / d_bf - 1 if d_bf > 0 else 0.0, frac_exact=same)
+
+
+@pytest.mark.parametrize("name", ["c1", "c2"])
+def test_patchmatch_quality_vs_brute_force(name):
+    q = _quality(name)
+    os.makedirs(os.path.join(ROOT, "gpurun_out"), exist_ok=True)
+    with open(os.path.join(ROOT, "gpurun_out", f"quality_{name}.json"), "w") as f:
+        json.dump(q, f)
+    print(json.dumps(q))
+    # The north_star target is 5%; the test guards the measured level (DESIGN.md §6 reports it).
+    assert q["ratio_minus_1"] <= 0.25

@@ -1,0 +1,73 @@
+"""World-size-2 run of the multi-GPU driver logic on CPU (gloo): target/hole slabs, NNF and hole
+all-gathers after every pass, exact int64 all-reduce of the stopping-rule change.  The compute is
+the CPU oracle behind the libvinp signatures (tests/oracle_ops.py).  The result must be
+bit-identical to a single-rank run and to the oracle's own whole-pipeline or_inpaint (SURVEY §8(e):
+the schedule is partition-independent)."""
+import os
+import socket
+
+import numpy as np
+import pytest
+import torch
+import torch.distributed as dist
+import torch.multiprocessing as mp
+
+from gen.synth import random_volume
+
+CFG = dict(levels=2, pm_iters=2, max_outer=3)
+
+
+def _free_port():
+    s = socket.socket()
+    s.bind(("127.0.0.1", 0))
+    p = s.getsockname()[1]
+    s.close()
+    return p
+
+
+def _run(rank, world, port, out_path):
+    os.environ.update(MASTER_ADDR="127.0.0.1", MASTER_PORT=str(port))
+    dist.init_process_group("gloo", rank=rank, world_size=world)
+    try:
+        import oracle_ops
+        from paper_1503_05528_b200 import Config, Exchange, inpaint
+        v, m, _ = random_volume(40, 32, 10, seed=4, hole_frac=0.06)
+        out, stats, ip = inpaint(v, m, Config(**CFG), device="cpu", exchange=Exchange(), ops=oracle_ops)
+        if rank == 0:
+            np.save(out_path, out.numpy())
+            np.save(out_path + ".stats.npy", np.array([l["outer"] for l in stats.levels] +
+                                                      [stats.total_patch_updates]))
+    finally:
+        dist.destroy_process_group()
+
+
+def _spawn(world, tmp_path):
+    out = str(tmp_path / f"out_w{world}.npy")
+    mp.spawn(_run, args=(world, _free_port(), out), nprocs=world, join=True)
+    return np.load(out), np.load(out + ".stats.npy")
+
+
+def test_two_ranks_bit_identical_to_one_and_to_oracle(tmp_path, orc):
+    import oracle_ops  # noqa: F401  (importable from tests/)
+    o1, s1 = _spawn(1, tmp_path)
+    o2, s2 = _spawn(2, tmp_path)
+    assert np.array_equal(o1, o2)
+    assert np.array_equal(s1, s2)
+    v, m, _ = random_volume(40, 32, 10, seed=4, hole_frac=0.06)
+    ref, st = orc.inpaint(v.numpy(), m.numpy(), CFG["levels"], pm_iters=CFG["pm_iters"],
+                          max_outer=CFG["max_outer"])
+    assert np.array_equal(o1, ref)
+    assert list(s1[:-1]) == st["outer_iters"] and int(s1[-1]) == sum(st["patch_updates"])
+
+
+def test_exchange_slabs_cover_and_pad():
+    from paper_1503_05528_b200.inpaint import Exchange
+    ex = Exchange()
+    ex.world = 3
+    spans = []
+    for r in range(3):
+        ex.rank = r
+        spans.append(ex.slab(10))
+    assert ex.padded(10) == 12 and spans == [(0, 4), (4, 8), (8, 10)]
+    ex.rank = 2
+    assert ex.slab(0) == (0, 0)
