@@ -25,6 +25,8 @@ ROOT = os.path.dirname(os.path.abspath(__file__))
 sys.path.insert(0, ROOT)
 
 B_PU, B_TP, B_HOLE = 625, 29, 662  # algorithmic bytes: per patch-update / target-pass / hole
+CPU_SAMPLE = (24, 38, 4)  # oracle cpu_baseline sample: frames, first frame, PM iterations (~10-30 s)
+REF_SAMPLE = (12, 44, 2)  # --impl reference step: a smaller sample so W+K steps finish in minutes
 
 
 def _peaks():
@@ -119,16 +121,17 @@ def run_reference(args):
     rank = int(os.environ.get("RANK", "0"))
     if rank != 0:
         return 0
-    frames, t0 = 4, 48
+    frames, t0, iters = REF_SAMPLE
     for _ in range(args.warmup):
-        oracle_sample(args.config, frames, t0)
+        oracle_sample(args.config, frames, t0, iters)
     tot_pu, tot_s = 0, 0.0
     for _ in range(args.steps):
-        pu, s, thr = oracle_sample(args.config, frames, t0)
+        pu, s, thr = oracle_sample(args.config, frames, t0, iters)
         tot_pu += pu
         tot_s += s
     val = tot_pu / tot_s
-    sample = f"{args.config} frames [{t0},{t0 + frames}) at level 1: evaluate + 1 PatchMatch iteration from random init"
+    sample = (f"{args.config} frames [{t0},{t0 + frames}) at level 1: evaluate + {iters} PatchMatch "
+              f"iterations from random init")
     line = {"impl": "reference", "metric": "PatchMatch patch-updates/sec", "value": val,
             "unit": "patch-updates/s", "n_gpus": args.gpus, "steps": args.steps, "warmup": args.warmup,
             "ms_per_step": 1000 * tot_s / args.steps, "higher_is_better": True, "dtype": "u8",
@@ -151,6 +154,8 @@ def main():
     ap.add_argument("--config", default="c5")
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--no-cpu", action="store_true")
+    ap.add_argument("--no-extra", action="store_true",
+                    help="only the timed steps (no per-level / roofline / e2e / cpu runs): for ncu launch lists")
     args = ap.parse_args()
     if args.impl == "reference":
         return run_reference(args)
@@ -205,17 +210,18 @@ def main():
     ms = float(t.item())
     value = pu / (ms / 1000.0)
 
-    # per-level seconds (one timed run with per-level events)
-    ip.load(v, m)
-    stats = ip.run(timing=True)
-    levels = [{"level": l["level"], "outer": l["outer"], "s": l["ms"] / 1000.0} for l in stats.levels]
-    levels[-1]["onion_s"] = stats.onion_ms / 1000.0
-
-    # dominant-kernel roofline: one instrumented step with events around every pass
-    roof = measure_roofline(ip, v, m, dev)
+    levels, roof = None, None
+    if not args.no_extra:
+        # per-level seconds (one timed run with per-level events)
+        ip.load(v, m)
+        stats = ip.run(timing=True)
+        levels = [{"level": l["level"], "outer": l["outer"], "s": l["ms"] / 1000.0} for l in stats.levels]
+        levels[-1]["onion_s"] = stats.onion_ms / 1000.0
+        # dominant-kernel roofline: one instrumented step with events around every pass
+        roof = measure_roofline(ip, v, m, dev)
 
     e2e = None
-    if not args.no_e2e:
+    if not args.no_e2e and not args.no_extra:
         rgb_h = v.cpu().pin_memory()
         m_h = m.cpu().pin_memory()
         for _ in range(1):
@@ -240,11 +246,11 @@ def main():
                "h2d_bytes_per_step": int(v.numel() + m.numel()), "d2h_bytes_per_step": int(res.numel())}
 
     cpu = None
-    if rank == 0 and world == 1 and not args.no_cpu:
-        frames, t0 = 4, 48
-        pu_c, s_c, thr = oracle_sample(args.config, frames, t0)
+    if rank == 0 and world == 1 and not args.no_cpu and not args.no_extra:
+        frames, t0, iters = CPU_SAMPLE
+        pu_c, s_c, thr = oracle_sample(args.config, frames, t0, iters)
         cpu = {"value": pu_c / s_c, "unit": "patch-updates/s", "cores": thr, "kind": "oracle",
-               "sample": f"{args.config} frames [{t0},{t0 + frames}) level 1: evaluate + 1 PM iteration "
+               "sample": f"{args.config} frames [{t0},{t0 + frames}) level 1: evaluate + {iters} PM iterations "
                          f"from random init ({pu_c} patch-updates in {s_c:.1f} s)"}
 
     if rank == 0:

@@ -352,7 +352,20 @@ struct Radii {
   int M;
 };
 
-template <int NC, int WPB>
+// Random search, evaluation by 5-lane column groups: lanes 5g..5g+4 (g < 6) evaluate one
+// (target, candidate) pair, lane k owning patch column dx = k - 2, so every row of a patch is one
+// 40-byte gather per group and 6 pairs share each warp instruction.  Pairs come from the warp's
+// flattened candidate list (owner lane = target, rank order).  Exact partial-distance elimination
+// after every frame dt (25 voxels): the group sum is all-reduced over its 5 lanes (3 shuffles) and
+// the pair is dropped once it reaches its target's best at the start of the batch.  Survivors are
+// applied in pair order (rank order within a target) with strict improvement (R25).
+__device__ __forceinline__ uint32_t sum5(uint32_t x, int base, int k) {
+  uint32_t s1 = x + __shfl_sync(kFull, x, base + (k + 1) % 5);
+  uint32_t s2 = s1 + __shfl_sync(kFull, s1, base + (k + 2) % 5);
+  return s2 + __shfl_sync(kFull, x, base + (k + 4) % 5);
+}
+
+template <int NC, int WPB, bool KNOWN>
 __global__ void __launch_bounds__(32 * WPB, VINP_MINB * 8 / WPB) k_random_search(
     LevelArgs a, const uint64_t* __restrict__ ein, uint64_t* __restrict__ eout, int lambda, Radii rad,
     uint64_t seed, uint32_t oc, int pm_iter, int kb, int only_layer, int32_t b, int32_t e,
@@ -367,9 +380,13 @@ __global__ void __launch_bounds__(32 * WPB, VINP_MINB * 8 / WPB) k_random_search
   uint64_t inc = have ? __ldg(reinterpret_cast<const unsigned long long*>(ein) + s) : 0ull;
   bool act = have && (only_layer < 0 || a.layer[p] == only_layer);
   __shared__ int s_cand[WPB][NC * 32];
+  __shared__ int2 s_pairs[WPB][NC * 32];
   int* cand = s_cand[threadIdx.x >> 5];
+  int2* pairs = s_pairs[threadIdx.x >> 5];
   int nc = 0;
+  int px = 0, py = 0, pt = 0;
   if (act) {
+    decode(a.g, p, px, py, pt);
     int q0 = e_q(inc);
     int q0x, q0y, q0t;
     decode(a.g, q0, q0x, q0y, q0t);
@@ -388,12 +405,81 @@ __global__ void __launch_bounds__(32 * WPB, VINP_MINB * 8 / WPB) k_random_search
       }
     }
   }
+  // flatten (owner lane, rank) pairs in lane order
+  int incl = nc;
+#pragma unroll
+  for (int d = 1; d < 32; d <<= 1) {
+    int y = __shfl_up_sync(kFull, incl, d);
+    if (lane >= d) incl += y;
+  }
+  int P = __shfl_sync(kFull, incl, 31);
+  for (int j = 0; j < nc; ++j) pairs[incl - nc + j] = make_int2(cand[j * 32 + lane], lane);
   __syncwarp();
-  uint64_t res;
-  unsigned cnt = 0;
-  phase2<NC>(a, lane, lambda, kb, p, inc, cand, nc, res, cnt);
-  if (have) eout[s] = res;
-  if (lane == 0) flush_count(counter, cnt);
+  uint32_t bestD = e_D(inc);
+  int bestq = e_q(inc);
+  const int g = lane / 5, k = lane - 5 * (lane / 5), gbase = 5 * g, dx = k - 2;
+  const unsigned long long* v = reinterpret_cast<const unsigned long long*>(a.vox);
+  for (int base = 0; base < P; base += 6) {
+    int j = base + g;
+    bool valid = g < 6 && j < P;
+    int2 pr = valid ? pairs[j] : make_int2(0, 0);
+    int t = pr.y;
+    int pi = __shfl_sync(kFull, p, t);
+    int tx = __shfl_sync(kFull, px, t), ty = __shfl_sync(kFull, py, t), tt = __shfl_sync(kFull, pt, t);
+    uint32_t thr = __shfl_sync(kFull, bestD, t);
+    bool colok = valid && (unsigned)(tx + dx) < (unsigned)a.g.W;
+    bool alive = valid;
+    uint32_t accc = 0, acct = 0, tot = 0;
+#pragma unroll 1
+    for (int dt = -2; dt <= 2; ++dt) {
+      bool tok = alive && colok && (unsigned)(tt + dt) < (unsigned)a.g.T;
+      // predicates first, then all 10 gathers of the frame (invalid rows read the target's own
+      // centre voxel and are masked), then the arithmetic: one memory round trip per frame
+      int ro[5];
+      bool okr[5];
+#pragma unroll
+      for (int r = 0; r < 5; ++r) {
+        ro[r] = dt * a.g.HW + (r - 2) * a.g.W + dx;
+        okr[r] = tok && (unsigned)(ty + r - 2) < (unsigned)a.g.H;
+        if (KNOWN) okr[r] = okr[r] && a.layer[pi + (okr[r] ? ro[r] : 0)] < kb;
+      }
+      uint64_t tv[5], sv[5];
+#pragma unroll
+      for (int r = 0; r < 5; ++r) {
+        tv[r] = __ldg(v + pi + (okr[r] ? ro[r] : 0));
+        sv[r] = __ldg(v + pr.x + (okr[r] ? ro[r] : 0));
+      }
+#pragma unroll
+      for (int r = 0; r < 5; ++r) {
+        uint64_t tw = okr[r] ? tv[r] : 0ull, sw = okr[r] ? sv[r] : 0ull;
+        uint32_t dc = __vabsdiffu4((uint32_t)tw, (uint32_t)sw);
+        uint32_t dtx = __vabsdiffu4((uint32_t)(tw >> 32), (uint32_t)(sw >> 32));
+        accc = __dp4a(dc, dc, accc);
+        acct = __dp4a(dtx, dtx, acct);
+      }
+      tot = sum5(4u * accc + (uint32_t)lambda * acct, gbase < 30 ? gbase : 0, k);
+      if (tot >= thr) alive = false;
+      if (!__any_sync(kFull, alive)) break;
+    }
+    // apply the surviving pairs of this batch in order
+#pragma unroll
+    for (int g2 = 0; g2 < 6; ++g2) {
+      int src = 5 * g2;
+      bool al = __shfl_sync(kFull, (int)alive, src);
+      if (al) {
+        uint32_t D = __shfl_sync(kFull, tot, src);
+        int tq = __shfl_sync(kFull, pr.x, src);
+        int towner = __shfl_sync(kFull, t, src);
+        uint32_t cur = __shfl_sync(kFull, bestD, towner);
+        if (D < cur && lane == towner) {
+          bestD = D;
+          bestq = tq;
+        }
+      }
+    }
+  }
+  if (have) eout[s] = pack_e(bestD, bestq);
+  if (lane == 0) flush_count(counter, (unsigned)P);
 }
 
 // ------------------------------------------------------------------ a13: brute force (CUDA cores)
@@ -638,10 +724,15 @@ vinp_status launch_random_search(const vinp_level* lv, const vinp_nnf* in, vinp_
   if (e > b) {
     cudaStream_t cs = S(stream);
     LevelArgs la = args_of(lv);
-#define VINP_RS(NC, WPB)                                                                          \
-  k_random_search<NC, WPB><<<nblk(e - b, 32 * WPB), 32 * WPB, 0, cs>>>(                          \
-      la, in->e, out->e, prm->lambda, r, prm->seed, outer_code, pm_iter, kb, only_layer, b, e, list, \
-      counter)
+#define VINP_RS(NC, WPB)                                                                           \
+  if (kb >= 0)                                                                                     \
+    k_random_search<NC, WPB, true><<<nblk(e - b, 32 * WPB), 32 * WPB, 0, cs>>>(                     \
+        la, in->e, out->e, prm->lambda, r, prm->seed, outer_code, pm_iter, kb, only_layer, b, e,     \
+        list, counter);                                                                            \
+  else                                                                                             \
+    k_random_search<NC, WPB, false><<<nblk(e - b, 32 * WPB), 32 * WPB, 0, cs>>>(                    \
+        la, in->e, out->e, prm->lambda, r, prm->seed, outer_code, pm_iter, kb, only_layer, b, e,     \
+        list, counter)
     if (r.M <= 8)
       VINP_RS(8, 8);
     else if (r.M <= 12)

@@ -620,3 +620,88 @@ def test_pipeline_periodic_texture_psnr(orc):
     d = out.astype(float) - rgb
     psnr = 10 * np.log10(255 ** 2 / np.mean(d[occ.astype(bool)] ** 2))
     assert psnr > 28
+
+
+# ----------------------------------------------------------------------------- directed pins
+def _copy_world(orc):
+    """Exact-copy volume: the right half repeats the left half, so shift (+20, 0, 0) is perfect."""
+    T, H, W = 9, 12, 40
+    base = _vol(T, H, 20, seed=31)
+    rgb = np.concatenate([base, base], axis=2)
+    occ = np.zeros((T, H, W), np.uint8)
+    occ[4, 6, 6] = 1  # one hole voxel -> a 5x5x5 block of targets around (6, 6, 4)
+    lv = _level(orc, rgb, occ)
+    lv.rgb[4, 6, 6] = rgb[4, 6, 26]  # hole content equals its copy
+    return lv
+
+
+@pytest.mark.parametrize("axis", [0, 1, 2])
+@pytest.mark.parametrize("sign", [1, -1])
+def test_propagation_direction_and_axis(orc, axis, sign):
+    """P:377-386 / Alg. 1: the candidate of target p is phi(p + sign*step*e_axis).  Only the
+    neighbour on that side holds the perfect shift, so exactly the matching (axis, sign) pass
+    improves p to D = 0."""
+    lv = _copy_world(orc)
+    nt = len(lv.targets)
+    f = orc.NNF.empty(nt)
+    bad = (1, 1, 0)  # a poor but valid shift for everyone
+    f.dx[:] = bad[0]
+    f.dy[:] = bad[1]
+    f.dt[:] = bad[2]
+    orc.evaluate(lv, f, 50)
+    H, W = lv.H, lv.W
+    p = (4 * H + 6) * W + 6  # centre target
+    off = [0, 0, 0]
+    off[axis] = sign * 2
+    r = ((4 + off[2]) * H + 6 + off[1]) * W + 6 + off[0]
+    sp, sr = lv.slot[p], lv.slot[r]
+    assert sp >= 0 and sr >= 0
+    f.dx[sr], f.dy[sr], f.dt[sr] = 20, 0, 0  # the perfect shift, on one side only
+    orc.evaluate(lv, f, 50)
+    assert f.D[sp] > 0
+    for ax2 in range(3):
+        for sg2 in (1, -1):
+            g = f.copy()
+            orc.propagate(lv, f, g, 50, 2, sg2)
+            got = g.D[sp] == 0 and (g.dx[sp], g.dy[sp], g.dt[sp]) == (20, 0, 0)
+            assert got == (sg2 == sign), (ax2, sg2)
+    g = f.copy()
+    orc.propagate(lv, f, g, 50, 2, 0)  # both directions always see it
+    assert g.D[sp] == 0
+
+
+def test_upsample_spec_example(orc):
+    """coarse shift (2, -1, 3) at (x, y, t) -> fine (4, -2, 3) at (2x, 2y, t); a zero
+    map stays zero where valid; invalid results are re-drawn inside D~ (R21)."""
+    T, H, W = 12, 24, 40
+    rgb = _vol(T, H, W, seed=2)
+    occ = np.zeros((T, H, W), np.uint8)
+    occ[5:7, 10:14, 16:20] = 1
+    fine = _level(orc, rgb, occ)
+    rc, oc = orc.pyramid_down(rgb, occ)
+    coarse = _level(orc, rc, oc)
+    cn = orc.NNF.empty(len(coarse.targets))
+    cn.dx[:] = 2
+    cn.dy[:] = -1
+    cn.dt[:] = 3
+    fn = orc.NNF.empty(len(fine.targets))
+    orc.upsample(coarse, cn, fine, fn, 7, 1)
+    Wc = coarse.W
+    n_ok = 0
+    for s, p in enumerate(fine.targets):
+        t, y, x = p // (H * W), (p // W) % H, p % W
+        q = (t + fn.dt[s], y + fn.dy[s], x + fn.dx[s])
+        assert fine.src[q] == 1  # always valid after repair
+        cs = coarse.slot[(t * coarse.H + y // 2) * Wc + x // 2]
+        want_ok = cs >= 0 and 0 <= t + 3 < T and 0 <= y - 2 < H and 0 <= x + 4 < W and \
+            fine.src[t + 3, y - 2, x + 4] == 1
+        if want_ok:
+            assert (fn.dx[s], fn.dy[s], fn.dt[s]) == (4, -2, 3)
+            n_ok += 1
+    assert n_ok > 100
+    cn.dx[:] = 0
+    cn.dy[:] = 0
+    cn.dt[:] = 0  # zero map: invalid everywhere (targets are not sources), so all re-drawn
+    orc.upsample(coarse, cn, fine, fn, 7, 1)
+    assert all(fine.src[(p // (H * W) + fn.dt[s], (p // W) % H + fn.dy[s], p % W + fn.dx[s])]
+               for s, p in enumerate(fine.targets))

@@ -25,16 +25,36 @@ def main():
     ap.add_argument("--config", default="c5")
     ap.add_argument("--warm", type=int, default=3)
     ap.add_argument("--level", type=int, default=1)
+    ap.add_argument("--random-init", action="store_true",
+                    help="start level 1 from random init + --warm iterations instead of the pipeline")
     args = ap.parse_args()
     c = CONFIGS[args.config]
     v, m, _ = generate(args.config, device="cuda")
     ip = Inpainter(c.W, c.H, c.T, Config(levels=c.levels, lam=c.lam, seed=c.seed), "cuda")
     ip.load(v, m)
+    if args.random_init:
+        st = ip.states[args.level - 1]
+        V.nnf_init_random(st.lv, st.a, ip.prm, 0)
+        V.ann_search(st.lv, st.a, st.b, ip.prm, 0, args.warm)
+    else:
+        # Alg. 4 down to level `level`: onion peel, one outer iteration per coarser level, upsample
+        # + unweighted reconstruction -> the state of the first outer iteration at that level.
+        # RS launches before the timed one: (n_layers + 1 + L - level) * K.
+        ip.onion_peel()
+        for l in range(c.levels, args.level, -1):
+            s_, f_ = ip.states[l - 1], ip.states[l - 2]
+            ip.ann_search(s_, 0)
+            ip.reconstruct(s_, V.WEIGHTED)
+            V.nnf_upsample(s_.lv, s_.a, f_.lv, f_.a, ip.prm)
+            ip.reconstruct(f_, V.UNWEIGHTED)
+        args.warm = 0
     st = ip.states[args.level - 1]
     lv = st.lv
-    V.nnf_init_random(lv, st.a, ip.prm, 0)
-    V.ann_search(lv, st.a, st.b, ip.prm, 0, args.warm)
     torch.cuda.synchronize()
+    if not args.random_init:
+        print(json.dumps(dict(rs_launches_before=(ip.n_layers + 1 + c.levels - args.level) * 10,
+                              prop_launches_before=(ip.n_layers + 1 + c.levels - args.level) * 40,
+                              rec_launches_before=ip.n_layers + 2 * (c.levels - args.level))))
     cnt = torch.zeros(1, dtype=torch.int64, device="cuda")
     res = []
 
