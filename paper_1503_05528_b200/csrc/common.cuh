@@ -58,16 +58,34 @@ vinp_status launch_reconstruct(vinp_level* lv, const vinp_nnf* nnf, int mode, in
                                int commit, void* stream);
 
 // ---------------------------------------------------------------- geometry
+// Division by the invariant W and HW via multiply-high: for 0 <= n < 2^31 and d >= 1,
+// floor(n / d) = (n * m) >> (32 + s) with s = ceil(log2 d), m = floor(2^(32+s) / d) + 1
+// (error n*(m - 2^(32+s)/d)/2^(32+s) < 2^-(1+s) <= 1/(2d), below the gap to the next integer).
 struct Geo {
   int W, H, T;
   int HW;
+  uint64_t mW, mHW;
+  int sW, sHW;
 };
-inline Geo geo_of(const vinp_level* lv) { return Geo{lv->W, lv->H, lv->T, lv->W * lv->H}; }
+inline void magic_of(uint32_t d, uint64_t& m, int& s) {
+  s = 0;
+  while ((1ull << s) < d) ++s;
+  m = ((1ull << (32 + s)) / d) + 1;
+}
+inline Geo geo_of(const vinp_level* lv) {
+  Geo g{lv->W, lv->H, lv->T, lv->W * lv->H, 0, 0, 0, 0};
+  magic_of((uint32_t)g.W, g.mW, g.sW);
+  magic_of((uint32_t)g.HW, g.mHW, g.sHW);
+  return g;
+}
+__device__ __forceinline__ int fdiv(uint32_t n, uint64_t m, int s) {
+  return (int)(((uint64_t)n * m) >> (32 + s));  // n < 2^31, m <= 2^33: the product fits in 64 bits
+}
 
 __device__ __forceinline__ void decode(const Geo& g, int p, int& x, int& y, int& t) {
-  t = p / g.HW;
+  t = fdiv((uint32_t)p, g.mHW, g.sHW);
   int r = p - t * g.HW;
-  y = r / g.W;
+  y = fdiv((uint32_t)r, g.mW, g.sW);
   x = r - y * g.W;
 }
 

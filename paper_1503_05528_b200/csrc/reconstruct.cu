@@ -65,15 +65,14 @@ __global__ void __launch_bounds__(256) k_reconstruct(ReconArgs a, int mode, int 
   if (layer_j >= 0 && a.layer[p] != layer_j) return;
   int px, py, pt;
   decode(a.g, p, px, py, pt);
-  uint64_t key[4];
   uint32_t Dq[4], nq[4];
   uint64_t val[4];
   unsigned valid = 0;
+  bool n125 = true;  // every valid contributor has a full patch (n = 125)
 #pragma unroll
   for (int i = 0; i < 4; ++i) {
     int v = lane + 32 * i;
-    key[i] = ~0ull;
-    Dq[i] = 0; nq[i] = 1; val[i] = 0;
+    Dq[i] = 0; nq[i] = 125; val[i] = 0;
     if (v < kPatch) {
       int dx, dy, dt;
       voff(v, dx, dy, dt);
@@ -88,8 +87,8 @@ __global__ void __launch_bounds__(256) k_reconstruct(ReconArgs a, int mode, int 
               uint64_t e = __ldg(reinterpret_cast<const unsigned long long*>(a.e) + s);
               Dq[i] = e_D(e);
               nq[i] = n;
+              n125 &= (n == 125);
               val[i] = __ldg(reinterpret_cast<const unsigned long long*>(a.vox) + (e_q(e) - off));
-              if (n > 0) key[i] = (uint64_t)__double_as_longlong((double)Dq[i] / (double)n);
               valid |= 1u << i;
             }
           }
@@ -99,10 +98,25 @@ __global__ void __launch_bounds__(256) k_reconstruct(ReconArgs a, int mode, int 
   }
   uint32_t m = __reduce_add_sync(kFull, (uint32_t)__popc(valid));
   if (m == 0) return;
+  n125 = __all_sync(kFull, n125);
+  // exact order keys of d^2 = D/(4n): D itself when every n = 125 (fast path), else the fp64
+  // bit pattern of D/n (distinct rationals with n <= 125 are distinct, ordered doubles)
+  uint64_t key[4];
+  if (mode != VINP_UNWEIGHTED) {
+#pragma unroll
+    for (int i = 0; i < 4; ++i)
+      key[i] = !(valid >> i & 1) ? ~0ull
+               : n125 ? (uint64_t)Dq[i]
+                      : (uint64_t)__double_as_longlong((double)Dq[i] / (double)nq[i]);
+  }
   int64_t w[4];
   if (mode == VINP_BEST_PATCH) {
-    uint64_t kmin = min(min(key[0], key[1]), min(key[2], key[3]));
-    kmin = warp_min64(kmin);
+    uint64_t kmin;
+    if (n125) {
+      kmin = __reduce_min_sync(kFull, (uint32_t)min(min(key[0], key[1]), min(key[2], key[3])));
+    } else {
+      kmin = warp_min64(min(min(key[0], key[1]), min(key[2], key[3])));
+    }
     uint32_t vbest = 0xffffffffu;
 #pragma unroll
     for (int i = 3; i >= 0; --i)
@@ -114,73 +128,85 @@ __global__ void __launch_bounds__(256) k_reconstruct(ReconArgs a, int mode, int 
 #pragma unroll
     for (int i = 0; i < 4; ++i) w[i] = (valid >> i) & 1;
   } else {
-    // sigma^2 key: the r-th smallest key, r = ceil(0.75 m) (nearest rank, R10).  The key is the
-    // fp64 bit pattern of D/n (positive, so unsigned order = numeric order).  Rank search on the
-    // high 32 bits first, from the highest bit where the keys differ; only when keys sharing the
-    // selected high half differ in their low half is the low half searched as well.
+    // sigma^2 key: the r-th smallest key, r = ceil(0.75 m) (nearest rank, R10), by a bitwise rank
+    // search (one REDUX.SUM per bit) on the high 32 key bits from the first bit where the warp's
+    // keys differ; the low 32 bits are searched only if the selected high half is shared by
+    // unequal keys.  In the n = 125 fast path the key is D (high half 0).
     uint32_t r = (3 * m + 3) / 4;
     uint32_t hi[4], lo[4];
 #pragma unroll
     for (int i = 0; i < 4; ++i) {
-      hi[i] = (uint32_t)(key[i] >> 32);
-      lo[i] = (uint32_t)key[i];
+      hi[i] = n125 ? (uint32_t)key[i] : (uint32_t)(key[i] >> 32);  // ~0 for invalid
+      lo[i] = n125 ? 0u : (uint32_t)key[i];
     }
     uint32_t hmin = __reduce_min_sync(kFull, min(min(hi[0], hi[1]), min(hi[2], hi[3])));
     uint32_t hmax = __reduce_max_sync(kFull, max(max((valid & 1) ? hi[0] : 0u, (valid & 2) ? hi[1] : 0u),
                                                  max((valid & 4) ? hi[2] : 0u, (valid & 8) ? hi[3] : 0u)));
-    uint32_t ans = hmin & ~((hmax ^ hmin) ? (0xffffffffu >> __clz(hmax ^ hmin)) : 0u);
-    for (int bit = 31 - (hmax ^ hmin ? __clz(hmax ^ hmin) : 32); bit >= 0; --bit) {
+    uint32_t x = hmax ^ hmin;
+    uint32_t ans = hmin & ~(x ? (0xffffffffu >> __clz(x)) : 0u);
+    for (int bit = 31 - (x ? __clz(x) : 32); bit >= 0; --bit) {
       uint32_t T = ans | ((1u << bit) - 1);
       uint32_t c = 0;
 #pragma unroll
-      for (int i = 0; i < 4; ++i) c += hi[i] <= T;  // invalid keys are ~0: never counted (T < ~0)
+      for (int i = 0; i < 4; ++i) c += ((valid >> i & 1) && hi[i] <= T);
       c = __reduce_add_sync(kFull, c);
       if (c < r) ans |= 1u << bit;
     }
-    // keys whose high half equals ans: resolve the low half if they are not all equal
-    uint32_t below = 0, lmin = 0xffffffffu, lmax = 0;
+    uint32_t lans = 0;
+    if (!n125) {
+      uint32_t below = 0, lmin = 0xffffffffu, lmax = 0;
 #pragma unroll
-    for (int i = 0; i < 4; ++i) {
-      below += hi[i] < ans;
-      if (hi[i] == ans && (valid >> i & 1)) { lmin = min(lmin, lo[i]); lmax = max(lmax, lo[i]); }
-    }
-    below = __reduce_add_sync(kFull, below);
-    lmin = __reduce_min_sync(kFull, lmin);
-    lmax = __reduce_max_sync(kFull, lmax);
-    uint32_t lans = lmin;
-    if (lmin != lmax) {
-      uint32_t r2 = r - below;
-      lans = lmin & ~(0xffffffffu >> __clz(lmax ^ lmin));
-      for (int bit = 31 - __clz(lmax ^ lmin); bit >= 0; --bit) {
-        uint32_t T = lans | ((1u << bit) - 1);
-        uint32_t c = 0;
+      for (int i = 0; i < 4; ++i) {
+        below += (valid >> i & 1) && hi[i] < ans;
+        if (hi[i] == ans && (valid >> i & 1)) { lmin = min(lmin, lo[i]); lmax = max(lmax, lo[i]); }
+      }
+      below = __reduce_add_sync(kFull, below);
+      lmin = __reduce_min_sync(kFull, lmin);
+      lmax = __reduce_max_sync(kFull, lmax);
+      lans = lmin;
+      if (lmin != lmax) {
+        uint32_t r2 = r - below;
+        lans = lmin & ~(0xffffffffu >> __clz(lmax ^ lmin));
+        for (int bit = 31 - __clz(lmax ^ lmin); bit >= 0; --bit) {
+          uint32_t T = lans | ((1u << bit) - 1);
+          uint32_t c = 0;
 #pragma unroll
-        for (int i = 0; i < 4; ++i) c += (hi[i] == ans && (valid >> i & 1) && lo[i] <= T);
-        c = __reduce_add_sync(kFull, c);
-        if (c < r2) lans |= 1u << bit;
+          for (int i = 0; i < 4; ++i) c += (hi[i] == ans && (valid >> i & 1) && lo[i] <= T);
+          c = __reduce_add_sync(kFull, c);
+          if (c < r2) lans |= 1u << bit;
+        }
       }
     }
-    uint64_t kans = ((uint64_t)ans << 32) | lans;
-    // a representative (D_s, n_s) with key == kans (equal keys are equal rationals)
-    int own = -1;
+    uint32_t Ds, ns;
+    if (n125) {
+      Ds = ans;
+      ns = 125;
+    } else {
+      uint64_t kans = ((uint64_t)ans << 32) | lans;
+      // a representative (D_s, n_s) with key == kans (equal keys are equal rationals)
+      int own = -1;
 #pragma unroll
-    for (int i = 3; i >= 0; --i)
-      if ((valid >> i & 1) && key[i] == kans) own = i;
-    unsigned bal = __ballot_sync(kFull, own >= 0);
-    int src = __ffs(bal) - 1;
-    uint32_t myD = 0, myn = 1;
+      for (int i = 3; i >= 0; --i)
+        if ((valid >> i & 1) && key[i] == kans) own = i;
+      unsigned bal = __ballot_sync(kFull, own >= 0);
+      int src = __ffs(bal) - 1;
+      uint32_t myD = 0, myn = 1;
 #pragma unroll
-    for (int i = 0; i < 4; ++i)
-      if (i == own) { myD = Dq[i]; myn = nq[i]; }
-    uint32_t Ds = __shfl_sync(kFull, myD, src), ns = __shfl_sync(kFull, myn, src);
+      for (int i = 0; i < 4; ++i)
+        if (i == own) { myD = Dq[i]; myn = nq[i]; }
+      Ds = __shfl_sync(kFull, myD, src);
+      ns = __shfl_sync(kFull, myn, src);
+    }
 #pragma unroll
     for (int i = 0; i < 4; ++i) {
       if (!(valid >> i & 1)) { w[i] = 0; continue; }
       if (Ds == 0) {
         w[i] = Dq[i] == 0;
       } else {
-        double an = (double)((uint64_t)Dq[i] * ns);
-        double ad = (double)(2ull * nq[i] * Ds);
+        // a = D_q n_s / (2 n_q D_s): one correctly rounded division of exact operands (with all
+        // n = 125 the same real quotient as D_q / (2 D_s), hence the same double)
+        double an = n125 ? (double)Dq[i] : (double)((uint64_t)Dq[i] * ns);
+        double ad = n125 ? (double)(2ull * Ds) : (double)(2ull * nq[i] * Ds);
         double aa = __ddiv_rn(an, ad);
         w[i] = __double2ll_rn(__dmul_rn(exp(-aa), 68719476736.0));
       }

@@ -1,0 +1,125 @@
+"""Full-size parity at BASELINE.json's c5 (1920x1080x100, L=4) in the launch configuration bench.py
+times, on sampled outputs the oracle can compute one range at a time.
+
+Setup stages: per-frame oracle pyramid / texture on sampled frames (both operate frame by frame)
+and the sets on a temporal window around sampled frames.  Passes: the GPU state is brought to
+the first outer iteration of level 1 exactly as Alg. 4 does (onion peel, one outer iteration per
+coarse level, upsample, unweighted reconstruction); then evaluate / propagate / random search /
+weighted reconstruction run on the GPU over the whole level and the oracle recomputes sampled
+contiguous slot (hole) ranges from the same input state: bit-exact NNF entries and counts-free
+equality, fp32 hole values within 1e-3."""
+import numpy as np
+import pytest
+import torch
+
+from gen.synth import CONFIGS, generate
+import oracle_ops as OO
+
+pytestmark = pytest.mark.gpu
+
+
+@pytest.fixture(scope="module")
+def c5():
+    from paper_1503_05528_b200 import Config, Inpainter, vinp as V
+    c = CONFIGS["c5"]
+    v, m, _ = generate("c5", device="cuda")
+    ip = Inpainter(c.W, c.H, c.T, Config(levels=c.levels, pm_iters=c.pm_iters, lam=c.lam, seed=c.seed), "cuda")
+    ip.load(v, m)
+    torch.cuda.synchronize()
+    return ip, v, m
+
+
+def test_c5_setup_sampled_frames(orc, c5):
+    ip, v, m = c5
+    rgb = v.cpu().numpy()
+    occ = m.cpu().numpy()
+    L = ip.cfg.levels
+    for t in (3, 49, 96):
+        r, o = rgb[t:t + 1], occ[t:t + 1]
+        tex1 = orc.texture(r, o, 2 ** (L - 2))
+        for l, lv in enumerate(ip.levels):
+            vb = lv.vox.view(torch.uint8).view(lv.T, lv.H, lv.W, 8)[t].cpu().numpy()
+            fl = lv.flags.view(lv.T, lv.H, lv.W)[t].cpu().numpy()
+            assert np.array_equal(fl & 1, o[0]), (t, l)
+            assert np.array_equal(vb[..., :3], r[0]), (t, l)
+            tl = tex1 if l == 0 else orc.texture_decimate(tex1, l + 1, lv.W, lv.H)
+            assert np.array_equal(vb[..., 4:6], tl[0]), (t, l)
+            if l + 1 < L:
+                r, o = orc.pyramid_down(r, o)
+    lv = ip.levels[0]
+    for t in (2, 50, 97):
+        t0, t1 = max(0, t - 2), min(lv.T, t + 3)
+        src, tgt = orc.sets(np.ascontiguousarray(occ[t0:t1]))
+        fl = lv.flags.view(lv.T, lv.H, lv.W)[t].cpu().numpy()
+        assert np.array_equal((fl >> 1) & 1, src[t - t0]) and np.array_equal((fl >> 2) & 1, tgt[t - t0])
+
+
+def _ranges(n, k=6, width=400):
+    rng = np.random.default_rng(n)
+    starts = sorted(set([0, max(0, n - width)] + list(rng.integers(0, max(1, n - width), k))))
+    return [(int(b), int(min(n, b + width))) for b in starts]
+
+
+def test_c5_level1_passes_sampled_ranges(orc, c5):
+    from paper_1503_05528_b200 import vinp as V
+    ip, _, _ = c5
+    c = CONFIGS["c5"]
+    ip.onion_peel()
+    for l in range(c.levels, 1, -1):
+        s_, f_ = ip.states[l - 1], ip.states[l - 2]
+        ip.ann_search(s_, 0)
+        ip.reconstruct(s_, V.WEIGHTED)
+        V.nnf_upsample(s_.lv, s_.a, f_.lv, f_.a, ip.prm)
+        ip.reconstruct(f_, V.UNWEIGHTED)
+    st = ip.states[0]
+    lv = st.lv
+    prm = ip.prm
+    # host copy of level 1 in the GPU layout, for the oracle adapter
+    host = V.Level(lv.W, lv.H, lv.T, 1, torch.device("cpu"))
+    for name in ("vox", "flags", "slot", "targets", "holes", "sources"):
+        setattr(host, name, getattr(lv, name).cpu())
+    host.n_targets, host.n_holes, host.n_sources = lv.n_targets, lv.n_holes, lv.n_sources
+    ol = OO._OLevel(host)
+
+    def gpu_nnf(x):
+        return V.NNF(x.e.cpu(), x.n.cpu())
+
+    checks = 0
+    # evaluate
+    f_pre = OO._to_orc(host, gpu_nnf(st.a))
+    V.nnf_evaluate(lv, st.a, prm)
+    f_in = OO._to_orc(host, gpu_nnf(st.a))
+    # propagate (s = 8, sign +1) and random search (k = 1) over the whole level on the GPU
+    V.propagate(lv, st.a, st.b, prm, 8, 1)
+    g_prop = gpu_nnf(st.b)
+    st.a, st.b = st.b, st.a
+    V.random_search(lv, st.a, st.b, prm, 0, 1)
+    g_rs = gpu_nnf(st.b)
+    f_prop = OO._to_orc(host, g_prop)
+    f_rs = OO._to_orc(host, g_rs)
+    for b, e in _ranges(lv.n_targets):
+        f_ev = f_pre.copy()
+        orc.evaluate(ol, f_ev, prm.lam, -1, -1, b, e)
+        assert np.array_equal(f_ev.D[b:e], f_in.D[b:e]) and np.array_equal(f_ev.n[b:e], f_in.n[b:e])
+        g = f_in.copy()
+        orc.propagate(ol, f_in, g, prm.lam, 8, 1, -1, -1, b, e)
+        for arr in ("dx", "dy", "dt", "D"):
+            assert np.array_equal(getattr(g, arr)[b:e], getattr(f_prop, arr)[b:e]), ("propagate", arr, b)
+        g2 = f_prop.copy()
+        orc.random_search(ol, f_prop, g2, prm.lam, prm.seed, prm.rho, ol.rmax, 1, 0, 1, -1, -1, b, e)
+        for arr in ("dx", "dy", "dt", "D"):
+            assert np.array_equal(getattr(g2, arr)[b:e], getattr(f_rs, arr)[b:e]), ("random search", arr, b)
+        checks += e - b
+    # weighted reconstruction of sampled hole ranges from the random-search NNF
+    st.a, st.b = st.b, st.a
+    V.reconstruct(lv, st.a, V.WEIGHTED, st.cur_rgb, st.cur_tex, commit=False)
+    g_rgb = st.cur_rgb[:lv.n_holes].cpu().numpy()
+    g_tex = st.cur_tex[:lv.n_holes].cpu().numpy()
+    f_a = OO._to_orc(host, gpu_nnf(st.a))
+    o_rgb = np.zeros((lv.n_holes, 3), np.float32)
+    o_tex = np.zeros((lv.n_holes, 2), np.float32)
+    for hb, he in _ranges(lv.n_holes):
+        orc.reconstruct(ol, f_a, orc.WEIGHTED, -1, hb, he, o_rgb, o_tex)
+        assert np.abs(o_rgb[hb:he] - g_rgb[hb:he]).max() <= 1e-3
+        assert np.abs(o_tex[hb:he] - g_tex[hb:he]).max() <= 1e-3
+    assert checks > 2000
