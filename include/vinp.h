@@ -198,13 +198,28 @@ vinp_status vinp_energy(const vinp_level* lv, const vinp_nnf* nnf, double* out, 
 size_t vinp_brute_force_ws_bytes(const vinp_level* lv);
 vinp_status vinp_brute_force(const vinp_level* lv, vinp_nnf* out, const vinp_params* prm, int32_t b,
                              int32_t e, void* ws, size_t ws_bytes, void* stream);
+/* The same exact NN over an explicit list of target slots (CUDA cores). */
+vinp_status vinp_brute_force_list(const vinp_level* lv, vinp_nnf* out, const vinp_params* prm,
+                                  const int32_t* list, int32_t n, void* stream);
+/* Tensor-core form (north_star: "optional exact brute-force NN mode expressed as a dense
+ * contraction"): for targets whose patch lies inside Omega, D(p,q) = E(p) + E(q) - 2(4 X_c + lambda
+ * X_t) with X the u8 patch dot products computed by tcgen05.mma kind::i8 (colour K = 384, texture
+ * K = 256), minimised exactly in the epilogue (ties -> smallest q); border targets go to the CUDA-core
+ * path.  Same result as vinp_brute_force, bit for bit.  Synchronises once (target counts).
+ * ws: vinp_brute_force_tc_ws_bytes(lv, b, e) (holds the im2col rows: 640 B per target and source). */
+size_t vinp_brute_force_tc_ws_bytes(const vinp_level* lv, int32_t b, int32_t e);
+vinp_status vinp_brute_force_tc(const vinp_level* lv, vinp_nnf* out, const vinp_params* prm, int32_t b,
+                                int32_t e, void* ws, size_t ws_bytes, void* stream);
 
 /* ---- test hooks ----
  * vinp_patch_ssd: D and n of pairs (p[i], q[i]) with known set kb (q must be in D~).
- * vinp_philox: out[i][0..3] = Philox4x32-10(ctr[i][0..3], key = seed). */
+ * vinp_philox: out[i][0..3] = Philox4x32-10(ctr[i][0..3], key = seed).
+ * vinp_tc_gemm_u8: C[128][128] (s32) = A[128][K] * B[128][K]^T for u8 A, B (K % 32 == 0, K <= 512),
+ * one tcgen05.mma kind::i8 tile — pins the tensor-core plumbing used by the exact NN mode. */
 vinp_status vinp_patch_ssd(const vinp_level* lv, const int32_t* p, const int32_t* q, int64_t n,
                            const vinp_params* prm, int kb, uint32_t* D, uint8_t* cnt, void* stream);
 vinp_status vinp_philox(const uint32_t* ctr, int64_t n, uint64_t seed, uint32_t* out, void* stream);
+vinp_status vinp_tc_gemm_u8(const uint8_t* A, const uint8_t* B, int K, int32_t* C, void* stream);
 
 #ifdef __cplusplus
 }

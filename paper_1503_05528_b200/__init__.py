@@ -1,7 +1,23 @@
 """B200 (sm_100a) hot path of Newson et al., "Video inpainting of complex scenes" (arXiv 1503.05528).
 
-libvinp.so (include/vinp.h) holds every kernel; `vinp` is its ctypes binding and `inpaint`
-the Alg. 4 driver.  Importing this package loads libvinp.so and raises if it is missing.
+libvinp.so (include/vinp.h) holds every kernel; `vinp` is its ctypes binding and `inpaint` the
+Alg. 4 driver.  Exports are resolved lazily so that `paper_1503_05528_b200.build` can run before
+the library exists; any use of the binding loads libvinp.so and raises if it is missing (there
+is no CPU fallback).
 """
-from . import vinp  # noqa: F401  (loads libvinp.so; no fallback)
-from .inpaint import Config, Exchange, Inpainter, inpaint  # noqa: F401
+import importlib
+
+_EXPORTS = {"vinp": (".vinp", None), "Config": (".inpaint", "Config"),
+            "Exchange": (".inpaint", "Exchange"), "Inpainter": (".inpaint", "Inpainter"),
+            "inpaint": (".inpaint", "inpaint")}
+
+
+def __getattr__(name):
+    if name in _EXPORTS:
+        mod, attr = _EXPORTS[name]
+        m = importlib.import_module(mod, __name__)
+        return m if attr is None else getattr(m, attr)
+    raise AttributeError(name)
+
+
+__all__ = list(_EXPORTS)

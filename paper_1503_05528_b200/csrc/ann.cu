@@ -84,6 +84,9 @@ __global__ void k_upsample(LevelArgs c, const uint64_t* __restrict__ ce, LevelAr
 #ifndef VINP_MINB
 #define VINP_MINB 3
 #endif
+#ifndef VINP_PROP_MINB
+#define VINP_PROP_MINB 4
+#endif
 #ifndef VINP_GROUP
 #define VINP_GROUP 8
 #endif
@@ -183,7 +186,7 @@ __global__ void __launch_bounds__(256) k_evaluate(LevelArgs a, uint64_t* __restr
 // Lane = target (thread-per-target, coherent candidates).  Candidates of rank 1..3 are evaluated
 // one rank at a time by all lanes that have one, each against the running best of its own target
 // (strict improvement in rank order, R25).
-__global__ void __launch_bounds__(256) k_propagate(LevelArgs a, const uint64_t* __restrict__ ein,
+__global__ void __launch_bounds__(256, VINP_PROP_MINB) k_propagate(LevelArgs a, const uint64_t* __restrict__ ein,
                                                    uint64_t* __restrict__ eout, int lambda, int step,
                                                    int sign, int kb, int only_layer, int32_t b,
                                                    int32_t e, const int32_t* __restrict__ list,
@@ -230,6 +233,21 @@ __global__ void __launch_bounds__(256) k_propagate(LevelArgs a, const uint64_t* 
       if (dup) q[c] = -1;
     }
   }
+  // compact this lane's candidates to the front (rank order kept), so that the warp runs the
+  // SSD loop once per candidate *slot* rather than once per neighbour rank any lane has
+  int cq[NCMAX];
+  int ncand = 0;
+#pragma unroll
+  for (int c = 0; c < NCMAX; ++c) cq[c] = -1;
+#pragma unroll
+  for (int c = 0; c < NCMAX; ++c) {
+    if (act && q[c] >= 0) {
+#pragma unroll
+      for (int d = 0; d < NCMAX; ++d)
+        if (d == ncand) cq[d] = q[c];
+      ++ncand;
+    }
+  }
   uint32_t bestD = e_D(inc);
   int bestq = q0;
   unsigned cnt = 0;
@@ -238,15 +256,15 @@ __global__ void __launch_bounds__(256) k_propagate(LevelArgs a, const uint64_t* 
   bool allfull = __all_sync(kFull, full || !act);
 #pragma unroll
   for (int c = 0; c < NCMAX; ++c) {
-    bool mine = act && q[c] >= 0;
-    if (!__any_sync(kFull, mine)) continue;
+    bool mine = c < ncand;
+    if (!__any_sync(kFull, mine)) break;
     if (mine) {
       bool alive = true;
-      uint32_t D = allfull ? thread_ssd<true>(a, p, px, py, pt, q[c], lambda, kb, true, bestD, alive)
-                           : thread_ssd<true>(a, p, px, py, pt, q[c], lambda, kb, full, bestD, alive);
+      uint32_t D = allfull ? thread_ssd<true>(a, p, px, py, pt, cq[c], lambda, kb, true, bestD, alive)
+                           : thread_ssd<true>(a, p, px, py, pt, cq[c], lambda, kb, full, bestD, alive);
       if (alive && D < bestD) {
         bestD = D;
-        bestq = q[c];
+        bestq = cq[c];
       }
       ++cnt;
     }
@@ -489,11 +507,12 @@ __global__ void __launch_bounds__(32 * WPB, VINP_MINB * 8 / WPB) k_random_search
 // cannot become the (first) minimum.  The block then takes the lexicographic min of (D, i).
 __global__ void __launch_bounds__(256) k_brute_force(LevelArgs a, uint64_t* __restrict__ ee,
                                                      uint8_t* __restrict__ en, int lambda, int32_t b,
-                                                     int32_t e) {
+                                                     int32_t e, const int32_t* __restrict__ list) {
   constexpr int G = 8;
   int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
-  int s = b + blockIdx.x;
-  if (s >= e) return;
+  int idx = b + blockIdx.x;
+  if (idx >= e) return;
+  int s = list ? list[idx] : idx;
   int p = a.targets[s];
   PatchLanes L;
   init_lanes(L, a.g, lane);
@@ -803,10 +822,20 @@ vinp_status vinp_brute_force(const vinp_level* lv, vinp_nnf* out, const vinp_par
   }
   if (e > b) {
     k_brute_force<<<e - b, 32 * kWarpsPerBlock, 0, S(stream)>>>(args_of(lv), out->e, out->n,
-                                                                 prm->lambda, b, e);
+                                                                 prm->lambda, b, e, nullptr);
     count_launch();
   }
   return check_launch("vinp_brute_force");
+}
+
+vinp_status vinp_brute_force_list(const vinp_level* lv, vinp_nnf* out, const vinp_params* prm,
+                                  const int32_t* list, int32_t n, void* stream) {
+  if (n > 0) {
+    k_brute_force<<<n, 32 * kWarpsPerBlock, 0, S(stream)>>>(args_of(lv), out->e, out->n, prm->lambda, 0,
+                                                             n, list);
+    count_launch();
+  }
+  return check_launch("vinp_brute_force_list");
 }
 
 vinp_status vinp_patch_ssd(const vinp_level* lv, const int32_t* p, const int32_t* q, int64_t n,

@@ -73,8 +73,12 @@ def _load():
         "vinp_energy": (I, [P, P, P, P]),
         "vinp_brute_force_ws_bytes": (C.c_size_t, [P]),
         "vinp_brute_force": (I, [P, P, P, I32, I32, P, C.c_size_t, P]),
+        "vinp_brute_force_list": (I, [P, P, P, P, I32, P]),
+        "vinp_brute_force_tc_ws_bytes": (C.c_size_t, [P, I32, I32]),
+        "vinp_brute_force_tc": (I, [P, P, P, I32, I32, P, C.c_size_t, P]),
         "vinp_patch_ssd": (I, [P, P, P, I64, P, I, P, P, P]),
         "vinp_philox": (I, [P, I64, U64, P, P]),
+        "vinp_tc_gemm_u8": (I, [P, P, I, P, P]),
     }
     for name, (res, args) in sigs.items():
         f = getattr(lib, name)
@@ -91,7 +95,8 @@ EXPORTED = [
     "vinp_nnf_evaluate", "vinp_propagate", "vinp_random_search", "vinp_ann_search",
     "vinp_onion_ws_bytes", "vinp_onion_peel",
     "vinp_reconstruct", "vinp_commit", "vinp_change_l1", "vinp_energy",
-    "vinp_brute_force_ws_bytes", "vinp_brute_force", "vinp_patch_ssd", "vinp_philox"]
+    "vinp_brute_force_ws_bytes", "vinp_brute_force", "vinp_patch_ssd", "vinp_philox",
+    "vinp_tc_gemm_u8", "vinp_brute_force_list", "vinp_brute_force_tc_ws_bytes", "vinp_brute_force_tc"]
 
 
 def _check(rc: int, what: str):
@@ -330,6 +335,21 @@ def brute_force(lv, nnf, prm, b=0, e=None, ws=None):
                                  ws.numel(), _stream()), "vinp_brute_force")
 
 
+def brute_force_tc(lv, nnf, prm, b=0, e=None, ws=None):
+    """Exact NN on the tensor cores (tcgen05 kind::i8); border targets on CUDA cores."""
+    e = lv.n_targets if e is None else e
+    nbytes = int(_lib.vinp_brute_force_tc_ws_bytes(lv.struct(), b, e))
+    if ws is None or ws.numel() < nbytes:
+        ws = torch.empty(nbytes, dtype=torch.uint8, device=lv.device)
+    _check(_lib.vinp_brute_force_tc(lv.struct(), nnf.struct(), C.byref(prm.struct()), b, e, _ptr(ws),
+                                    ws.numel(), _stream()), "vinp_brute_force_tc")
+
+
+def brute_force_list(lv, nnf, prm, slots: torch.Tensor):
+    _check(_lib.vinp_brute_force_list(lv.struct(), nnf.struct(), C.byref(prm.struct()), _ptr(slots),
+                                      slots.numel(), _stream()), "vinp_brute_force_list")
+
+
 def patch_ssd(lv, p, q, prm, kb=-1):
     n = p.numel()
     D = torch.empty(n, dtype=torch.int32, device=lv.device)
@@ -343,3 +363,11 @@ def philox(ctr: torch.Tensor, seed: int):
     out = torch.empty_like(ctr)
     _check(_lib.vinp_philox(_ptr(ctr), ctr.shape[0], seed, _ptr(out), _stream()), "vinp_philox")
     return out
+
+
+def tc_gemm_u8(A: torch.Tensor, B: torch.Tensor):
+    """C = A B^T on the tensor cores (tcgen05 kind::i8); A, B u8 [128, K]."""
+    K = A.shape[1]
+    C = torch.empty((128, 128), dtype=torch.int32, device=A.device)
+    _check(_lib.vinp_tc_gemm_u8(_ptr(A), _ptr(B), K, _ptr(C), _stream()), "vinp_tc_gemm_u8")
+    return C

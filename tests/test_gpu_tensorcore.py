@@ -1,0 +1,37 @@
+"""Tensor-core (tcgen05.mma kind::i8) plumbing of the exact-NN mode, pinned by integer matmul."""
+import numpy as np
+import pytest
+import torch
+
+pytestmark = pytest.mark.gpu
+
+
+@pytest.mark.parametrize("K", [32, 64, 384, 512])
+def test_tc_gemm_u8_matches_integer_matmul(K):
+    from paper_1503_05528_b200 import vinp as V
+    rng = np.random.default_rng(K)
+    A = rng.integers(0, 256, (128, K), dtype=np.uint8)
+    B = rng.integers(0, 256, (128, K), dtype=np.uint8)
+    A[0] = 255
+    B[0] = 255  # 255*255*K: the largest value of a u8 dot product
+    C = V.tc_gemm_u8(torch.from_numpy(A).cuda(), torch.from_numpy(B).cuda()).cpu().numpy()
+    ref = A.astype(np.int64) @ B.astype(np.int64).T
+    assert np.array_equal(C.astype(np.int64), ref)
+
+
+@pytest.mark.parametrize("case,lam", [("c1", 50), ("odd", 0), ("odd", 126), ("c2", 50)])
+def test_brute_force_tc_equals_cuda_core(case, lam):
+    """Tensor-core exact NN == CUDA-core exact NN (itself bit-exact vs the oracle), bit for bit."""
+    import time
+    from test_gpu_parity import _setup
+    from paper_1503_05528_b200 import vinp as V
+    ip, _, _ = _setup(case, lam)
+    lv = ip.levels[0]
+    n = lv.n_targets if case != "c2" else 6000
+    for b, e in ((0, n), (lv.n_targets // 2, min(lv.n_targets, lv.n_targets // 2 + 3000))):
+        x = V.NNF.alloc(lv.n_targets, "cuda")
+        y = V.NNF.alloc(lv.n_targets, "cuda")
+        V.brute_force(lv, x, ip.prm, b, e)
+        V.brute_force_tc(lv, y, ip.prm, b, e)
+        torch.cuda.synchronize()
+        assert torch.equal(x.e[b:e], y.e[b:e]) and torch.equal(x.n[b:e], y.n[b:e]), (case, lam, b)
