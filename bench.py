@@ -326,8 +326,10 @@ def measure_roofline(ip, v, m, dev):
             a["launches"] += 1
             a["pu"] += pu
     tot = sum(a["ms"] for a in agg.values())
-    dom = max(agg, key=lambda k: agg[k]["ms"])
-    a = agg[dom]
+    # the roofline line is the dominant (kernel, level) pair: that is where ncu captures the
+    # DRAM traffic (profiles/traffic.json) of one launch
+    dom = max(per_level, key=lambda k: per_level[k]["ms"])
+    a = per_level[dom]
     achieved = a["bytes"] / (a["ms"] / 1000.0) / 1e9
     kernels = {k: {"share": round(x["ms"] / tot, 4), "GB/s": round(x["bytes"] / (x["ms"] / 1000) / 1e9, 1),
                    "launches": x["launches"], "patch_updates": x["pu"]} for k, x in agg.items()}
@@ -340,7 +342,8 @@ def measure_roofline(ip, v, m, dev):
     return {"kernel": f"vinp_{dom}", "bound": "hbm", "achieved": round(achieved, 1), "peak": peak,
             "peak_kind": kind, "unit": "GB/s", "frac": round(achieved / peak, 4),
             "traffic": traffic, "bytes_per_launch": a["bytes"] / a["launches"],
-            "avg_launch_ms": a["ms"] / a["launches"], "kernels": kernels,
+            "avg_launch_ms": a["ms"] / a["launches"], "share_of_step": round(a["ms"] / tot, 4),
+            "kernels": kernels,
             "by_level": {k: {"ms": round(x["ms"], 2), "GB/s": round(x["bytes"] / (x["ms"] / 1000) / 1e9, 1),
                              "launches": x["launches"], "patch_updates": x["pu"]}
                          for k, x in sorted(per_level.items())}}
