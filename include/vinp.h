@@ -211,6 +211,13 @@ size_t vinp_brute_force_tc_ws_bytes(const vinp_level* lv, int32_t b, int32_t e);
 vinp_status vinp_brute_force_tc(const vinp_level* lv, vinp_nnf* out, const vinp_params* prm, int32_t b,
                                 int32_t e, void* ws, size_t ws_bytes, void* stream);
 
+/* ---- App. B Monte-Carlo (Table 2; NEXT #3): *hits (device) += number of trials t in
+ * [trial0, trial0 + n_trials) in which a random patch V beats the constant patch Z = mu for a random
+ * reference W (N i.i.d. N(mu, sigma^2) components; fp64 Box-Muller on Philox, counter (t lo, t hi,
+ * 4<<16 | k, 0)).  Probability estimate = hits / n_trials. */
+vinp_status vinp_patch_ambiguity(int N, double sigma, uint64_t seed, uint64_t trial0, uint64_t n_trials,
+                                 unsigned long long* hits, void* stream);
+
 /* ---- test hooks ----
  * vinp_patch_ssd: D and n of pairs (p[i], q[i]) with known set kb (q must be in D~).
  * vinp_philox: out[i][0..3] = Philox4x32-10(ctr[i][0..3], key = seed).

@@ -792,3 +792,65 @@ int or_inpaint(const uint8_t* rgb, const uint8_t* occ, int W, int H, int T, cons
   free(w);
   return 0;
 }
+
+/* ------------------------------------------------------------------------------------------
+ * App. B: W, V i.i.d. N(mu, sigma^2)^N, Z = mu.  With X = (W-mu)/sigma,
+ * Y = (V-mu)/sigma:  ||W-V||^2 < ||W-Z||^2  <=>  ||Y||^2 < 2 <X,Y>, and <X,Y> | Y ~ N(0, ||Y||^2),
+ * so P_N = E[Q(||Y|| / 2)], ||Y||^2 ~ chi2_N.  Integral over s = ||Y|| by composite Simpson on
+ * [0, sqrt(N) + 40] (the chi density of s is negligible beyond), in log space.
+ * ---------------------------------------------------------------------------------------- */
+double or_ambiguity_exact(int N) {
+  const int n = 400000;
+  double smax = sqrt((double)N) + 40.0, h = smax / n, acc = 0.0;
+  /* chi density of s = ||Y||: s^(N-1) e^(-s^2/2) / (2^(N/2-1) Gamma(N/2)) */
+  double lc = -(N / 2.0 - 1.0) * log(2.0) - lgamma(N / 2.0);
+  for (int i = 0; i <= n; ++i) {
+    double s = i * h;
+    double f;
+    if (s > 0)
+      f = exp(lc + (N - 1) * log(s) - s * s / 2.0);
+    else
+      f = N == 1 ? exp(lc) : 0.0;
+    f *= 0.5 * erfc(s / 2.0 / sqrt(2.0)); /* Q(s/2) */
+    double w = (i == 0 || i == n) ? 1.0 : ((i & 1) ? 4.0 : 2.0);
+    acc += w * f;
+  }
+  return acc * h / 3.0;
+}
+
+/* The paper's simulation (Table 2 caption): per trial draw W, V ~ N(0, sigma^2)^N, count
+ * sum (W-V)^2 < sum W^2.  Normals: Box-Muller on Philox words (u1 = (U0 + 0.5) 2^-32,
+ * u2 = U1 2^-32 -> two normals; U2, U3 -> two more), component pair k = components 4k..4k+3. */
+int64_t or_ambiguity_mc(int N, double sigma, uint64_t seed, uint64_t trial0, uint64_t n_trials) {
+  int64_t hits = 0;
+#pragma omp parallel for reduction(+ : hits) schedule(static, 4096)
+  for (int64_t tr = 0; tr < (int64_t)n_trials; ++tr) {
+    uint64_t t = trial0 + (uint64_t)tr;
+    double a = 0.0, b = 0.0, z[4];
+    /* 2N normals, 4 per Philox call; W_c uses normal 2c, V_c normal 2c + 1 */
+    int nn = 2 * N;
+    double w = 0.0;
+    for (int k = 0; k < (nn + 3) / 4; ++k) {
+      uint32_t ctr[4] = {(uint32_t)t, (uint32_t)(t >> 32), (4u << 16) | (uint32_t)k, 0u}, u[4];
+      or_philox4x32_10(ctr, seed, u);
+      double r1 = sqrt(-2.0 * log(((double)u[0] + 0.5) / 4294967296.0));
+      double r2 = sqrt(-2.0 * log(((double)u[2] + 0.5) / 4294967296.0));
+      double th1 = 2.0 * 3.14159265358979323846 * ((double)u[1] / 4294967296.0);
+      double th2 = 2.0 * 3.14159265358979323846 * ((double)u[3] / 4294967296.0);
+      z[0] = r1 * cos(th1); z[1] = r1 * sin(th1); z[2] = r2 * cos(th2); z[3] = r2 * sin(th2);
+      for (int j = 0; j < 4; ++j) {
+        int idx = 4 * k + j;
+        if (idx >= nn) break;
+        if ((idx & 1) == 0) {
+          w = sigma * z[j];          /* W_c - mu, c = idx / 2 */
+        } else {
+          double v = sigma * z[j];   /* V_c - mu */
+          a += (w - v) * (w - v);
+          b += w * w;
+        }
+      }
+    }
+    hits += (a < b);
+  }
+  return hits;
+}

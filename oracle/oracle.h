@@ -81,6 +81,14 @@ int64_t or_change_l1(const float* a, const float* b, int64_t n);
 double or_energy(const or_level* lv, const or_nnf* nnf);
 int64_t or_brute_force(const or_level* lv, or_nnf* out, int lambda, int32_t b, int32_t e);
 
+/* App. B, Table 2 (NEXT #3): probability that a random patch V is closer (SSD) to a
+ * random reference patch W than the constant patch Z = mu, components i.i.d. N(mu, sigma^2).
+ * Exact value P_N = E[Q(sqrt(chi2_N) / 2)] (1-D integral, independent of sigma), and the paper's
+ * direct simulation on the CPU (fp64 Box-Muller on this oracle's Philox; counter (trial lo,
+ * trial hi, 4 << 16 | component pair, 0)). */
+double or_ambiguity_exact(int N);
+int64_t or_ambiguity_mc(int N, double sigma, uint64_t seed, uint64_t trial0, uint64_t n_trials);
+
 /* Whole Alg. 4 (without alignment) on host buffers; returns 0 on success. */
 typedef struct {
   int levels, pm_iters, fixed_outer, max_outer, lambda, tex_half, n_steps, sign_policy;

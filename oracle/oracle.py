@@ -80,6 +80,8 @@ def lib():
             "or_energy": (D, [P, P]),
             "or_brute_force": (I64, [P, P, I, I32, I32]),
             "or_inpaint": (I, [P, P, I, I, I, P, P, P]),
+            "or_ambiguity_exact": (D, [I]),
+            "or_ambiguity_mc": (I64, [I, D, U64, U64, U64]),
         }
         for name, (res, args) in sig.items():
             f = getattr(_lib, name)
@@ -291,3 +293,12 @@ def inpaint(rgb, occ, levels, pm_iters=10, fixed_outer=0, max_outer=20, lam=50, 
         raise RuntimeError(f"or_inpaint failed: {rc}")
     return out, dict(outer_iters=list(st.outer_iters)[:levels],
                      patch_updates=list(st.patch_updates)[:levels], onion_layers=st.onion_layers)
+
+
+def ambiguity_exact(N):
+    """App. B: exact P(random patch beats the constant patch) for N i.i.d. Gaussian components."""
+    return lib().or_ambiguity_exact(N)
+
+
+def ambiguity_mc(N, n_trials, sigma=5.0, seed=1, trial0=0):
+    return lib().or_ambiguity_mc(N, sigma, seed, trial0, n_trials)

@@ -87,6 +87,9 @@ __global__ void k_upsample(LevelArgs c, const uint64_t* __restrict__ ce, LevelAr
 #ifndef VINP_PROP_MINB
 #define VINP_PROP_MINB 4
 #endif
+#ifndef VINP_FRAME_BATCH
+#define VINP_FRAME_BATCH 1
+#endif
 #ifndef VINP_GROUP
 #define VINP_GROUP 8
 #endif
@@ -99,6 +102,13 @@ __global__ void k_upsample(LevelArgs c, const uint64_t* __restrict__ ce, LevelAr
 // Exact partial-distance elimination after every frame of 25 voxels (SPEC: early abort that
 // changes no comparison): a lane drops its candidate once the partial sum reaches `thr`.
 // `full` = 1: every voxel of N_p is in Omega and K (interior target, K = Omega).
+#define VINP_ACC(T, S)                                                        \
+  {                                                                           \
+    uint32_t dc = __vabsdiffu4((uint32_t)(T), (uint32_t)(S));                 \
+    uint32_t dx_ = __vabsdiffu4((uint32_t)((T) >> 32), (uint32_t)((S) >> 32)); \
+    accc = __dp4a(dc, dc, accc);                                              \
+    acct = __dp4a(dx_, dx_, acct);                                            \
+  }
 template <bool ABORT>
 __device__ __forceinline__ uint32_t thread_ssd(const LevelArgs& a, int p, int px, int py, int pt,
                                                int q, int lambda, int kb, bool full, uint32_t thr,
@@ -107,22 +117,40 @@ __device__ __forceinline__ uint32_t thread_ssd(const LevelArgs& a, int p, int px
   uint32_t accc = 0, acct = 0;
 #pragma unroll 1
   for (int dt = -2; dt <= 2; ++dt) {
+#if VINP_FRAME_BATCH
+    if (full) {  // all 50 gathers of the frame in flight, then the arithmetic
+      uint64_t tv[25], sv[25];
+#pragma unroll
+      for (int dy = -2; dy <= 2; ++dy) {
+        int ro = dt * a.g.HW + dy * a.g.W;
+#pragma unroll
+        for (int dx = -2; dx <= 2; ++dx) {
+          tv[(dy + 2) * 5 + dx + 2] = __ldg(v + (p + ro + dx));
+          sv[(dy + 2) * 5 + dx + 2] = __ldg(v + (q + ro + dx));
+        }
+      }
+#pragma unroll
+      for (int k = 0; k < 25; ++k) {
+        uint32_t dc = __vabsdiffu4((uint32_t)tv[k], (uint32_t)sv[k]);
+        uint32_t dx_ = __vabsdiffu4((uint32_t)(tv[k] >> 32), (uint32_t)(sv[k] >> 32));
+        accc = __dp4a(dc, dc, accc);
+        acct = __dp4a(dx_, dx_, acct);
+      }
+    }
+#endif
 #pragma unroll
     for (int dy = -2; dy <= 2; ++dy) {
       int ro = dt * a.g.HW + dy * a.g.W;
       const unsigned long long* tr = v + (p + ro);
       const unsigned long long* sr = v + (q + ro);
       if (full) {
+#if VINP_FRAME_BATCH
+        continue;  // handled per frame below
+#else
         uint64_t t0 = __ldg(tr - 2), t1 = __ldg(tr - 1), t2 = __ldg(tr), t3 = __ldg(tr + 1), t4 = __ldg(tr + 2);
         uint64_t s0 = __ldg(sr - 2), s1 = __ldg(sr - 1), s2 = __ldg(sr), s3 = __ldg(sr + 1), s4 = __ldg(sr + 2);
-#define VINP_ACC(T, S)                                                        \
-  {                                                                           \
-    uint32_t dc = __vabsdiffu4((uint32_t)(T), (uint32_t)(S));                 \
-    uint32_t dx_ = __vabsdiffu4((uint32_t)((T) >> 32), (uint32_t)((S) >> 32)); \
-    accc = __dp4a(dc, dc, accc);                                              \
-    acct = __dp4a(dx_, dx_, acct);                                            \
-  }
         VINP_ACC(t0, s0) VINP_ACC(t1, s1) VINP_ACC(t2, s2) VINP_ACC(t3, s3) VINP_ACC(t4, s4)
+#endif
       } else {
 #pragma unroll
         for (int dx = -2; dx <= 2; ++dx) {
@@ -132,7 +160,6 @@ __device__ __forceinline__ uint32_t thread_ssd(const LevelArgs& a, int p, int px
           VINP_ACC(t, s)
         }
       }
-#undef VINP_ACC
     }
     if (ABORT) {
       uint32_t part = 4u * accc + (uint32_t)lambda * acct;
@@ -257,6 +284,9 @@ __global__ void __launch_bounds__(256, VINP_PROP_MINB) k_propagate(LevelArgs a, 
 #pragma unroll
   for (int c = 0; c < NCMAX; ++c) {
     bool mine = c < ncand;
+#ifdef VINP_DIAG_NOSSD
+    mine = false;  // diagnostic timing build only: candidate generation without evaluation
+#endif
     if (!__any_sync(kFull, mine)) break;
     if (mine) {
       bool alive = true;

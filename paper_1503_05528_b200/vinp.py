@@ -79,6 +79,7 @@ def _load():
         "vinp_patch_ssd": (I, [P, P, P, I64, P, I, P, P, P]),
         "vinp_philox": (I, [P, I64, U64, P, P]),
         "vinp_tc_gemm_u8": (I, [P, P, I, P, P]),
+        "vinp_patch_ambiguity": (I, [I, C.c_double, U64, U64, U64, P, P]),
     }
     for name, (res, args) in sigs.items():
         f = getattr(lib, name)
@@ -96,7 +97,7 @@ EXPORTED = [
     "vinp_onion_ws_bytes", "vinp_onion_peel",
     "vinp_reconstruct", "vinp_commit", "vinp_change_l1", "vinp_energy",
     "vinp_brute_force_ws_bytes", "vinp_brute_force", "vinp_patch_ssd", "vinp_philox",
-    "vinp_tc_gemm_u8", "vinp_brute_force_list", "vinp_brute_force_tc_ws_bytes", "vinp_brute_force_tc"]
+    "vinp_tc_gemm_u8", "vinp_patch_ambiguity", "vinp_brute_force_list", "vinp_brute_force_tc_ws_bytes", "vinp_brute_force_tc"]
 
 
 def _check(rc: int, what: str):
@@ -371,3 +372,12 @@ def tc_gemm_u8(A: torch.Tensor, B: torch.Tensor):
     C = torch.empty((128, 128), dtype=torch.int32, device=A.device)
     _check(_lib.vinp_tc_gemm_u8(_ptr(A), _ptr(B), K, _ptr(C), _stream()), "vinp_tc_gemm_u8")
     return C
+
+
+def patch_ambiguity(N: int, n_trials: int, sigma=5.0, seed=1, trial0=0, hits=None):
+    """App. B Monte-Carlo: returns the device int64 hit counter (accumulated)."""
+    if hits is None:
+        hits = torch.zeros(1, dtype=torch.int64, device="cuda")
+    _check(_lib.vinp_patch_ambiguity(N, sigma, seed, trial0, n_trials, _ptr(hits), _stream()),
+           "vinp_patch_ambiguity")
+    return hits

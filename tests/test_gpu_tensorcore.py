@@ -35,3 +35,21 @@ def test_brute_force_tc_equals_cuda_core(case, lam):
         V.brute_force_tc(lv, y, ip.prm, b, e)
         torch.cuda.synchronize()
         assert torch.equal(x.e[b:e], y.e[b:e]) and torch.equal(x.n[b:e], y.n[b:e]), (case, lam, b)
+
+
+@pytest.mark.parametrize("N,n", [(9, 1_000_000), (27, 400_000), (125, 100_000)])
+def test_ambiguity_gpu_counts_equal_oracle(orc, N, n):
+    """Same Philox counters and Box-Muller: the GPU hit count equals the oracle's simulation."""
+    from paper_1503_05528_b200 import vinp as V
+    for seed, t0 in ((1, 0), (7, 123456789)):
+        h = int(V.patch_ambiguity(N, n, 5.0, seed, t0).item())
+        assert h == orc.ambiguity_mc(N, n, sigma=5.0, seed=seed, trial0=t0)
+
+
+def test_ambiguity_gpu_statistics(orc):
+    import math
+    from paper_1503_05528_b200 import vinp as V
+    for N, n in ((25, 50_000_000), (49, 200_000_000)):
+        p = orc.ambiguity_exact(N)
+        h = int(V.patch_ambiguity(N, n, 5.0, 11).item())
+        assert abs(h / n - p) < 5 * math.sqrt(p * (1 - p) / n)

@@ -705,3 +705,34 @@ def test_upsample_spec_example(orc):
     orc.upsample(coarse, cn, fine, fn, 7, 1)
     assert all(fine.src[(p // (H * W) + fn.dt[s], (p // W) % H + fn.dy[s], p % W + fn.dx[s])]
                for s, p in enumerate(fine.targets))
+
+
+# ----------------------------------------------------------------------------- App. B (NEXT #3)
+def test_ambiguity_exact_closed_forms(orc):
+    """N = 1: P(Y^2 < 2XY) for independent standard normals = atan(2)/pi (planar angle); N = 2:
+    (1 - 1/sqrt 5)/2 (Rayleigh, by parts); N >= 9 vs scipy's quadrature of E[Q(sqrt(chi2_N)/2)]."""
+    import math
+    from scipy import integrate, stats
+    assert orc.ambiguity_exact(1) == pytest.approx(math.atan(2) / math.pi, rel=1e-9)
+    assert orc.ambiguity_exact(2) == pytest.approx((1 - 1 / math.sqrt(5)) / 2, rel=1e-9)  # by parts
+    for N in (9, 25, 27, 125):
+        f = lambda r: stats.norm.sf(np.sqrt(r) / 2) * stats.chi2.pdf(r, N)
+        ref, _ = integrate.quad(f, 0, np.inf, limit=500, epsabs=0, epsrel=1e-12)
+        assert orc.ambiguity_exact(N) == pytest.approx(ref, rel=1e-7)
+
+
+def test_ambiguity_paper_table2(orc):
+    """Table 2: 3x3 -> 8e-2, 5x5 -> 1e-2 (the paper's simulation; our exact values agree
+    within 5%).  The rarer entries are reported, not pinned."""
+    assert orc.ambiguity_exact(9) == pytest.approx(8e-2, rel=0.06)
+    assert orc.ambiguity_exact(25) == pytest.approx(1e-2, rel=0.05)
+    vals = [orc.ambiguity_exact(N) for N in (9, 25, 27, 49, 81, 121, 125)]
+    assert all(a > b for a, b in zip(vals, vals[1:]))  # strictly decreasing (SPEC acceptance 1)
+
+
+def test_ambiguity_simulation_matches_exact(orc):
+    for N in (9, 25):
+        n = 1_000_000
+        p = orc.ambiguity_exact(N)
+        h = orc.ambiguity_mc(N, n, sigma=5.0, seed=3)
+        assert abs(h / n - p) < 5 * (p * (1 - p) / n) ** 0.5
