@@ -854,3 +854,67 @@ int64_t or_ambiguity_mc(int N, double sigma, uint64_t seed, uint64_t trial0, uin
   }
   return hits;
 }
+
+/* ------------------------------------------------------------------------------------------
+ * NEXT #2: the paper's sequential ANN search, Alg. 1 P:411-443 as printed (with R1, R2, R3, R7).
+ * ---------------------------------------------------------------------------------------- */
+static int64_t seq_try(const or_level* lv, or_nnf* f, int32_t s, int32_t p, int px, int py, int pt,
+                       int vx, int vy, int vt, int lambda, int (*seen)[3], int* nseen) {
+  if (!valid_source(lv, px, py, pt, vx, vy, vt)) return 0;
+  for (int k = 0; k < *nseen; ++k)
+    if (seen[k][0] == vx && seen[k][1] == vy && seen[k][2] == vt) return 0;
+  seen[*nseen][0] = vx; seen[*nseen][1] = vy; seen[*nseen][2] = vt; ++*nseen;
+  uint32_t D, n;
+  or_patch_ssd(lv, p, (int32_t)lin(lv, px + vx, py + vy, pt + vt), lambda, -1, &D, &n);
+  if (D < f->D[s]) {
+    f->dx[s] = vx; f->dy[s] = vy; f->dt[s] = vt; f->D[s] = D;
+  }
+  return 1;
+}
+
+int64_t or_ann_search_sequential(const or_level* lv, or_nnf* f, int lambda, uint64_t seed,
+                                 double rho, int rmax, int level, uint32_t outer_code, int K) {
+  int32_t nt = lv->n_targets;
+  int64_t cnt = or_nnf_evaluate(lv, f, lambda, -1, -1, 0, nt);
+  for (int k = 1; k <= K; ++k) {
+    int fwd = (k % 2 == 0);          /* Alg. 1: k even -> forward scan, p - e_*; odd -> reverse, p + e_* */
+    int sg = fwd ? -1 : 1;
+    for (int32_t i = 0; i < nt; ++i) {
+      int32_t s = fwd ? i : nt - 1 - i;
+      int32_t p = lv->targets[s];
+      int px, py, pt;
+      coords(lv, p, &px, &py, &pt);
+      int seen[4][3], nseen = 0;
+      seen[0][0] = f->dx[s]; seen[0][1] = f->dy[s]; seen[0][2] = f->dt[s]; nseen = 1;
+      for (int a = 0; a < 3; ++a) {
+        int rx = px + (a == 0 ? sg : 0), ry = py + (a == 1 ? sg : 0), rt = pt + (a == 2 ? sg : 0);
+        if (!inside(lv, rx, ry, rt)) continue;
+        int32_t rs = lv->slot[lin(lv, rx, ry, rt)];
+        if (rs < 0) continue;
+        /* the neighbour's CURRENT shift: already updated in this scan if it precedes p */
+        cnt += seq_try(lv, f, s, p, px, py, pt, f->dx[rs], f->dy[rs], f->dt[rs], lambda, seen, &nseen);
+      }
+    }
+    for (int32_t s = 0; s < nt; ++s) {  /* random search, lexicographic order (Alg. 1) */
+      int32_t p = lv->targets[s];
+      int px, py, pt;
+      coords(lv, p, &px, &py, &pt);
+      int v0x = f->dx[s], v0y = f->dy[s], v0t = f->dt[s];
+      int seen[64][3], nseen = 1;
+      seen[0][0] = v0x; seen[0][1] = v0y; seen[0][2] = v0t;
+      double R = (double)rmax;
+      for (int i = 1; i < 64; ++i) {
+        R = R * rho;
+        if (!(R >= 1.0)) break;
+        uint32_t u[4];
+        draw((uint32_t)p, (uint32_t)k, level, ST_RS, i, outer_code, seed, u);
+        int off[3];
+        for (int c = 0; c < 3; ++c)
+          off[c] = (int)floor(R * (((double)u[c] - 2147483648.0) * (1.0 / 2147483648.0)));
+        cnt += seq_try(lv, f, s, p, px, py, pt, v0x + off[0], v0y + off[1], v0t + off[2], lambda, seen,
+                       &nseen);
+      }
+    }
+  }
+  return cnt;
+}

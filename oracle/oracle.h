@@ -89,6 +89,15 @@ int64_t or_brute_force(const or_level* lv, or_nnf* out, int lambda, int32_t b, i
 double or_ambiguity_exact(int N);
 int64_t or_ambiguity_mc(int N, double sigma, uint64_t seed, uint64_t trial0, uint64_t n_trials);
 
+/* NEXT #2: Alg. 1 as printed — in-place lexicographic scans: even k forward with
+ * the -1 neighbours, odd k reverse with the +1 neighbours (reusing entries already
+ * updated in the same scan), then an in-place random search over the targets in lexicographic
+ * order (Eq. 3 with the R3 inner loop, centred on the current phi(p)).  Same validity,
+ * de-duplication and strict-improvement rules as the Jacobi passes.  Starts with an evaluate.
+ * Single-threaded by definition.  Returns the number of evaluated candidates. */
+int64_t or_ann_search_sequential(const or_level* lv, or_nnf* nnf, int lambda, uint64_t seed,
+                                 double rho, int rmax, int level, uint32_t outer_code, int K);
+
 /* Whole Alg. 4 (without alignment) on host buffers; returns 0 on success. */
 typedef struct {
   int levels, pm_iters, fixed_outer, max_outer, lambda, tex_half, n_steps, sign_policy;

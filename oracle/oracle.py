@@ -81,6 +81,7 @@ def lib():
             "or_brute_force": (I64, [P, P, I, I32, I32]),
             "or_inpaint": (I, [P, P, I, I, I, P, P, P]),
             "or_ambiguity_exact": (D, [I]),
+            "or_ann_search_sequential": (I64, [P, P, I, U64, D, I, I, C.c_uint32, I]),
             "or_ambiguity_mc": (I64, [I, D, U64, U64, U64]),
         }
         for name, (res, args) in sig.items():
@@ -302,3 +303,10 @@ def ambiguity_exact(N):
 
 def ambiguity_mc(N, n_trials, sigma=5.0, seed=1, trial0=0):
     return lib().or_ambiguity_mc(N, sigma, seed, trial0, n_trials)
+
+
+def ann_search_sequential(lv, nnf, lam, seed, level, outer_code, K, rho=0.5, rmax=None):
+    """NEXT #2: Alg. 1 as printed (in-place lexicographic scans); modifies ``nnf``."""
+    rmax = lv.rmax if rmax is None else rmax
+    return lib().or_ann_search_sequential(lv.struct(), nnf.struct(), lam, seed, rho, rmax, level,
+                                          outer_code, K)

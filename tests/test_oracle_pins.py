@@ -736,3 +736,43 @@ def test_ambiguity_simulation_matches_exact(orc):
         p = orc.ambiguity_exact(N)
         h = orc.ambiguity_mc(N, n, sigma=5.0, seed=3)
         assert abs(h / n - p) < 5 * (p * (1 - p) / n) ** 0.5
+
+
+# ----------------------------------------------------------------------------- NEXT #2 sequential scan
+def test_sequential_scan_invariants_and_reuse(orc):
+    lv = _c1_level(orc)
+    a = orc.NNF.empty(len(lv.targets))
+    orc.init_random(lv, a, 5, 1, 0)
+    b = a.copy()
+    orc.evaluate(lv, b, 50)
+    d0 = b.D.copy()
+    cnt = orc.ann_search_sequential(lv, b, 50, 5, 1, 0, 4)
+    assert cnt > 0 and (b.D <= d0).all()
+    _check_nnf(orc, lv, b, 50)
+    bf = orc.NNF.empty(len(lv.targets))
+    orc.brute_force(lv, bf, 50)
+    assert (b.D >= bf.D).all()
+    assert (b.D / (4.0 * b.n)).mean() <= 1.5 * (bf.D / (4.0 * bf.n)).mean()
+
+
+def test_sequential_scan_propagates_along_a_row_in_one_pass(orc):
+    """in-place scans reuse entries already updated, so one forward scan carries a good
+    shift along a whole row of targets; a single Jacobi pass moves it by one step only."""
+    lv = _copy_world(orc)
+    nt = len(lv.targets)
+    f = orc.NNF.empty(nt)
+    f.dx[:], f.dy[:], f.dt[:] = 1, 1, 0
+    H, W = lv.H, lv.W
+    row = [s for s, p in enumerate(lv.targets) if p // (H * W) == 4 and (p // W) % H == 6]
+    xs = [lv.targets[s] % W for s in row]
+    first = row[int(np.argmin(xs))]
+    f.dx[first], f.dy[first], f.dt[first] = 20, 0, 0  # perfect shift at the row's left end
+    g = f.copy()
+    # K = 0 evaluates only; K = 2 runs one reverse (+1) and one forward (-1) scan before RS
+    orc.ann_search_sequential(lv, g, 0, 3, 1, 0, 2, rmax=1)
+    assert all(g.D[s] == 0 for s in row)
+    j = f.copy()
+    orc.evaluate(lv, j, 0)
+    k2 = j.copy()
+    orc.propagate(lv, j, k2, 0, 1, -1)
+    assert sum(k2.D[s] == 0 for s in row) == 2  # the first target and its right neighbour only
