@@ -7,9 +7,9 @@ is no CPU fallback).
 """
 import importlib
 
-_EXPORTS = {"vinp": (".vinp", None), "Config": (".inpaint", "Config"),
-            "Exchange": (".inpaint", "Exchange"), "Inpainter": (".inpaint", "Inpainter"),
-            "inpaint": (".inpaint", "inpaint")}
+_EXPORTS = {"vinp": (".vinp", None), "Config": (".driver", "Config"),
+            "Exchange": (".driver", "Exchange"), "Inpainter": (".driver", "Inpainter"),
+            "inpaint": (".driver", "inpaint")}
 
 
 def __getattr__(name):

@@ -138,16 +138,24 @@ class Inpainter:
                 raise V.VinpError(f"D~ is empty at level {lv.level} (S:237)")
             lv.alloc_lists()
         self.V.build_lists(self.levels, self.ws)
+        old = {id(st.lv): st for st in self.states}
         self.states = []
         for lv in self.levels:
             npad = self.ex.padded(lv.n_targets)
             hpad = self.ex.padded(lv.n_holes)
-            a = V.NNF.alloc(npad, self.device)
-            b = V.NNF.alloc(npad, self.device, n=a.n)
-            z = lambda k: torch.zeros((hpad, k), dtype=torch.float32, device=self.device)
+            st = old.get(id(lv))
+            if st is not None and st.a.e.numel() == npad and st.cur_rgb.shape[0] == hpad:
+                self.states.append(st)  # same sizes: reuse the buffers (repeated calls)
+                continue
+            # every NNF entry / hole value is written (init, upsample, evaluate, reconstruct)
+            # before it is read, so no zero fill is needed
+            a = V.NNF.alloc(npad, self.device, zero=False)
+            b = V.NNF.alloc(npad, self.device, n=a.n, zero=False)
+            z = lambda k: torch.empty((hpad, k), dtype=torch.float32, device=self.device)
             self.states.append(LevelState(lv, a, b, z(3), z(2), z(3), z(2)))
         top = self.levels[-1]
-        top.layer = torch.empty(top.N, dtype=torch.uint8, device=self.device)
+        if top.layer is None:
+            top.layer = torch.empty(top.N, dtype=torch.uint8, device=self.device)
         self.n_layers = self.V.layers(top, self.ws)
         self.stats.onion_layers = self.n_layers
         return counts
@@ -284,10 +292,18 @@ class Inpainter:
         return torch.where(m[..., None], vb, rgb_in)
 
 
+_PLANS = {}
+
+
 def inpaint(rgb: torch.Tensor, mask: torch.Tensor, cfg: Config, device="cuda", exchange=None, ops=None):
-    """Convenience: whole Alg. 4 on one video.  rgb/mask may live on the host (copied in)."""
+    """Convenience: whole Alg. 4 on one video.  rgb/mask may live on the host (copied in; pinned
+    host memory makes the copy asynchronous).  The device buffers of an Inpainter are cached per
+    (shape, config, device, exchange), so repeated calls on same-shaped videos allocate nothing."""
     T, H, W, _ = rgb.shape
-    ip = Inpainter(W, H, T, cfg, device, exchange, ops)
+    key = (W, H, T, repr(cfg), str(torch.device(device)), id(exchange), id(ops))
+    ip = _PLANS.get(key)
+    if ip is None:
+        ip = _PLANS[key] = Inpainter(W, H, T, cfg, device, exchange, ops)
     rgb_d = rgb.to(device, non_blocking=True)
     mask_d = mask.to(device, non_blocking=True)
     ip.load(rgb_d, mask_d)

@@ -154,8 +154,9 @@ class Level:
     def alloc(cls, W, H, T, level, device):
         lv = cls(W, H, T, level, torch.device(device))
         N = W * H * T
-        lv.vox = torch.zeros(N, dtype=torch.int64, device=device)
-        lv.flags = torch.zeros(N, dtype=torch.uint8, device=device)
+        # every element is written by vinp_build_pyramid / vinp_texture_features before any read
+        lv.vox = torch.empty(N, dtype=torch.int64, device=device)
+        lv.flags = torch.empty(N, dtype=torch.uint8, device=device)
         return lv
 
     @property
@@ -174,11 +175,15 @@ class Level:
         return C.byref(s)
 
     def alloc_lists(self):
+        """(Re)allocate the list buffers only when a size changes (repeated calls reuse them)."""
         d = self.device
-        self.targets = torch.empty(max(self.n_targets, 1), dtype=torch.int32, device=d)
-        self.holes = torch.empty(max(self.n_holes, 1), dtype=torch.int32, device=d)
-        self.sources = torch.empty(max(self.n_sources, 1), dtype=torch.int32, device=d)
-        self.slot = torch.empty(self.N, dtype=torch.int32, device=d)
+
+        def fit(t, n):
+            return t if (t is not None and t.numel() == max(n, 1)) else torch.empty(max(n, 1), dtype=torch.int32, device=d)
+        self.targets = fit(self.targets, self.n_targets)
+        self.holes = fit(self.holes, self.n_holes)
+        self.sources = fit(self.sources, self.n_sources)
+        self.slot = fit(self.slot, self.N)
 
 
 @dataclass
@@ -188,10 +193,11 @@ class NNF:
     _s: object = field(default=None, repr=False)
 
     @classmethod
-    def alloc(cls, n_slots, device, n=None):
-        e = torch.zeros(max(n_slots, 1), dtype=torch.int64, device=device)
+    def alloc(cls, n_slots, device, n=None, zero=True):
+        mk = torch.zeros if zero else torch.empty
+        e = mk(max(n_slots, 1), dtype=torch.int64, device=device)
         if n is None:
-            n = torch.zeros(max(n_slots, 1), dtype=torch.uint8, device=device)
+            n = mk(max(n_slots, 1), dtype=torch.uint8, device=device)
         return cls(e, n)
 
     def struct(self):

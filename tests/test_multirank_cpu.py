@@ -61,7 +61,7 @@ def test_two_ranks_bit_identical_to_one_and_to_oracle(tmp_path, orc):
 
 
 def test_exchange_slabs_cover_and_pad():
-    from paper_1503_05528_b200.inpaint import Exchange
+    from paper_1503_05528_b200.driver import Exchange
     ex = Exchange()
     ex.world = 3
     spans = []
