@@ -8,6 +8,8 @@
 // exactly in the epilogue with E(q), running (D, index) minimum per target row (ties -> smallest
 // index, as the oracle's exhaustive scan).  tcgen05.mma.cta_group::1.kind::i8, M = 128 targets,
 // N = 128 sources per MMA, operands staged K-major (no swizzle) in shared memory.
+#include <vector>
+
 #include "common.cuh"
 #include "tc.cuh"
 
@@ -75,38 +77,52 @@ __device__ __forceinline__ bool full_patch(const Geo& g, int x, int y, int t) {
   return x >= 2 && x < g.W - 2 && y >= 2 && y < g.H - 2 && t >= 2 && t < g.T - 2;
 }
 
-// im2col row of the patch around voxel p (must be a full patch) + its energy E = 4 sum c^2 + lambda sum t^2
-__global__ void k_im2col(const uint64_t* __restrict__ vox, Geo g, const int32_t* __restrict__ pos,
-                         const int32_t* __restrict__ idx, int32_t n, int32_t npad, int lambda,
-                         uint8_t* __restrict__ rows, int64_t* __restrict__ energy) {
+// im2col of the patch around voxel p (a full patch) in the TILED core-matrix layout of tc.cuh: rows are
+// grouped in tiles of TR rows; a tile is [colour: 24 K-chunks x TR/8 core matrices][texture: 16 x
+// TR/8], K byte k of row r at  part + (k/16)*TR*16 + (r/8)*128 + (r%8)*16 + k%16, so that a whole tile
+// is one contiguous block that a bulk (TMA) copy lands in shared memory ready for tcgen05.mma.
+// energy[i] = 4 sum c^2 + lambda sum t^2 (padded rows: zeros, energy kEPad).
+__device__ __forceinline__ size_t tiled_off(int i, int k, int TR) {
+  int tile = i / TR, r = i % TR;
+  size_t base = (size_t)tile * TR * kRow;
+  if (k >= kColK) {
+    base += (size_t)TR * kColK;
+    k -= kColK;
+  }
+  return base + (size_t)(k >> 4) * TR * 16 + (r >> 3) * 128 + (r & 7) * 16 + (k & 15);
+}
+
+__global__ void k_im2col_tiled(const uint64_t* __restrict__ vox, Geo g, const int32_t* __restrict__ pos,
+                               const int32_t* __restrict__ idx, int32_t n, int32_t npad, int lambda, int TR,
+                               uint8_t* __restrict__ rows, int64_t* __restrict__ energy) {
   int i = blockIdx.x;  // one block (128 threads) per row
   if (i >= npad) return;
-  uint8_t* row = rows + (size_t)i * kRow;
   if (i >= n) {
-    for (int k = threadIdx.x; k < kRow; k += blockDim.x) row[k] = 0;
+    for (int k = threadIdx.x; k < kRow; k += blockDim.x) rows[tiled_off(i, k, TR)] = 0;
     if (threadIdx.x == 0) energy[i] = kEPad;
     return;
   }
   int p = pos[idx ? idx[i] : i];
+  int px, py, pt;
+  decode(g, p, px, py, pt);
   uint32_t ec = 0, et = 0;
-  for (int v = threadIdx.x; v < 128; v += blockDim.x) {
-    uint64_t w = 0;
-    if (v < kPatch) {
-      int dx, dy, dt;
-      voff(v, dx, dy, dt);
-      w = vox[p + dt * g.HW + dy * g.W + dx];
-      uint32_t r = w & 255, gg = (w >> 8) & 255, b = (w >> 16) & 255, tx = (w >> 32) & 255, ty = (w >> 40) & 255;
-      row[3 * v] = (uint8_t)r;
-      row[3 * v + 1] = (uint8_t)gg;
-      row[3 * v + 2] = (uint8_t)b;
-      row[kColK + 2 * v] = (uint8_t)tx;
-      row[kColK + 2 * v + 1] = (uint8_t)ty;
-      ec += r * r + gg * gg + b * b;
-      et += tx * tx + ty * ty;
-    }
+  int v = threadIdx.x;
+  if (v < kPatch) {
+    int dx, dy, dt;
+    voff(v, dx, dy, dt);
+    // voxels of a clipped (border) patch outside Omega are zero rows of the contraction
+    uint64_t w = inside(g, px + dx, py + dy, pt + dt) ? vox[p + dt * g.HW + dy * g.W + dx] : 0ull;
+    uint32_t c0 = w & 255, c1 = (w >> 8) & 255, c2 = (w >> 16) & 255, t0 = (w >> 32) & 255, t1 = (w >> 40) & 255;
+    rows[tiled_off(i, 3 * v, TR)] = (uint8_t)c0;
+    rows[tiled_off(i, 3 * v + 1, TR)] = (uint8_t)c1;
+    rows[tiled_off(i, 3 * v + 2, TR)] = (uint8_t)c2;
+    rows[tiled_off(i, kColK + 2 * v, TR)] = (uint8_t)t0;
+    rows[tiled_off(i, kColK + 2 * v + 1, TR)] = (uint8_t)t1;
+    ec = c0 * c0 + c1 * c1 + c2 * c2;
+    et = t0 * t0 + t1 * t1;
   }
-  for (int k = 375 + threadIdx.x; k < kColK; k += blockDim.x) row[k] = 0;
-  for (int k = kColK + 250 + threadIdx.x; k < kRow; k += blockDim.x) row[k] = 0;
+  for (int k = 375 + threadIdx.x; k < kColK; k += blockDim.x) rows[tiled_off(i, k, TR)] = 0;
+  for (int k = kColK + 250 + threadIdx.x; k < kRow; k += blockDim.x) rows[tiled_off(i, k, TR)] = 0;
   ec = __reduce_add_sync(kFull, ec);
   et = __reduce_add_sync(kFull, et);
   __shared__ uint32_t sc[4], st[4];
@@ -119,162 +135,179 @@ __global__ void k_im2col(const uint64_t* __restrict__ vox, Geo g, const int32_t*
   }
 }
 
-// stage a [128][640] row block into shared memory in the core-matrix layout of tc.cuh, separately
-// for the colour (K = 384) and texture (K = 256) parts
-__device__ __forceinline__ void stage_rows(uint8_t* sc, uint8_t* st, const uint8_t* __restrict__ g) {
-  for (int c = threadIdx.x; c < kTile * (kRow / 16); c += blockDim.x) {
-    int m = c / (kRow / 16), kc = c % (kRow / 16);
-    const uint8_t* src = g + (size_t)m * kRow + kc * 16;
-    if (kc < kColK / 16)
-      tc::cp16(sc + (m >> 3) * 128 + kc * (kTile * 16) + (m & 7) * 16, src);
-    else
-      tc::cp16(st + (m >> 3) * 128 + (kc - kColK / 16) * (kTile * 16) + (m & 7) * 16, src);
-  }
-}
+// Warp-specialised exact-NN GEMM.  CTA = (m tile of 128 targets, chunk of source tiles of 64).
+// warp 0: producer — bulk (TMA) copies of the A tile (once) and of B tiles into a 2-stage ring;
+// warp 1: MMA issuer — 12 colour + 8 texture tcgen05.mma kind::i8 (M=128, N=64, K=32) per B tile
+//         into a 2-stage TMEM accumulator ring (stage s: colour cols s*128+[0,64), texture +64);
+// warps 2-5: epilogue — tcgen05.ld of their 32 TMEM lanes, D = E(q) - 2(4 X_c + lambda X_t), running
+//         (D, index) minimum per target row (strict <, ascending sources: first minimum).
+// Barriers: a_full; b_full[2] / b_empty[2] (producer <-> MMA); acc_full[2] / acc_empty[2] (MMA <->
+// epilogue, 128 arrivals).  All waits are bounded (trap instead of hang).
+constexpr int kTA = 128, kTB = 64;
+constexpr uint32_t kABytes = kTA * kRow, kBBytes = kTB * kRow;
 
-// grid (m tiles, n splits); 128 threads; out[split][row] = (D_partial << 32 | source index) min
-__global__ void __launch_bounds__(128, 1) k_bf_tc(const uint8_t* __restrict__ A, const int64_t* __restrict__ Ep,
-                                                  const uint8_t* __restrict__ B, const int64_t* __restrict__ Eq,
-                                                  int n_tiles, int tiles_per_split, int lambda,
-                                                  int32_t mpad, uint64_t* __restrict__ out) {
+__global__ void __launch_bounds__(192, 1) k_bf_tc2(const uint8_t* __restrict__ A, const int64_t* __restrict__ Ep,
+                                                   const uint8_t* __restrict__ B, const int64_t* __restrict__ Eq,
+                                                   int nb_tiles, int tiles_per_chunk, int lambda, int32_t mpad,
+                                                   uint64_t* __restrict__ out) {
   extern __shared__ __align__(1024) uint8_t sm[];
-  uint8_t* sAc = sm;
-  uint8_t* sAt = sAc + kTile * kColK;
-  uint8_t* sBc = sAt + kTile * kTexK;
-  uint8_t* sBt = sBc + kTile * kColK;
-  int64_t* sE = reinterpret_cast<int64_t*>(sBt + kTile * kTexK);
-  __shared__ uint64_t mbar;
+  uint8_t* sA = sm;
+  uint8_t* sB0 = sm + kABytes;
+  __shared__ uint64_t bar[9];  // 0 a_full, 1-2 b_full, 3-4 b_empty, 5-6 acc_full, 7-8 acc_empty
   __shared__ uint32_t tmem_base;
   int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
   int mt = blockIdx.x;
-  int t0 = blockIdx.y * tiles_per_split, t1 = min(n_tiles, t0 + tiles_per_split);
-  stage_rows(sAc, sAt, A + (size_t)mt * kTile * kRow);
-  if (warp == 0) tc::tmem_alloc(&tmem_base, 256);
-  if (tid == 0) tc::mbar_init(&mbar, 1);
+  int t0 = blockIdx.y * tiles_per_chunk, t1 = min(nb_tiles, t0 + tiles_per_chunk);
+  int nt = max(0, t1 - t0);
+  if (tid == 0) {
+    tc::mbar_init(&bar[0], 1);
+    for (int k = 1; k <= 6; ++k) tc::mbar_init(&bar[k], 1);
+    tc::mbar_init(&bar[7], 128);
+    tc::mbar_init(&bar[8], 128);
+    tc::fence_mbar_init();
+  }
+  if (warp == 1) tc::tmem_alloc(&tmem_base, 256);
   tc::fence_before();
   __syncthreads();
   tc::fence_after();
   const uint32_t tm = tmem_base;
-  const uint32_t id = tc::idesc_u8(kTile, kTile);
-  const uint32_t lane_off = (uint32_t)(32 * warp) << 16;
-  int64_t best = INT64_MAX;  // (partial D << 32 | index) packed later
-  int64_t bestD = INT64_MAX;
-  int bestI = 0x7fffffff;
-  uint32_t phase = 0;
-  for (int nt = t0; nt < t1; ++nt) {
-    stage_rows(sBc, sBt, B + (size_t)nt * kTile * kRow);
-    sE[tid] = Eq[(size_t)nt * kTile + tid];
-    tc::cp_wait_all();
-    tc::fence_proxy_async();
-    __syncthreads();
-    if (tid == 0) {
-      tc::fence_after();
-      uint32_t ac = tc::smem_u32(sAc), at = tc::smem_u32(sAt), bc = tc::smem_u32(sBc), bt = tc::smem_u32(sBt);
-#pragma unroll
-      for (int j = 0; j < kColK / 32; ++j)
-        tc::mma_u8(tm, tc::desc_kmajor(ac + 2 * j * 2048, 2048, 128), tc::desc_kmajor(bc + 2 * j * 2048, 2048, 128),
-                   id, j > 0);
-#pragma unroll
-      for (int j = 0; j < kTexK / 32; ++j)
-        tc::mma_u8(tm + kTile, tc::desc_kmajor(at + 2 * j * 2048, 2048, 128),
-                   tc::desc_kmajor(bt + 2 * j * 2048, 2048, 128), id, j > 0);
-      tc::commit(&mbar);
-    }
-    tc::mbar_wait(&mbar, phase);
-    phase ^= 1;
-    tc::fence_after();
-#pragma unroll 1
-    for (int c = 0; c < kTile / 32; ++c) {
-      uint32_t vc[32], vt[32];
-      tc::tmem_ld32(tm + lane_off + 32 * c, vc);
-      tc::tmem_ld32(tm + lane_off + kTile + 32 * c, vt);
-#pragma unroll
-      for (int j = 0; j < 32; ++j) {
-        int col = 32 * c + j;
-        int64_t d = sE[col] - 2 * (4 * (int64_t)vc[j] + (int64_t)lambda * (int64_t)vt[j]);
-        if (d < bestD) {
-          bestD = d;
-          bestI = nt * kTile + col;
-        }
+  if (warp == 0) {
+    if (lane == 0) {
+      const uint8_t* ga = A + (size_t)mt * kABytes;
+      tc::mbar_expect_tx(&bar[0], kABytes);
+      for (uint32_t o = 0; o < kABytes; o += 16384) tc::bulk_g2s(sA + o, ga + o, min(16384u, kABytes - o), &bar[0]);
+      for (int i = 0; i < nt; ++i) {
+        int st = i & 1;
+        uint32_t ph = (i >> 1) & 1;
+        tc::mbar_wait(&bar[3 + st], ph ^ 1);
+        uint8_t* sb = sB0 + st * kBBytes;
+        const uint8_t* gb = B + (size_t)(t0 + i) * kBBytes;
+        tc::mbar_expect_tx(&bar[1 + st], kBBytes);
+        for (uint32_t o = 0; o < kBBytes; o += 16384) tc::bulk_g2s(sb + o, gb + o, min(16384u, kBBytes - o), &bar[1 + st]);
       }
     }
-    tc::fence_before();
-    __syncthreads();  // TMEM and sB are reused by the next tile
+  } else if (warp == 1) {
+    if (lane == 0) {
+      const uint32_t id = tc::idesc_u8(kTA, kTB);
+      const uint32_t ac = tc::smem_u32(sA), at = ac + kTA * kColK;
+      tc::mbar_wait(&bar[0], 0);
+      for (int i = 0; i < nt; ++i) {
+        int st = i & 1;
+        uint32_t ph = (i >> 1) & 1;
+        tc::mbar_wait(&bar[1 + st], ph);
+        tc::mbar_wait(&bar[7 + st], ph ^ 1);
+        tc::fence_after();
+        uint32_t bc = tc::smem_u32(sB0 + st * kBBytes), bt = bc + kTB * kColK;
+        uint32_t dc = tm + st * 128, dt = dc + 64;
+#pragma unroll
+        for (int j = 0; j < kColK / 32; ++j)
+          tc::mma_u8(dc, tc::desc_kmajor(ac + 2 * j * (kTA * 16), kTA * 16, 128),
+                     tc::desc_kmajor(bc + 2 * j * (kTB * 16), kTB * 16, 128), id, j > 0);
+#pragma unroll
+        for (int j = 0; j < kTexK / 32; ++j)
+          tc::mma_u8(dt, tc::desc_kmajor(at + 2 * j * (kTA * 16), kTA * 16, 128),
+                     tc::desc_kmajor(bt + 2 * j * (kTB * 16), kTB * 16, 128), id, j > 0);
+        tc::commit(&bar[3 + st]);  // B stage free once these MMAs have read it
+        tc::commit(&bar[5 + st]);  // accumulator stage ready
+      }
+    }
+  } else {
+    const int q = warp & 3;  // TMEM lane quarter accessible to this warp
+    const int row = 32 * q + lane;
+    int64_t bestD = INT64_MAX;
+    int bestI = 0x7fffffff;
+    for (int i = 0; i < nt; ++i) {
+      int st = i & 1;
+      uint32_t ph = (i >> 1) & 1;
+      tc::mbar_wait(&bar[5 + st], ph);
+      tc::fence_after();
+      uint32_t c0[32], c1[32], x0[32], x1[32];
+      uint32_t base = tm + ((uint32_t)(32 * q) << 16) + st * 128;
+      tc::tmem_ld32(base + 0, c0);
+      tc::tmem_ld32(base + 32, c1);
+      tc::tmem_ld32(base + 64, x0);
+      tc::tmem_ld32(base + 96, x1);
+      tc::fence_before();
+      tc::mbar_arrive(&bar[7 + st]);  // accumulator stage drained
+      const int64_t* E = Eq + (size_t)(t0 + i) * kTB;
+      int cbase = (t0 + i) * kTB;
+#pragma unroll
+      for (int j = 0; j < 32; ++j) {
+        int64_t d = __ldg(E + j) - 2 * (4 * (int64_t)c0[j] + (int64_t)lambda * (int64_t)x0[j]);
+        if (d < bestD) { bestD = d; bestI = cbase + j; }
+      }
+#pragma unroll
+      for (int j = 0; j < 32; ++j) {
+        int64_t d = __ldg(E + 32 + j) - 2 * (4 * (int64_t)c1[j] + (int64_t)lambda * (int64_t)x1[j]);
+        if (d < bestD) { bestD = d; bestI = cbase + 32 + j; }
+      }
+    }
+    int64_t D = bestD + Ep[(size_t)mt * kTA + row];
+    uint64_t packed = bestI == 0x7fffffff ? ~0ull : (((uint64_t)(uint32_t)D << 32) | (uint32_t)bestI);
+    out[(size_t)blockIdx.y * mpad + (size_t)mt * kTA + row] = packed;
   }
-  (void)best;
-  tc::cp_wait_all();
-  int row = 32 * warp + lane;
-  int64_t D = bestD + Ep[(size_t)mt * kTile + row];
-  uint64_t packed = bestI == 0x7fffffff ? ~0ull : (((uint64_t)(uint32_t)D << 32) | (uint32_t)bestI);
-  out[(size_t)blockIdx.y * mpad + (size_t)mt * kTile + row] = packed;
+  tc::fence_before();
   __syncthreads();
-  if (warp == 0) tc::tmem_free(tm, 256);
+  if (warp == 1) tc::tmem_free(tm, 256);
 }
 
-// full targets of [b, e): flag, per-block count, scan, stable write (ascending slots)
-__global__ void k_full_flags(const int32_t* __restrict__ targets, Geo g, int32_t b, int32_t e,
-                             int32_t* __restrict__ bc) {
-  int i = b + blockIdx.x * 256 + threadIdx.x;
-  bool f = false;
-  if (i < e) {
-    int x, y, t;
-    decode(g, targets[i], x, y, t);
-    f = full_patch(g, x, y, t);
-  }
-  int c = __syncthreads_count(f);
-  if (threadIdx.x == 0) bc[blockIdx.x] = c;
+// Clip pattern of a target patch: how many voxel layers fall outside Omega on each side of each
+// axis (0..2 each); pid = xl + 3xh + 9yl + 27yh + 81tl + 243th, 0 = full patch.
+__device__ __forceinline__ int clip_pid(const Geo& g, int x, int y, int t) {
+  int xl = max(0, 2 - x), xh = max(0, x + 3 - g.W), yl = max(0, 2 - y), yh = max(0, y + 3 - g.H);
+  int tl = max(0, 2 - t), th = max(0, t + 3 - g.T);
+  return xl + 3 * xh + 9 * yl + 27 * yh + 81 * tl + 243 * th;
 }
-__global__ void k_full_scan(int32_t* bc, int nb, int32_t* total) {
-  if (threadIdx.x == 0 && blockIdx.x == 0) {
-    int32_t run = 0;
-    for (int k = 0; k < nb; ++k) {
-      int32_t v = bc[k];
-      bc[k] = run;
-      run += v;
-    }
-    *total = run;
-  }
+constexpr int kPids = 729;
+
+__global__ void k_pid_count(const int32_t* __restrict__ targets, Geo g, int32_t b, int32_t e,
+                            int32_t* __restrict__ cnt) {
+  int i = b + blockIdx.x * blockDim.x + threadIdx.x;
+  if (i >= e) return;
+  int x, y, t;
+  decode(g, targets[i], x, y, t);
+  atomicAdd(cnt + clip_pid(g, x, y, t), 1);
 }
-__global__ void k_full_write(const int32_t* __restrict__ targets, Geo g, int32_t b, int32_t e,
-                             const int32_t* __restrict__ bc, int32_t* __restrict__ list) {
-  int i = b + blockIdx.x * 256 + threadIdx.x;
-  bool f = false;
-  if (i < e) {
-    int x, y, t;
-    decode(g, targets[i], x, y, t);
-    f = full_patch(g, x, y, t);
-  }
-  __shared__ int32_t wc[8];
-  unsigned bal = __ballot_sync(kFull, f);
-  int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
-  if (lane == 0) wc[w] = __popc(bal);
-  __syncthreads();
-  int off = bc[blockIdx.x];
-  for (int k = 0; k < w; ++k) off += wc[k];
-  if (f) list[off + __popc(bal & ((1u << lane) - 1))] = i;
+// slots grouped by pattern (order within a group is irrelevant: targets are independent)
+__global__ void k_pid_scatter(const int32_t* __restrict__ targets, Geo g, int32_t b, int32_t e,
+                              int32_t* __restrict__ cursor, int32_t* __restrict__ list) {
+  int i = b + blockIdx.x * blockDim.x + threadIdx.x;
+  if (i >= e) return;
+  int x, y, t;
+  decode(g, targets[i], x, y, t);
+  list[atomicAdd(cursor + clip_pid(g, x, y, t), 1)] = i;
+}
+// per-source energy over the sub-box of a clip pattern: 4 sum c^2 + lambda sum t^2
+__global__ void k_energy_box(const uint64_t* __restrict__ vox, Geo g, const int32_t* __restrict__ sources,
+                             int32_t n, int32_t npad, int lambda, int pid, int64_t* __restrict__ E) {
+  int i = blockIdx.x * blockDim.x + threadIdx.x;
+  if (i >= npad) return;
+  if (i >= n) { E[i] = kEPad; return; }
+  int xl = pid % 3, xh = pid / 3 % 3, yl = pid / 9 % 3, yh = pid / 27 % 3, tl = pid / 81 % 3, th = pid / 243;
+  int q = sources[i];
+  uint64_t c = 0, tt = 0;
+  for (int dt = -2 + tl; dt <= 2 - th; ++dt)
+    for (int dy = -2 + yl; dy <= 2 - yh; ++dy)
+      for (int dx = -2 + xl; dx <= 2 - xh; ++dx) {
+        uint64_t w = vox[q + dt * g.HW + dy * g.W + dx];
+        uint32_t c0 = w & 255, c1 = (w >> 8) & 255, c2 = (w >> 16) & 255, t0 = (w >> 32) & 255, t1 = (w >> 40) & 255;
+        c += c0 * c0 + c1 * c1 + c2 * c2;
+        tt += t0 * t0 + t1 * t1;
+      }
+  E[i] = (int64_t)(4 * c + (uint64_t)lambda * tt);
 }
 
 // merge the split minima (lexicographic (D, index) = smallest D, then smallest source index)
 __global__ void k_bf_merge(const uint64_t* __restrict__ part, int splits, int32_t mpad, int32_t m,
                            const int32_t* __restrict__ list, const int32_t* __restrict__ sources,
-                           uint64_t* __restrict__ ee, uint8_t* __restrict__ en) {
+                           uint64_t* __restrict__ ee, uint8_t* __restrict__ en, int nvox) {
   int i = blockIdx.x * blockDim.x + threadIdx.x;
   if (i >= m) return;
   uint64_t best = ~0ull;
   for (int s = 0; s < splits; ++s) best = min(best, part[(size_t)s * mpad + i]);
   int slot = list[i];
   ee[slot] = pack_e((uint32_t)(best >> 32), sources[(uint32_t)best]);
-  en[slot] = 125;
-}
-
-// border (clipped) targets: the CUDA-core path, restricted to non-full targets
-__global__ void k_border_list(const int32_t* __restrict__ targets, Geo g, int32_t b, int32_t e,
-                              int32_t* __restrict__ list, int32_t* __restrict__ count) {
-  int i = b + blockIdx.x * blockDim.x + threadIdx.x;
-  if (i >= e) return;
-  int x, y, t;
-  decode(g, targets[i], x, y, t);
-  if (!full_patch(g, x, y, t)) list[atomicAdd(count, 1)] = i;
+  en[slot] = (uint8_t)nvox;
 }
 
 }  // namespace vinp
@@ -288,9 +321,10 @@ size_t vinp_brute_force_tc_ws_bytes(const vinp_level* lv, int32_t b, int32_t e) 
   int64_t m = std::max<int64_t>(0, e - b), mpad = (m + kTile - 1) / kTile * kTile;
   int64_t npad = ((int64_t)lv->n_sources + kTile - 1) / kTile * kTile;
   int64_t nb = (m + 255) / 256 + 1;
-  int splits = 64;
-  return (size_t)(mpad * kRow + mpad * 8 + npad * kRow + npad * 8 + mpad * 4 * 2 + nb * 4 + 64 +
-                  (int64_t)splits * mpad * 8 + 4096);
+  int64_t splits = (npad / 64) / ((64ll << 20) / (64 * kRow)) + 2;  // source chunks of 64 MB
+  (void)nb;
+  return (size_t)((mpad + 128 * 8) * kRow + (mpad + 128 * 8) * 8 + npad * kRow + 2 * npad * 8 + mpad * 4 +
+                  2 * 729 * 4 + 64 + splits * (mpad + 128 * 8) * 8 + 4096);
 }
 
 // implemented in ann.cu: CUDA-core exact NN over an explicit slot list
@@ -314,50 +348,57 @@ vinp_status vinp_brute_force_tc(const vinp_level* lv, vinp_nnf* out, const vinp_
   Geo g = geo_of(lv);
   int64_t m_all = e - b, mpad = (m_all + kTile - 1) / kTile * kTile;
   int64_t npad = ((int64_t)lv->n_sources + kTile - 1) / kTile * kTile;
+  int64_t np = ((int64_t)lv->n_sources + kTB - 1) / kTB * kTB;
   char* w = (char*)(((uintptr_t)ws + 1023) & ~(uintptr_t)1023);
-  uint8_t* A = (uint8_t*)w; w += mpad * kRow;
+  uint8_t* A = (uint8_t*)w; w += (mpad + kTA * 8) * kRow;
   uint8_t* B = (uint8_t*)w; w += npad * kRow;
-  int64_t* Ep = (int64_t*)w; w += mpad * 8;
+  int64_t* Ep = (int64_t*)w; w += (mpad + kTA * 8) * 8;
   int64_t* Eq = (int64_t*)w; w += npad * 8;
+  int64_t* Eb = (int64_t*)w; w += npad * 8;  // per-pattern source energies
   int32_t* list = (int32_t*)w; w += mpad * 4;
-  int32_t* blist = (int32_t*)w; w += mpad * 4;
-  int nb = (int)((m_all + 255) / 256);
-  int32_t* bc = (int32_t*)w; w += ((int64_t)nb + 1) * 4;
-  int32_t* cnt = (int32_t*)(((uintptr_t)w + 63) & ~(uintptr_t)63); w = (char*)cnt + 64;
+  int32_t* cnt = (int32_t*)(((uintptr_t)w + 63) & ~(uintptr_t)63); w = (char*)(cnt + 2 * kPids);
   uint64_t* part = (uint64_t*)(((uintptr_t)w + 63) & ~(uintptr_t)63);
-  // 1. full targets of [b, e) (ascending) and the border ones
-  k_full_flags<<<nb, 256, 0, s>>>(lv->targets, g, b, e, bc);
-  k_full_scan<<<1, 32, 0, s>>>(bc, nb, cnt);
-  k_full_write<<<nb, 256, 0, s>>>(lv->targets, g, b, e, bc, list);
-  cudaMemsetAsync(cnt + 1, 0, 4, s);
-  k_border_list<<<nblk(m_all, 256), 256, 0, s>>>(lv->targets, g, b, e, blist, cnt + 1);
-  count_launch(4);
-  int32_t h[2];
-  if (cudaMemcpyAsync(h, cnt, 8, cudaMemcpyDeviceToHost, s) != cudaSuccess || cudaStreamSynchronize(s) != cudaSuccess)
+  // 1. group the targets of [b, e) by clip pattern (one sync for the group sizes)
+  cudaMemsetAsync(cnt, 0, sizeof(int32_t) * 2 * kPids, s);
+  k_pid_count<<<nblk(m_all, 256), 256, 0, s>>>(lv->targets, g, b, e, cnt);
+  std::vector<int32_t> hc(kPids);
+  if (cudaMemcpyAsync(hc.data(), cnt, sizeof(int32_t) * kPids, cudaMemcpyDeviceToHost, s) != cudaSuccess ||
+      cudaStreamSynchronize(s) != cudaSuccess)
     return check_launch("vinp_brute_force_tc(count)");
-  int32_t m = h[0], nborder = h[1];
-  int32_t mp = (m + kTile - 1) / kTile * kTile;
-  if (m > 0) {
-    // 2. im2col of the full targets (by slot -> position) and of all sources
-    k_im2col<<<mp, 128, 0, s>>>(lv->vox, g, lv->targets, list, m, mp, prm->lambda, A, Ep);
-    k_im2col<<<(int)npad, 128, 0, s>>>(lv->vox, g, lv->sources, nullptr, lv->n_sources, (int)npad, prm->lambda, B, Eq);
-    // 3. tensor-core GEMM + exact argmin, N split across CTAs
-    int m_tiles = mp / kTile, n_tiles = (int)(npad / kTile);
-    int splits = std::max(1, std::min(std::min(64, n_tiles), (2 * 148 + m_tiles - 1) / m_tiles));
-    int per = (n_tiles + splits - 1) / splits;
-    splits = (n_tiles + per - 1) / per;
-    size_t smem = 2 * (size_t)kTile * kRow + kTile * 8;
-    cudaFuncSetAttribute(k_bf_tc, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
-    k_bf_tc<<<dim3(m_tiles, splits), 128, smem, s>>>(A, Ep, B, Eq, n_tiles, per, prm->lambda, mp, part);
-    k_bf_merge<<<nblk(m, 256), 256, 0, s>>>(part, splits, mp, m, list, lv->sources, out->e, out->n);
-    count_launch(4);
+  std::vector<int32_t> off(kPids + 1, 0);
+  for (int k = 0; k < kPids; ++k) off[k + 1] = off[k] + hc[k];
+  cudaMemcpyAsync(cnt + kPids, off.data(), sizeof(int32_t) * kPids, cudaMemcpyHostToDevice, s);
+  k_pid_scatter<<<nblk(m_all, 256), 256, 0, s>>>(lv->targets, g, b, e, cnt + kPids, list);
+  count_launch(2);
+  // 2. source im2col (tiles of 64) once, with the full-patch energies
+  k_im2col_tiled<<<(int)np, 128, 0, s>>>(lv->vox, g, lv->sources, nullptr, lv->n_sources, (int)np, prm->lambda,
+                                         kTB, B, Eq);
+  count_launch();
+  int nb_tiles = (int)(np / kTB);
+  int per = std::max(1, std::min(nb_tiles, (int)((64ll << 20) / kBBytes)));
+  int chunks = (nb_tiles + per - 1) / per;
+  size_t smem = kABytes + 2 * (size_t)kBBytes;
+  cudaFuncSetAttribute(k_bf_tc2, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+  // 3. one warp-specialised tensor-core GEMM + exact argmin per clip pattern
+  for (int pid = 0; pid < kPids; ++pid) {
+    int32_t m = hc[pid];
+    if (m == 0) continue;
+    int32_t mp = (m + kTA - 1) / kTA * kTA;
+    const int32_t* lst = list + off[pid];
+    const int64_t* E = Eq;
+    if (pid != 0) {
+      k_energy_box<<<nblk(np, 256), 256, 0, s>>>(lv->vox, g, lv->sources, lv->n_sources, (int)np, prm->lambda, pid, Eb);
+      count_launch();
+      E = Eb;
+    }
+    int nvox = (5 - pid % 3 - pid / 3 % 3) * (5 - pid / 9 % 3 - pid / 27 % 3) * (5 - pid / 81 % 3 - pid / 243);
+    k_im2col_tiled<<<mp, 128, 0, s>>>(lv->vox, g, lv->targets, lst, m, mp, prm->lambda, kTA, A, Ep);
+    k_bf_tc2<<<dim3(mp / kTA, chunks), 192, smem, s>>>(A, Ep, B, E, nb_tiles, per, prm->lambda, mp, part);
+    k_bf_merge<<<nblk(m, 256), 256, 0, s>>>(part, chunks, mp, m, lst, lv->sources, out->e, out->n, nvox);
+    count_launch(3);
   }
-  st = check_launch("vinp_brute_force_tc");
-  if (st) return st;
-  if (nborder > 0) return vinp_brute_force_list(lv, out, prm, blist, nborder, stream);
-  return VINP_OK;
+  return check_launch("vinp_brute_force_tc");
 }
-
 
 vinp_status vinp_tc_gemm_u8(const uint8_t* A, const uint8_t* B, int K, int32_t* C, void* stream) {
   VINP_REQUIRE(A && B && C && K > 0 && K % 32 == 0 && K <= 512, "vinp_tc_gemm_u8: bad arguments");
