@@ -36,7 +36,7 @@ def _quality(name, max_targets=None, steps=(8, 4, 2, 1), sign_policy=0):
     cnt = torch.zeros(1, dtype=torch.int64, device="cuda")
     V.ann_search(lv, st.a, st.b, ip.prm, 0, c.pm_iters, tuple(steps), counter=cnt, sign_policy=sign_policy)
     bf = V.NNF.alloc(lv.n_targets, "cuda")
-    V.brute_force(lv, bf, ip.prm, 0, n)
+    V.brute_force_tc(lv, bf, ip.prm, 0, n)  # exact; bit-identical to the CUDA-core form (tests)
     torch.cuda.synchronize()
     Dp = (st.a.e[:n] >> 32).double()
     Db = (bf.e[:n] >> 32).double()
@@ -52,7 +52,7 @@ def _quality(name, max_targets=None, steps=(8, 4, 2, 1), sign_policy=0):
                 ratio_minus_1=d_pm / d_bf - 1 if d_bf > 0 else 0.0, frac_exact=same)
 
 
-@pytest.mark.parametrize("name", ["c1", "c2"])
+@pytest.mark.parametrize("name", ["c1", "c2", "c3"])
 def test_patchmatch_quality_vs_brute_force(name):
     q = _quality(name)
     os.makedirs(os.path.join(ROOT, "gpurun_out"), exist_ok=True)
