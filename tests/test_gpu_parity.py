@@ -346,3 +346,19 @@ def test_native_onion_peel_equals_stepwise(V):
     for x, y in zip(res[0][:5], res[1][:5]):
         assert torch.equal(x, y)
     assert res[0][5] == res[1][5]
+
+
+def test_pipeline_c2_full_config_end_to_end(orc):
+    """BASELINE c2 as configured (2 levels, K = 10, stopping rule, max 20): the whole Alg. 4 on the
+    GPU equals the oracle's whole pipeline, including every level's outer-iteration count."""
+    from paper_1503_05528_b200 import Config, inpaint
+    from gen.synth import CONFIGS
+    c = CONFIGS["c2"]
+    v, m, _ = generate("c2")
+    cfg = Config(levels=c.levels, pm_iters=c.pm_iters, max_outer=c.max_outer, lam=c.lam, seed=c.seed)
+    out, stats, _ = inpaint(v, m, cfg)
+    ref, st = orc.inpaint(v.numpy(), m.numpy(), c.levels, pm_iters=c.pm_iters, max_outer=c.max_outer,
+                          lam=c.lam, seed=c.seed)
+    assert [l["outer"] for l in stats.levels] == st["outer_iters"]
+    assert stats.total_patch_updates == sum(st["patch_updates"])
+    assert np.array_equal(out.cpu().numpy(), ref)
