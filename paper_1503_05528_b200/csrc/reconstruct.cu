@@ -65,35 +65,51 @@ __global__ void __launch_bounds__(256) k_reconstruct(ReconArgs a, int mode, int 
   if (layer_j >= 0 && a.layer[p] != layer_j) return;
   int px, py, pt;
   decode(a.g, p, px, py, pt);
+  // Gather in three dependent rounds with all four contributors of the lane in flight per round
+  // (branch-free: out-of-range entries read a safe address and are masked): slot[q]; then the NNF
+  // entry and n of that slot; then the proposed value u(p + phi(q)) = vox[src_q - off].
   uint32_t Dq[4], nq[4];
   uint64_t val[4];
   unsigned valid = 0;
-  bool n125 = true;  // every valid contributor has a full patch (n = 125)
+  bool n125 = true;
+  int off[4];
+  bool cand[4];
 #pragma unroll
   for (int i = 0; i < 4; ++i) {
     int v = lane + 32 * i;
-    Dq[i] = 0; nq[i] = 125; val[i] = 0;
-    if (v < kPatch) {
-      int dx, dy, dt;
-      voff(v, dx, dy, dt);
-      if (inside(a.g, px + dx, py + dy, pt + dt)) {
-        int off = dt * a.g.HW + dy * a.g.W + dx;
-        int q = p + off;
-        if (layer_j < 0 || a.layer[q] < layer_j) {
-          int s = __ldg(a.slot + q);
-          if (s >= 0) {
-            uint32_t n = __ldg(a.n + s);
-            if (mode == VINP_UNWEIGHTED || n > 0) {
-              uint64_t e = __ldg(reinterpret_cast<const unsigned long long*>(a.e) + s);
-              Dq[i] = e_D(e);
-              nq[i] = n;
-              n125 &= (n == 125);
-              val[i] = __ldg(reinterpret_cast<const unsigned long long*>(a.vox) + (e_q(e) - off));
-              valid |= 1u << i;
-            }
-          }
-        }
-      }
+    int dx, dy, dt;
+    voff(v < kPatch ? v : 62, dx, dy, dt);
+    off[i] = dt * a.g.HW + dy * a.g.W + dx;
+    cand[i] = v < kPatch && inside(a.g, px + dx, py + dy, pt + dt);
+  }
+  if (layer_j >= 0) {
+#pragma unroll
+    for (int i = 0; i < 4; ++i) cand[i] = cand[i] && a.layer[p + (cand[i] ? off[i] : 0)] < layer_j;
+  }
+  int sl[4];
+#pragma unroll
+  for (int i = 0; i < 4; ++i) sl[i] = __ldg(a.slot + p + (cand[i] ? off[i] : 0));
+  uint64_t ev[4];
+  uint32_t nv[4];
+#pragma unroll
+  for (int i = 0; i < 4; ++i) {
+    bool ok = cand[i] && sl[i] >= 0;
+    int si = ok ? sl[i] : 0;
+    ev[i] = __ldg(reinterpret_cast<const unsigned long long*>(a.e) + si);
+    nv[i] = __ldg(a.n + si);
+    cand[i] = ok;
+  }
+#pragma unroll
+  for (int i = 0; i < 4; ++i) {
+    bool ok = cand[i] && (mode == VINP_UNWEIGHTED || nv[i] > 0);
+    val[i] = __ldg(reinterpret_cast<const unsigned long long*>(a.vox) + (ok ? e_q(ev[i]) - off[i] : p));
+    Dq[i] = ok ? e_D(ev[i]) : 0;
+    nq[i] = ok ? nv[i] : 125;
+    if (ok) {
+      n125 &= (nv[i] == 125);
+      valid |= 1u << i;
+    } else {
+      val[i] = 0;
     }
   }
   uint32_t m = __reduce_add_sync(kFull, (uint32_t)__popc(valid));
