@@ -305,3 +305,32 @@ def random_volume(W, H, T, seed, hole_frac=0.05, device="cpu", smooth=True):
     truth = video.clone()
     video[mask.bool()] = 0
     return video, mask, truth
+
+
+def camera_video(W, H, T, seed, cams, noise=0.0, block=None, device="cpu", cell=32.0):
+    """Frames of a static textured world seen through per-frame affine cameras (NEXT #1 inputs).
+
+    ``cams[t]`` = (c0..c5): frame t's pixel (x, y) shows world point
+    (c0 + c1 x + c2 y, c3 + c4 x + c5 y); the world is 255 * fbm (one field per channel).  Then
+    the true inter-frame motion is theta_{t,t+1} = cams[t+1]^{-1} o cams[t].  ``noise``: i.i.d.
+    Gaussian sigma (grey levels) per pixel and channel.  ``block`` = (x0, y0, w, h, dx, dy): a
+    fixed frame rectangle showing a second texture that moves by (dx, dy) per frame (an
+    independently moving object).  Returns u8 [T, H, W, 3]."""
+    x, y = _grid(W, H, device)
+    out = torch.empty((T, H, W, 3), dtype=torch.uint8, device=device)
+    pix = (y * W + x).to(torch.int64)
+    for t in range(T):
+        c = cams[t]
+        wx = c[0] + c[1] * x + c[2] * y
+        wy = c[3] + c[4] * x + c[5] * y
+        img = [255.0 * fbm(wx, wy, 70 + k, seed, base_cell=cell) for k in range(3)]
+        if block is not None:
+            bx0, by0, bw, bh, bdx, bdy = block
+            ins = (x >= bx0) & (x < bx0 + bw) & (y >= by0) & (y < by0 + bh)
+            for k in range(3):
+                img[k] = torch.where(ins, 255.0 * fbm(x - bdx * t, y - bdy * t, 80 + k, seed, base_cell=cell),
+                                     img[k])
+        if noise > 0:
+            img = [v + noise * normal(pix, t, 90 + k, 3, seed) for k, v in enumerate(img)]
+        out[t] = _round_u8(torch.stack(img, -1))
+    return out

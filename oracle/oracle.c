@@ -691,6 +691,7 @@ int or_inpaint(const uint8_t* rgb, const uint8_t* occ, int W, int H, int T, cons
   int L = prm->levels;
   if (L < 1 || L > 16) return 1;
   or_work* w = (or_work*)calloc(L + 1, sizeof(or_work));
+  uint8_t* inv[17] = {0};
   memset(st, 0, sizeof(*st));
   /* pyramids: Alg. 4 */
   for (int l = 1; l <= L; ++l) {
@@ -705,12 +706,17 @@ int or_inpaint(const uint8_t* rgb, const uint8_t* occ, int W, int H, int T, cons
     lv->src = (uint8_t*)malloc(N);
     lv->tgt = (uint8_t*)malloc(N);
     lv->layer = NULL;
+    inv[l] = (uint8_t*)malloc(N);
     if (l == 1) {
       memcpy(lv->rgb, rgb, 3 * N);
-      memcpy(lv->occ, occ, N);
+      for (int64_t i = 0; i < N; ++i) { /* occ codes: 1 (any nonzero but 2) = H, 2 = X (R40) */
+        lv->occ[i] = (uint8_t)(occ[i] != 0 && occ[i] != 2);
+        inv[l][i] = (uint8_t)(occ[i] == 2);
+      }
     } else {
       or_level* f = &w[l - 1].lv;
       or_pyramid_down(f->rgb, f->occ, f->W, f->H, T, lv->rgb, lv->occ);
+      or_mask_down(inv[l - 1], f->W, f->H, T, inv[l]);
     }
   }
   int h = prm->tex_half >= 0 ? prm->tex_half : ((L >= 2 ? (1 << (L - 2)) : 1));
@@ -720,7 +726,7 @@ int or_inpaint(const uint8_t* rgb, const uint8_t* occ, int W, int H, int T, cons
     or_texture_decimate(w[1].lv.tex, W, H, T, l, w[l].lv.W, w[l].lv.H, w[l].lv.tex);
   for (int l = 1; l <= L; ++l) {
     or_level* lv = &w[l].lv;
-    or_sets(lv->occ, lv->W, lv->H, T, lv->src, lv->tgt);
+    or_sets_x(lv->occ, inv[l], lv->W, lv->H, T, lv->src, lv->tgt);
     build_lists(lv);
     if (lv->n_sources == 0) return 2; /* S:237 */
     alloc_nnf(&w[l].a, lv->n_targets);
@@ -785,6 +791,7 @@ int or_inpaint(const uint8_t* rgb, const uint8_t* occ, int W, int H, int T, cons
   for (int l = 1; l <= L; ++l) {
     or_level* lv = &w[l].lv;
     free(lv->rgb); free(lv->tex); free(lv->occ); free(lv->src); free(lv->tgt); free(lv->layer);
+    free(inv[l]);
     free(lv->slot); free(lv->targets); free(lv->holes); free(lv->sources);
     free_nnf(&w[l].a); free_nnf(&w[l].b);
     free(w[l].cur_rgb); free(w[l].cur_tex); free(w[l].prev_rgb); free(w[l].prev_tex);
@@ -917,4 +924,414 @@ int64_t or_ann_search_sequential(const or_level* lv, or_nnf* f, int lambda, uint
     }
   }
   return cnt;
+}
+
+/* ==========================================================================================
+ * a2 with the invalid set X of a realigned video (R40, S3.4 P:752-753 "the occlusion H is
+ * obviously also realigned"; "pixels whose source falls outside the original frame
+ * are flagged invalid (excluded from D~)").  Literal neighbourhood loops as or_sets.
+ * ======================================================================================== */
+void or_sets_x(const uint8_t* occ, const uint8_t* inv, int W, int H, int T, uint8_t* src,
+               uint8_t* tgt) {
+#pragma omp parallel for
+  for (int t = 0; t < T; ++t)
+    for (int y = 0; y < H; ++y)
+      for (int x = 0; x < W; ++x) {
+        int ok = 1, hit = 0;
+        for (int dt = -PR; dt <= PR; ++dt)
+          for (int dy = -PR; dy <= PR; ++dy)
+            for (int dx = -PR; dx <= PR; ++dx) {
+              int qx = x + dx, qy = y + dy, qt = t + dt;
+              if (qx < 0 || qx >= W || qy < 0 || qy >= H || qt < 0 || qt >= T) {
+                ok = 0;
+                continue;
+              }
+              int64_t q = ((int64_t)qt * H + qy) * W + qx;
+              if (occ[q]) {
+                ok = 0;
+                hit = 1;
+              }
+              if (inv && inv[q]) ok = 0;
+            }
+        int64_t o = ((int64_t)t * H + y) * W + x;
+        src[o] = (uint8_t)ok;
+        tgt[o] = (uint8_t)hit;
+      }
+}
+
+void or_mask_down(const uint8_t* m, int W, int H, int T, uint8_t* mc) {
+  int Wc = (W + 1) / 2, Hc = (H + 1) / 2;
+  for (int t = 0; t < T; ++t)
+    for (int Y = 0; Y < Hc; ++Y)
+      for (int X = 0; X < Wc; ++X) {
+        int any = 0;
+        for (int dy = 0; dy < 2; ++dy)
+          for (int dx = 0; dx < 2; ++dx) {
+            int fx = 2 * X + dx, fy = 2 * Y + dy;
+            if (fx < W && fy < H && m[((int64_t)t * H + fy) * W + fx]) any = 1;
+          }
+        mc[((int64_t)t * Hc + Y) * Wc + X] = (uint8_t)any;
+      }
+}
+
+/* ==========================================================================================
+ * NEXT #1 — Alg. 2: EstimateAffineMotion(u_n, u_{n+1}) for n = 1..N_f-1, the
+ * chain theta_{n,N_m}, AffineWarp; S3.4: Odobez-Bouthemy robust dominant affine
+ * motion, "linear interpolation" for the realigned colours, realigned occlusion, inverse
+ * transformation and paste into the original occluded area after inpainting.
+ * The paper names the estimator only by citation; R36-R38 fix it, after
+ * robust penalty of the brightness-constancy residual, IRLS on the linearised
+ * residual, 3-level coarse-to-fine, Tukey biweight with MAD scale, <= 20 iterations per level
+ * or update norm < 1e-4.  Everything is fp64 written out in a fixed operation order (no FMA
+ * contraction: the library is built with -ffp-contract=off) and the normal equations are summed
+ * exactly in 2^-16 fixed point, so the GPU's parallel sums reproduce them bit for bit.
+ * ======================================================================================== */
+void or_affine_compose(const double* t2, const double* t1, double* out) {
+  /* (A2, b2) o (A1, b1) = (A2 A1, A2 b1 + b2) */
+  double r[6];
+  r[1] = t2[1] * t1[1] + t2[2] * t1[4];
+  r[2] = t2[1] * t1[2] + t2[2] * t1[5];
+  r[4] = t2[4] * t1[1] + t2[5] * t1[4];
+  r[5] = t2[4] * t1[2] + t2[5] * t1[5];
+  r[0] = (t2[1] * t1[0] + t2[2] * t1[3]) + t2[0];
+  r[3] = (t2[4] * t1[0] + t2[5] * t1[3]) + t2[3];
+  for (int i = 0; i < 6; ++i) out[i] = r[i];
+}
+
+int or_affine_invert(const double* t, double* out) {
+  double det = t[1] * t[5] - t[2] * t[4];
+  if (!(fabs(det) > 1e-300)) return 1;
+  double i11 = t[5] / det, i12 = -t[2] / det, i21 = -t[4] / det, i22 = t[1] / det;
+  double r0 = -(i11 * t[0] + i12 * t[3]);
+  double r3 = -(i21 * t[0] + i22 * t[3]);
+  out[0] = r0; out[1] = i11; out[2] = i12; out[3] = r3; out[4] = i21; out[5] = i22;
+  return 0;
+}
+
+/* R36: grey level I = (299 R + 587 G + 114 B) / 1000 (exact integer numerator, one division);
+ * estimation pyramid: level k = 2x2 box mean of level k-1 on floor(W/2) x floor(H/2), excluded
+ * (occluded) if any of the 4 is; the number of levels is reduced while the coarsest would be
+ * smaller than 8 pixels on a side. */
+typedef struct {
+  int W, H;
+  double* I;
+  uint8_t* M;
+} or_grey;
+
+static void grey_pyr(const uint8_t* rgb, const uint8_t* occ, int W, int H, int L, or_grey* P) {
+  P[0].W = W; P[0].H = H;
+  P[0].I = (double*)malloc(sizeof(double) * W * H);
+  P[0].M = (uint8_t*)malloc((size_t)W * H);
+  for (int64_t i = 0; i < (int64_t)W * H; ++i) {
+    int g = 299 * rgb[3 * i] + 587 * rgb[3 * i + 1] + 114 * rgb[3 * i + 2];
+    P[0].I[i] = (double)g / 1000.0;
+    P[0].M[i] = (uint8_t)(occ && occ[i] ? 1 : 0);
+  }
+  for (int k = 1; k < L; ++k) {
+    int Wk = P[k - 1].W / 2, Hk = P[k - 1].H / 2, Wf = P[k - 1].W;
+    P[k].W = Wk; P[k].H = Hk;
+    P[k].I = (double*)malloc(sizeof(double) * Wk * Hk);
+    P[k].M = (uint8_t*)malloc((size_t)Wk * Hk);
+    for (int j = 0; j < Hk; ++j)
+      for (int i = 0; i < Wk; ++i) {
+        int64_t a = (int64_t)(2 * j) * Wf + 2 * i;
+        const double* F = P[k - 1].I;
+        const uint8_t* FM = P[k - 1].M;
+        P[k].I[(int64_t)j * Wk + i] = (((F[a] + F[a + 1]) + F[a + Wf]) + F[a + Wf + 1]) * 0.25;
+        P[k].M[(int64_t)j * Wk + i] = (uint8_t)(FM[a] | FM[a + 1] | FM[a + Wf] | FM[a + Wf + 1]);
+      }
+  }
+}
+
+static int est_levels(int W, int H, int levels) {
+  int L = levels < 1 ? 1 : levels;
+  while (L > 1 && ((W >> (L - 1)) < 8 || (H >> (L - 1)) < 8)) --L;
+  return L;
+}
+
+static int cmp_double(const void* a, const void* b) {
+  double x = *(const double*)a, y = *(const double*)b;
+  return x < y ? -1 : (x > y ? 1 : 0);
+}
+
+/* bilinear sample at (xw, yw) inside [0, W-1] x [0, H-1] (R37: x0 = min(floor(xw), W-2)) */
+static double bil(const double* I, int W, int x0, int y0, double fx, double fy) {
+  const double* r0 = I + (int64_t)y0 * W + x0;
+  const double* r1 = r0 + W;
+  return (1.0 - fy) * ((1.0 - fx) * r0[0] + fx * r0[1]) + fy * ((1.0 - fx) * r1[0] + fx * r1[1]);
+}
+
+/* central-difference gradient of I at integer (i, j), clamped indices (R37) */
+static double gradx(const double* I, int W, int i, int j) {
+  int ip = i + 1 < W ? i + 1 : W - 1, im = i - 1 >= 0 ? i - 1 : 0;
+  return (I[(int64_t)j * W + ip] - I[(int64_t)j * W + im]) * 0.5;
+}
+static double grady(const double* I, int W, int H, int i, int j) {
+  int jp = j + 1 < H ? j + 1 : H - 1, jm = j - 1 >= 0 ? j - 1 : 0;
+  return (I[(int64_t)jp * W + i] - I[(int64_t)jm * W + i]) * 0.5;
+}
+
+/* One pixel of frame a at level (W, H): warped position with the parameter vector
+ * p = (b_x, s A11, s A12, b_y, s A21, s A22) acting on normalised centred coordinates
+ * X = (i - cx) / s, Y = (j - cy) / s (R37).  Returns 1 if the pixel votes. */
+static int irls_pixel(const or_grey* A, const or_grey* B, const double* p, double cx, double cy,
+                      double s, int i, int j, double* r, int* x0o, int* y0o, double* fxo,
+                      double* fyo, double* Xo, double* Yo) {
+  int W = A->W, H = A->H;
+  if (A->M[(int64_t)j * W + i]) return 0;
+  double X = ((double)i - cx) / s, Y = ((double)j - cy) / s;
+  double xw = ((p[0] + p[1] * X) + p[2] * Y) + cx;
+  double yw = ((p[3] + p[4] * X) + p[5] * Y) + cy;
+  if (!(xw >= 0.0 && xw <= (double)(W - 1) && yw >= 0.0 && yw <= (double)(H - 1))) return 0;
+  int x0 = (int)floor(xw), y0 = (int)floor(yw);
+  if (x0 > W - 2) x0 = W - 2;
+  if (y0 > H - 2) y0 = H - 2;
+  /* frame b's occlusion: reject if any pixel the sample or its central-difference gradient
+   * reads (rows y0-1..y0+2 x cols x0-1..x0+2, clamped) is occluded */
+  for (int yy = y0 - 1; yy <= y0 + 2; ++yy)
+    for (int xx = x0 - 1; xx <= x0 + 2; ++xx) {
+      int cy_ = yy < 0 ? 0 : (yy > H - 1 ? H - 1 : yy), cx_ = xx < 0 ? 0 : (xx > W - 1 ? W - 1 : xx);
+      if (B->M[(int64_t)cy_ * W + cx_]) return 0;
+    }
+  double fx = xw - (double)x0, fy = yw - (double)y0;
+  *r = bil(B->I, W, x0, y0, fx, fy) - A->I[(int64_t)j * W + i];
+  *x0o = x0; *y0o = y0; *fxo = fx; *fyo = fy; *Xo = X; *Yo = Y;
+  return 1;
+}
+
+/* 6x6 solve, Gaussian elimination with partial pivoting (first maximal |pivot|); 1 = singular */
+static int solve6(double M[6][7], double* x) {
+  double md = 0.0;
+  for (int k = 0; k < 6; ++k)
+    if (fabs(M[k][k]) > md) md = fabs(M[k][k]);
+  for (int k = 0; k < 6; ++k) {
+    int pr = k;
+    for (int r = k + 1; r < 6; ++r)
+      if (fabs(M[r][k]) > fabs(M[pr][k])) pr = r;
+    if (pr != k)
+      for (int c = 0; c < 7; ++c) {
+        double tmp = M[k][c]; M[k][c] = M[pr][c]; M[pr][c] = tmp;
+      }
+    if (!(fabs(M[k][k]) > 1e-9 * md)) return 1;
+    for (int r = k + 1; r < 6; ++r) {
+      double f = M[r][k] / M[k][k];
+      for (int c = k; c < 7; ++c) M[r][c] = M[r][c] - f * M[k][c];
+    }
+  }
+  for (int k = 5; k >= 0; --k) {
+    double a = M[k][6];
+    for (int c = k + 1; c < 6; ++c) a = a - M[k][c] * x[c];
+    x[k] = a / M[k][k];
+  }
+  return 0;
+}
+
+/* R38: one level of IRLS.  Iteration: (1) residuals r of the voting pixels; n < 12 -> degenerate;
+ * (2) sigma = 1.4826 * lower median of |r| (rank floor((n-1)/2)), floored at 1e-6; c = 4.6851
+ * sigma; (3) Tukey weights w = (1 - (r/c)^2)^2 for |r| < c, else 0; normal equations of the
+ * linearised residual r + J.dp with J = (gx, gx X, gx Y, gy, gy X, gy Y), gx, gy the bilinearly
+ * interpolated central-difference gradient of frame b at the warped position, summed exactly as
+ * int64 of llrint(term * 2^16); (4) solve (sum w J J^T) dp = -(sum w J r); p += dp; stop when
+ * |dp|_2 < tol or after max_iter iterations. */
+static int irls_level(const or_grey* A, const or_grey* B, double* p, int max_iter, double tol,
+                      int* iters) {
+  int W = A->W, H = A->H;
+  double cx = (double)(W - 1) * 0.5, cy = (double)(H - 1) * 0.5;
+  double s = (double)(W > H ? W : H) * 0.5;
+  double* ar = (double*)malloc(sizeof(double) * W * H);
+  int status = 0;
+  for (int it = 0; it < max_iter; ++it) {
+    int64_t n = 0;
+    for (int j = 0; j < H; ++j)
+      for (int i = 0; i < W; ++i) {
+        double r, fx, fy, X, Y;
+        int x0, y0;
+        if (irls_pixel(A, B, p, cx, cy, s, i, j, &r, &x0, &y0, &fx, &fy, &X, &Y)) ar[n++] = fabs(r);
+      }
+    if (n < 12) { status = 1; break; }
+    qsort(ar, (size_t)n, sizeof(double), cmp_double);
+    double sigma = 1.4826 * ar[(n - 1) / 2];
+    if (sigma < 1e-6) sigma = 1e-6;
+    double c = 4.6851 * sigma;
+    int64_t S[6][6] = {{0}}, R[6] = {0};
+    for (int j = 0; j < H; ++j)
+      for (int i = 0; i < W; ++i) {
+        double r, fx, fy, X, Y;
+        int x0, y0;
+        if (!irls_pixel(A, B, p, cx, cy, s, i, j, &r, &x0, &y0, &fx, &fy, &X, &Y)) continue;
+        double u = r / c;
+        if (!(fabs(u) < 1.0)) continue;
+        double q = 1.0 - u * u;
+        double w = q * q;
+        double g00 = gradx(B->I, W, x0, y0), g10 = gradx(B->I, W, x0 + 1, y0);
+        double g01 = gradx(B->I, W, x0, y0 + 1), g11 = gradx(B->I, W, x0 + 1, y0 + 1);
+        double gx = (1.0 - fy) * ((1.0 - fx) * g00 + fx * g10) + fy * ((1.0 - fx) * g01 + fx * g11);
+        g00 = grady(B->I, W, H, x0, y0); g10 = grady(B->I, W, H, x0 + 1, y0);
+        g01 = grady(B->I, W, H, x0, y0 + 1); g11 = grady(B->I, W, H, x0 + 1, y0 + 1);
+        double gy = (1.0 - fy) * ((1.0 - fx) * g00 + fx * g10) + fy * ((1.0 - fx) * g01 + fx * g11);
+        double J[6] = {gx, gx * X, gx * Y, gy, gy * X, gy * Y};
+        for (int a = 0; a < 6; ++a) {
+          double wa = w * J[a];
+          for (int b = a; b < 6; ++b) S[a][b] += llrint(wa * J[b] * 65536.0);
+          R[a] += llrint(wa * r * 65536.0);
+        }
+      }
+    double M[6][7], dp[6];
+    for (int a = 0; a < 6; ++a) {
+      for (int b = 0; b < 6; ++b) M[a][b] = (double)(a <= b ? S[a][b] : S[b][a]) / 65536.0;
+      M[a][6] = -((double)R[a] / 65536.0);
+    }
+    ++*iters;
+    if (solve6(M, dp)) { status = 1; break; }
+    double nrm = 0.0;
+    for (int a = 0; a < 6; ++a) {
+      p[a] = p[a] + dp[a];
+      nrm = nrm + dp[a] * dp[a];
+    }
+    if (sqrt(nrm) < tol) break;
+  }
+  free(ar);
+  return status;
+}
+
+/* parameter vector of level k (coarse) -> level k-1 (fine): centred pixel coordinates satisfy
+ * X_fine = 2 X_coarse + d with d = 2 c_coarse + 0.5 - c_fine per axis; (A, b) -> (A, 2b + (I-A)d) */
+static void level_up(double* p, int Wc, int Hc, int Wf, int Hf) {
+  double sc = (double)(Wc > Hc ? Wc : Hc) * 0.5, sf = (double)(Wf > Hf ? Wf : Hf) * 0.5;
+  double a11 = p[1] / sc, a12 = p[2] / sc, a21 = p[4] / sc, a22 = p[5] / sc;
+  double dx = ((double)(Wc - 1) + 0.5) - (double)(Wf - 1) * 0.5;
+  double dy = ((double)(Hc - 1) + 0.5) - (double)(Hf - 1) * 0.5;
+  double bx = 2.0 * p[0] + ((dx - a11 * dx) - a12 * dy);
+  double by = 2.0 * p[3] + ((dy - a21 * dx) - a22 * dy);
+  p[0] = bx; p[1] = a11 * sf; p[2] = a12 * sf;
+  p[3] = by; p[4] = a21 * sf; p[5] = a22 * sf;
+}
+
+int or_affine_estimate(const uint8_t* rgb_a, const uint8_t* rgb_b, const uint8_t* occ_a,
+                       const uint8_t* occ_b, int W, int H, int levels, int max_iter, double tol,
+                       double* theta, int* iters_out) {
+  int L = est_levels(W, H, levels);
+  or_grey PA[8], PB[8];
+  grey_pyr(rgb_a, occ_a, W, H, L, PA);
+  grey_pyr(rgb_b, occ_b, W, H, L, PB);
+  double s = (double)(PA[L - 1].W > PA[L - 1].H ? PA[L - 1].W : PA[L - 1].H) * 0.5;
+  double p[6] = {0.0, s, 0.0, 0.0, 0.0, s};
+  int status = 0, iters = 0;
+  for (int k = L - 1; k >= 0; --k) {
+    if (k < L - 1) level_up(p, PA[k + 1].W, PA[k + 1].H, PA[k].W, PA[k].H);
+    status = irls_level(&PA[k], &PB[k], p, max_iter, tol, &iters);
+    if (status) break;
+  }
+  if (status) {
+    theta[0] = 0.0; theta[1] = 1.0; theta[2] = 0.0; theta[3] = 0.0; theta[4] = 0.0; theta[5] = 1.0;
+  } else {
+    /* centred normalised -> spec form: x' = A (x - c) + b + c */
+    double s0 = (double)(W > H ? W : H) * 0.5, cx = (double)(W - 1) * 0.5, cy = (double)(H - 1) * 0.5;
+    double a11 = p[1] / s0, a12 = p[2] / s0, a21 = p[4] / s0, a22 = p[5] / s0;
+    theta[0] = (p[0] + cx) - (a11 * cx + a12 * cy);
+    theta[1] = a11; theta[2] = a12;
+    theta[3] = (p[3] + cy) - (a21 * cx + a22 * cy);
+    theta[4] = a21; theta[5] = a22;
+  }
+  for (int k = 0; k < L; ++k) { free(PA[k].I); free(PA[k].M); free(PB[k].I); free(PB[k].M); }
+  if (iters_out) *iters_out = iters;
+  return status;
+}
+
+/* R39: 0-based reference m = max(floor(T/2) - 1, 0) (the paper's 1-based N_m = floor(N_f/2));
+ * theta_{m,m} = identity; n < m: theta_{n,m} = theta_{n+1,m} o theta_{n,n+1};
+ * n > m: theta_{n,m} = theta_{n-1,m} o theta_{n-1,n}^{-1} (Alg. 2, the n > N_m product
+ * read as theta^{-1}_{N_m,N_m+1} o ... o theta^{-1}_{n-1,n}). */
+int or_affine_chain(const double* pairs, int T, double* fwd, double* inv) {
+  int m = T / 2 - 1;
+  if (m < 0) m = 0;
+  double id[6] = {0.0, 1.0, 0.0, 0.0, 0.0, 1.0};
+  for (int i = 0; i < 6; ++i) fwd[6 * m + i] = id[i];
+  for (int n = m - 1; n >= 0; --n) or_affine_compose(fwd + 6 * (n + 1), pairs + 6 * n, fwd + 6 * n);
+  for (int n = m + 1; n < T; ++n) {
+    double pi[6];
+    if (or_affine_invert(pairs + 6 * (n - 1), pi)) return 1;
+    or_affine_compose(fwd + 6 * (n - 1), pi, fwd + 6 * n);
+  }
+  for (int n = 0; n < T; ++n)
+    if (or_affine_invert(fwd + 6 * n, inv + 6 * n)) return 1;
+  return 0;
+}
+
+/* R40: clamp-to-edge bilinear sample of an RGB frame at (xs, ys): coordinates clamped to
+ * [0, W-1] x [0, H-1], x0 = min(floor, W-2), value rounded half up to u8.  Also reports the
+ * footprint pixels with nonzero weight (bit 0: (x0,y0), 1: (x0+1,y0), 2: (x0,y0+1), 3: both). */
+static void sample_rgb(const uint8_t* F, int W, int H, double xs, double ys, uint8_t* out, int* x0o,
+                       int* y0o, int* fpo) {
+  double xc = xs >= 0.0 ? (xs <= (double)(W - 1) ? xs : (double)(W - 1)) : 0.0;
+  double yc = ys >= 0.0 ? (ys <= (double)(H - 1) ? ys : (double)(H - 1)) : 0.0;
+  int x0 = (int)floor(xc), y0 = (int)floor(yc);
+  if (x0 > W - 2) x0 = W - 2;
+  if (y0 > H - 2) y0 = H - 2;
+  double fx = xc - (double)x0, fy = yc - (double)y0;
+  const uint8_t* r0 = F + 3 * ((int64_t)y0 * W + x0);
+  const uint8_t* r1 = r0 + 3 * (int64_t)W;
+  for (int c = 0; c < 3; ++c) {
+    double v = (1.0 - fy) * ((1.0 - fx) * (double)r0[c] + fx * (double)r0[3 + c]) +
+               fy * ((1.0 - fx) * (double)r1[c] + fx * (double)r1[3 + c]);
+    double rv = floor(v + 0.5);
+    out[c] = (uint8_t)(rv < 0.0 ? 0 : (rv > 255.0 ? 255 : (int)rv));
+  }
+  int fp = 0;
+  if (fx < 1.0 && fy < 1.0) fp |= 1;
+  if (fx > 0.0 && fy < 1.0) fp |= 2;
+  if (fx < 1.0 && fy > 0.0) fp |= 4;
+  if (fx > 0.0 && fy > 0.0) fp |= 8;
+  *x0o = x0; *y0o = y0; *fpo = fp;
+}
+
+void or_align_warp(const uint8_t* rgb, const uint8_t* occ, int W, int H, int T, const double* inv,
+                   uint8_t* rgb_out, uint8_t* mask_out) {
+#pragma omp parallel for
+  for (int t = 0; t < T; ++t) {
+    const double* q = inv + 6 * t;
+    const uint8_t* F = rgb + 3 * (int64_t)t * W * H;
+    const uint8_t* M = occ + (int64_t)t * W * H;
+    for (int y = 0; y < H; ++y)
+      for (int x = 0; x < W; ++x) {
+        double xs = (q[0] + q[1] * (double)x) + q[2] * (double)y;
+        double ys = (q[3] + q[4] * (double)x) + q[5] * (double)y;
+        int64_t o = ((int64_t)t * H + y) * W + x;
+        int x0, y0, fp;
+        sample_rgb(F, W, H, xs, ys, rgb_out + 3 * o, &x0, &y0, &fp);
+        int invalid = !(xs >= 0.0 && xs <= (double)(W - 1) && ys >= 0.0 && ys <= (double)(H - 1));
+        uint8_t m = 0;
+        if (invalid) {
+          m = 2;
+        } else {
+          int64_t f = (int64_t)y0 * W + x0;
+          if (((fp & 1) && M[f]) || ((fp & 2) && M[f + 1]) || ((fp & 4) && M[f + W]) ||
+              ((fp & 8) && M[f + W + 1]))
+            m = 1;
+        }
+        mask_out[o] = m;
+      }
+  }
+}
+
+void or_unwarp(const uint8_t* rgb_aligned, const uint8_t* rgb_orig, const uint8_t* occ_orig, int W,
+               int H, int T, const double* fwd, uint8_t* out) {
+#pragma omp parallel for
+  for (int t = 0; t < T; ++t) {
+    const double* q = fwd + 6 * t;
+    const uint8_t* F = rgb_aligned + 3 * (int64_t)t * W * H;
+    for (int y = 0; y < H; ++y)
+      for (int x = 0; x < W; ++x) {
+        int64_t o = ((int64_t)t * H + y) * W + x;
+        if (!occ_orig[o]) {
+          out[3 * o] = rgb_orig[3 * o]; out[3 * o + 1] = rgb_orig[3 * o + 1];
+          out[3 * o + 2] = rgb_orig[3 * o + 2];
+          continue;
+        }
+        double xs = (q[0] + q[1] * (double)x) + q[2] * (double)y;
+        double ys = (q[3] + q[4] * (double)x) + q[5] * (double)y;
+        int x0, y0, fp;
+        sample_rgb(F, W, H, xs, ys, out + 3 * o, &x0, &y0, &fp);
+      }
+  }
 }

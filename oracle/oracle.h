@@ -98,7 +98,37 @@ int64_t or_ambiguity_mc(int N, double sigma, uint64_t seed, uint64_t trial0, uin
 int64_t or_ann_search_sequential(const or_level* lv, or_nnf* nnf, int lambda, uint64_t seed,
                                  double rho, int rmax, int level, uint32_t outer_code, int K);
 
-/* Whole Alg. 4 (without alignment) on host buffers; returns 0 on success. */
+/* a2 with the realignment's invalid set X (R40): D~ = {p : N_p inside Omega, N_p  disjoint from
+ * H and X}; H~ as or_sets.  inv may be NULL (= or_sets). */
+void or_sets_x(const uint8_t* occ, const uint8_t* inv, int W, int H, int T, uint8_t* src,
+               uint8_t* tgt);
+/* any-of-2x2 decimation of a 0/1 mask (R18; used for X) */
+void or_mask_down(const uint8_t* m, int W, int H, int T, uint8_t* mc);
+
+/* ---- NEXT #1: dominant affine motion and realignment (Alg. 2; S3.4 P:744-758) ----
+ * theta = (a1..a6): (x, y) -> (a1 + a2 x + a3 y, a4 + a5 x + a6 y), full-resolution pixel
+ * coordinates (x = column, y = row), theta_{n,n+1} maps frame n to frame n+1:
+ * I_{n+1}(theta(x)) ~ I_n(x).  Readings R36-R40. */
+void or_affine_compose(const double* t2, const double* t1, double* out); /* t2 o t1 */
+int or_affine_invert(const double* t, double* out);                     /* 0 ok, 1 singular */
+/* Robust IRLS estimate between two frames (R36-R38); occ_a excludes pixels of frame a, occ_b
+ * the footprints in frame b (NULL = none).  Returns 0, or 1 = degenerate (theta = identity).
+ * iters_out (may be NULL) = total IRLS iterations over all levels. */
+int or_affine_estimate(const uint8_t* rgb_a, const uint8_t* rgb_b, const uint8_t* occ_a,
+                       const uint8_t* occ_b, int W, int H, int levels, int max_iter, double tol,
+                       double* theta, int* iters_out);
+/* theta_{n,Nm} for every frame (Alg. 2 second loop, R39) and its inverse; 0 ok, 1 singular */
+int or_affine_chain(const double* pairs, int T, double* fwd, double* inv);
+/* aligned frame n = u_n sampled bilinearly at inv[n](y) (R40); mask_out: 0, 1 = occluded (any
+ * nonzero-weight footprint pixel occluded), 2 = invalid (source outside frame n) */
+void or_align_warp(const uint8_t* rgb, const uint8_t* occ, int W, int H, int T, const double* inv,
+                   uint8_t* rgb_out, uint8_t* mask_out);
+/* inverse warp of the inpainted aligned video, pasted into the original occluded pixels only */
+void or_unwarp(const uint8_t* rgb_aligned, const uint8_t* rgb_orig, const uint8_t* occ_orig, int W,
+               int H, int T, const double* fwd, uint8_t* out);
+
+/* Whole Alg. 4 on host buffers; occ codes 0 known, 1 occluded (H), 2 invalid (X, R40, only
+ * after realignment).  Returns 0 on success. */
 typedef struct {
   int levels, pm_iters, fixed_outer, max_outer, lambda, tex_half, n_steps, sign_policy;
   int steps[8];

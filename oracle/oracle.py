@@ -22,7 +22,7 @@ def build(force: bool = False) -> str:
     src = os.path.join(_HERE, "oracle.c")
     if force or not os.path.exists(_LIB_PATH) or os.path.getmtime(_LIB_PATH) < max(
             os.path.getmtime(src), os.path.getmtime(os.path.join(_HERE, "oracle.h"))):
-        cmd = f"gcc -O2 -std=c11 -fopenmp -fPIC -shared -o {_LIB_PATH} {src} -lm"
+        cmd = f"gcc -O2 -std=c11 -ffp-contract=off -fopenmp -fPIC -shared -o {_LIB_PATH} {src} -lm"
         if os.system(cmd) != 0:
             raise RuntimeError("oracle build failed: " + cmd)
     return _LIB_PATH
@@ -83,6 +83,14 @@ def lib():
             "or_ambiguity_exact": (D, [I]),
             "or_ann_search_sequential": (I64, [P, P, I, U64, D, I, I, C.c_uint32, I]),
             "or_ambiguity_mc": (I64, [I, D, U64, U64, U64]),
+            "or_sets_x": (None, [P, P, I, I, I, P, P]),
+            "or_mask_down": (None, [P, I, I, I, P]),
+            "or_affine_compose": (None, [P, P, P]),
+            "or_affine_invert": (I, [P, P]),
+            "or_affine_estimate": (I, [P, P, P, P, I, I, I, I, D, P, P]),
+            "or_affine_chain": (I, [P, I, P, P]),
+            "or_align_warp": (None, [P, P, I, I, I, P, P, P]),
+            "or_unwarp": (None, [P, P, P, I, I, I, P, P]),
         }
         for name, (res, args) in sig.items():
             f = getattr(_lib, name)
@@ -107,7 +115,8 @@ def pyramid_down(rgb, occ):
     Wc, Hc = (W + 1) // 2, (H + 1) // 2
     rc = np.zeros((T, Hc, Wc, 3), np.uint8)
     oc = np.zeros((T, Hc, Wc), np.uint8)
-    lib().or_pyramid_down(_p(np.ascontiguousarray(rgb)), _p(np.ascontiguousarray(occ)), W, H, T,
+    rgb, occ = np.ascontiguousarray(rgb), np.ascontiguousarray(occ)  # keep alive across the call
+    lib().or_pyramid_down(_p(rgb), _p(occ), W, H, T,
                           _p(rc), _p(oc))
     return rc, oc
 
@@ -115,7 +124,8 @@ def pyramid_down(rgb, occ):
 def texture(rgb, occ, h):
     T, H, W, _ = rgb.shape
     tex = np.zeros((T, H, W, 2), np.uint8)
-    lib().or_texture(_p(np.ascontiguousarray(rgb)), _p(np.ascontiguousarray(occ)), W, H, T, h,
+    rgb, occ = np.ascontiguousarray(rgb), np.ascontiguousarray(occ)
+    lib().or_texture(_p(rgb), _p(occ), W, H, T, h,
                      _p(tex))
     return tex
 
@@ -123,7 +133,8 @@ def texture(rgb, occ, h):
 def texture_decimate(tex1, level, Wl, Hl):
     T, H1, W1, _ = tex1.shape
     out = np.zeros((T, Hl, Wl, 2), np.uint8)
-    lib().or_texture_decimate(_p(np.ascontiguousarray(tex1)), W1, H1, T, level, Wl, Hl, _p(out))
+    tex1 = np.ascontiguousarray(tex1)
+    lib().or_texture_decimate(_p(tex1), W1, H1, T, level, Wl, Hl, _p(out))
     return out
 
 
@@ -131,14 +142,16 @@ def sets(occ):
     T, H, W = occ.shape
     src = np.zeros_like(occ)
     tgt = np.zeros_like(occ)
-    lib().or_sets(_p(np.ascontiguousarray(occ)), W, H, T, _p(src), _p(tgt))
+    occ = np.ascontiguousarray(occ)
+    lib().or_sets(_p(occ), W, H, T, _p(src), _p(tgt))
     return src, tgt
 
 
 def layers(occ):
     T, H, W = occ.shape
     lay = np.zeros_like(occ)
-    n = lib().or_layers(_p(np.ascontiguousarray(occ)), W, H, T, _p(lay))
+    occ = np.ascontiguousarray(occ)
+    n = lib().or_layers(_p(occ), W, H, T, _p(lay))
     return lay, n
 
 
@@ -288,7 +301,8 @@ def inpaint(rgb, occ, levels, pm_iters=10, fixed_outer=0, max_outer=20, lam=50, 
     prm.seed, prm.rho = seed, rho
     st = OrStats()
     out = np.zeros_like(rgb)
-    rc = lib().or_inpaint(_p(np.ascontiguousarray(rgb)), _p(np.ascontiguousarray(occ)), W, H, T,
+    rgb, occ = np.ascontiguousarray(rgb), np.ascontiguousarray(occ)
+    rc = lib().or_inpaint(_p(rgb), _p(occ), W, H, T,
                           C.byref(prm), _p(out), C.byref(st))
     if rc != 0:
         raise RuntimeError(f"or_inpaint failed: {rc}")
@@ -310,3 +324,89 @@ def ann_search_sequential(lv, nnf, lam, seed, level, outer_code, K, rho=0.5, rma
     rmax = lv.rmax if rmax is None else rmax
     return lib().or_ann_search_sequential(lv.struct(), nnf.struct(), lam, seed, rho, rmax, level,
                                           outer_code, K)
+
+
+# ---- NEXT #1: affine realignment (Alg. 2; R36-R40) --------------------------------------------
+IDENTITY = (0.0, 1.0, 0.0, 0.0, 0.0, 1.0)
+
+
+def _th(t):
+    return np.ascontiguousarray(np.asarray(t, dtype=np.float64).reshape(-1))
+
+
+def sets_x(occ, inv):
+    T, H, W = occ.shape
+    src = np.zeros_like(occ)
+    tgt = np.zeros_like(occ)
+    keep = [np.ascontiguousarray(occ), None if inv is None else np.ascontiguousarray(inv)]
+    lib().or_sets_x(_p(keep[0]), _p(keep[1]), W, H, T, _p(src), _p(tgt))
+    return src, tgt
+
+
+def affine_compose(t2, t1):
+    out = np.zeros(6)
+    a, b = _th(t2), _th(t1)
+    lib().or_affine_compose(_p(a), _p(b), _p(out))
+    return out
+
+
+def affine_invert(t):
+    out = np.zeros(6)
+    a = _th(t)
+    if lib().or_affine_invert(_p(a), _p(out)):
+        raise ValueError("singular affine map")
+    return out
+
+
+def affine_estimate(rgb_a, rgb_b, occ_a=None, occ_b=None, levels=3, max_iter=20, tol=1e-4):
+    """theta_{a->b} (6 doubles, spec form), status (0 ok / 1 degenerate), total IRLS iterations."""
+    H, W, _ = rgb_a.shape
+    th = np.zeros(6)
+    it = np.zeros(1, np.int32)
+    ca = lambda a: None if a is None else np.ascontiguousarray(a, np.uint8)
+    keep = [np.ascontiguousarray(rgb_a), np.ascontiguousarray(rgb_b), ca(occ_a), ca(occ_b)]
+    st = lib().or_affine_estimate(*[_p(k) for k in keep], W, H, levels, max_iter, tol, _p(th), _p(it))
+    return th, int(st), int(it[0])
+
+
+def affine_chain(pairs, T):
+    pairs = np.ascontiguousarray(np.asarray(pairs, np.float64).reshape(max(T - 1, 1), 6))
+    fwd = np.zeros((T, 6))
+    inv = np.zeros((T, 6))
+    if lib().or_affine_chain(_p(pairs), T, _p(fwd), _p(inv)):
+        raise ValueError("singular affine chain")
+    return fwd, inv
+
+
+def align_warp(rgb, occ, inv):
+    T, H, W, _ = rgb.shape
+    out = np.zeros_like(rgb)
+    mo = np.zeros((T, H, W), np.uint8)
+    keep = [np.ascontiguousarray(rgb), np.ascontiguousarray(occ), np.ascontiguousarray(inv, np.float64)]
+    lib().or_align_warp(_p(keep[0]), _p(keep[1]), W, H, T, _p(keep[2]), _p(out), _p(mo))
+    return out, mo
+
+
+def unwarp(rgb_aligned, rgb_orig, occ_orig, fwd):
+    T, H, W, _ = rgb_orig.shape
+    out = np.zeros_like(rgb_orig)
+    keep = [np.ascontiguousarray(rgb_aligned), np.ascontiguousarray(rgb_orig),
+            np.ascontiguousarray(occ_orig), np.ascontiguousarray(fwd, np.float64)]
+    lib().or_unwarp(_p(keep[0]), _p(keep[1]), _p(keep[2]), W, H, T, _p(keep[3]), _p(out))
+    return out
+
+
+def align_pipeline(rgb, occ, levels=3, max_iter=20, tol=1e-4):
+    """Alg. 2 on the host: pairwise estimates, chain, warp.  Returns (aligned rgb, aligned mask
+    codes, fwd, inv, pair thetas, statuses)."""
+    T = rgb.shape[0]
+    pairs = np.zeros((max(T - 1, 1), 6))
+    pairs[:] = IDENTITY
+    stats = []
+    for n in range(T - 1):
+        th, st, _ = affine_estimate(rgb[n], rgb[n + 1], occ[n], occ[n + 1], levels, max_iter, tol)
+        pairs[n] = th
+        stats.append(st)
+    fwd, inv = affine_chain(pairs, T)
+    ar, am = align_warp(rgb, occ, inv)
+    return ar, am, fwd, inv, pairs[:T - 1], stats
