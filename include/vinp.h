@@ -23,7 +23,8 @@
  *  - vox   u64 [T][H][W]: bits 0-7 R, 8-15 G, 16-23 B (working copy u), bits 32-39 T_x,
  *          40-47 T_y in half-grey-level units (T_q = round(2T), Eq. 8, R24); rest 0.
  *  - flags u8  [T][H][W]: bit0 = p in H (occlusion), bit1 = p in D~ (valid source
- *          centre), bit2 = p in H~ (target).
+ *          centre), bit2 = p in H~ (target), bit3 = p in X (invalid: outside
+ *          the realigned field of view, NEXT #1 only, R40).
  *  - layer u8  [T][H][W]: onion layer = L_inf distance to D (Alg. 3, R22); coarsest level only,
  *          else NULL.
  *  - slot  i32 [T][H][W]: voxel -> index in `targets`, or -1.
@@ -88,10 +89,13 @@ int vinp_version(void);
 uint64_t vinp_launch_count(void);
 
 /* ---- a1: video + occlusion pyramid (Alg. 4; spatial only P:878-882; R17/R18) ----
- * rgb: u8 [T][H][W][3] and mask: u8 [T][H][W] (nonzero = occluded), device, level-1 dims.
- * Writes vox colour bytes and flags bit0 of levels 1..L (lv[0..L-1]); texture bytes are zeroed.
- * Coarse value = round-half-up of the binomial (1,4,6,4,1)^2 mean over unoccluded fine voxels
- * (reflect-101 borders), 0 if none; coarse occluded iff any of its 2x2 fine voxels is. */
+ * rgb: u8 [T][H][W][3] and mask: u8 [T][H][W], device, level-1 dims.  Mask codes: 0 known,
+ * 2 = invalid X (a realigned pixel whose source lies outside its frame, R40; a known voxel that
+ * no source patch may contain), any other nonzero = occluded (H).
+ * Writes vox colour bytes and flags bits 0 and 3 of levels 1..L (lv[0..L-1]); texture bytes are
+ * zeroed.  Coarse value = round-half-up of the binomial (1,4,6,4,1)^2 mean over unoccluded fine
+ * voxels (reflect-101 borders), 0 if none; coarse occluded (invalid) iff any of its 2x2 fine
+ * voxels is. */
 vinp_status vinp_build_pyramid(const uint8_t* rgb, const uint8_t* mask, vinp_level* lv, int L,
                                void* stream);
 
@@ -104,7 +108,8 @@ vinp_status vinp_texture_features(const vinp_params* prm, vinp_level* lv, int L,
                                   size_t ws_bytes, void* stream);
 
 /* ---- a2: source/target sets ----
- * vinp_build_sets: flags bit1 (D~) and bit2 (H~) from bit0 for levels 1..L, and returns the
+ * vinp_build_sets: flags bit1 (D~: N_p inside Omega and disjoint from H and X) and bit2 (H~)
+ * from bits 0 and 3 for levels 1..L, and returns the
  * list sizes in counts_out[3l+0..2] = |H~|, |H|, |D~| (host memory; this call synchronises).
  * vinp_build_lists: fills targets/holes/sources (ascending) and slot for levels 1..L into
  * caller buffers sized from those counts; sets lv[l].n_*.  ws: vinp_sets_ws_bytes. */
@@ -217,6 +222,40 @@ vinp_status vinp_brute_force_tc(const vinp_level* lv, vinp_nnf* out, const vinp_
  * 4<<16 | k, 0)).  Probability estimate = hits / n_trials. */
 vinp_status vinp_patch_ambiguity(int N, double sigma, uint64_t seed, uint64_t trial0, uint64_t n_trials,
                                  unsigned long long* hits, void* stream);
+
+/* ---- NEXT #1: dominant affine motion and realignment (Alg. 2; S3.4 P:744-758) ----
+ * theta = 6 doubles (a1..a6): (x, y) -> (a1 + a2 x + a3 y, a4 + a5 x + a6 y) in full-resolution
+ * pixel coordinates (x column, y row).  All buffers device, caller-owned.
+ *
+ * vinp_affine_estimate: theta[n] (n < T-1) = theta_{n,n+1}, the dominant motion from frame n to
+ *   n+1 (I_{n+1}(theta(x)) ~ I_n(x)), by robust IRLS (R36-R38: grey pyramid of `levels` 2x2 box
+ *   levels (fewer while the coarsest side would be < 8), Tukey biweight, scale 1.4826 x exact
+ *   lower median of |r|, <= max_iter iterations per level or |dp| < tol).  Pixels with mask != 0
+ *   are excluded (in frame n as voters; in frame n+1 from every sample/gradient footprint).
+ *   status[n] = 0, or 1 = degenerate (fewer than 12 voters or singular normal equations), in
+ *   which case theta[n] = identity; iters[n] = IRLS iterations run.  Deterministic and
+ *   bit-identical to the oracle (exact fixed-point sums, no FMA contraction).  One CTA per pair.
+ *   ws: vinp_affine_ws_bytes(W, H, T, levels) (grey pyramids + |r| keys).
+ * vinp_affine_chain: fwd[n] = theta_{n,N_m} (frame n -> reference frame N_m = max(T/2 - 1, 0),
+ *   0-based, R39) by the products of Alg. 2, inv[n] = fwd[n]^-1; *err (device) = 1 if a map
+ *   was singular.  One thread (the chain is sequential by definition).
+ * vinp_align_warp: aligned frame n at reference pixel y = frame n sampled bilinearly at inv[n](y)
+ *   (clamp-to-edge, rounded half up to u8); mask_out = 2 where inv[n](y) falls outside frame n,
+ *   else 1 iff a nonzero-weight footprint pixel is occluded (mask != 0), else 0 (R40).
+ * vinp_unwarp: out = rgb_orig where mask_orig == 0; inside the original occlusion, the inpainted
+ *   aligned video sampled bilinearly at fwd[n](x) (clamp-to-edge, rounded half up) (R40). */
+size_t vinp_affine_ws_bytes(int W, int H, int T, int levels);
+vinp_status vinp_affine_estimate(const uint8_t* rgb, const uint8_t* mask, int W, int H, int T, int levels,
+                                 int max_iter, double tol, double* theta, int32_t* status, int32_t* iters,
+                                 void* ws, size_t ws_bytes, void* stream);
+vinp_status vinp_affine_chain(const double* pairs, int T, double* fwd, double* inv, int32_t* err,
+                              void* stream);
+vinp_status vinp_align_warp(const uint8_t* rgb, const uint8_t* mask, int W, int H, int T, const double* inv,
+                            uint8_t* rgb_out, uint8_t* mask_out, void* stream);
+vinp_status vinp_unwarp(const uint8_t* rgb_aligned, const uint8_t* rgb_orig, const uint8_t* mask_orig, int W,
+                        int H, int T, const double* fwd, uint8_t* out, void* stream);
+/* Final video of level 1: out[p] = the RGB bytes of vox[p] (input outside H, inpainted inside). */
+vinp_status vinp_output_rgb(const vinp_level* lv1, uint8_t* out, void* stream);
 
 /* ---- test hooks ----
  * vinp_patch_ssd: D and n of pairs (p[i], q[i]) with known set kb (q must be in D~).

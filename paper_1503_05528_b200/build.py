@@ -14,6 +14,9 @@ ARCH = ["-gencode", "arch=compute_100a,code=sm_100a"]
 FLAGS = ["-O3", "-lineinfo", "-std=c++17", "-Xcompiler", "-fPIC", "-Xptxas", "-v",
          "--expt-relaxed-constexpr"]
 
+# align.cu: fp64 expressions evaluated as written (no FMA contraction), like the oracle (R38)
+PER_FILE = {"align.cu": ["-fmad=false"]}
+
 
 def sources():
     return sorted(glob.glob(os.path.join(HERE, "csrc", "*.cu")))
@@ -37,7 +40,8 @@ def build(force: bool = False, verbose: bool = False, defines=(), out=None) -> s
     for src in sources():
         tag = "" if not defines else "_" + os.path.basename(lib)[:-3]
         obj = os.path.join(HERE, "csrc", os.path.basename(src)[:-3] + tag + ".o")
-        cmd = [NVCC, *ARCH, *FLAGS, *["-D" + d for d in defines], "-I", os.path.join(ROOT, "include"),
+        extra = PER_FILE.get(os.path.basename(src), [])
+        cmd = [NVCC, *ARCH, *FLAGS, *extra, *["-D" + d for d in defines], "-I", os.path.join(ROOT, "include"),
                "-c", src, "-o", obj]
         r = subprocess.run(cmd, capture_output=True, text=True)
         log.append(r.stderr)

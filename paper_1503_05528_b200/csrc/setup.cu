@@ -38,7 +38,8 @@ __global__ void k_level1(const uint8_t* __restrict__ rgb, const uint8_t* __restr
   uint32_t c = (uint32_t)rgb[3 * (int64_t)i] | ((uint32_t)rgb[3 * (int64_t)i + 1] << 8) |
                ((uint32_t)rgb[3 * (int64_t)i + 2] << 16);
   vox[i] = c;
-  flags[i] = mask[i] ? 1 : 0;
+  uint8_t m = mask[i];
+  flags[i] = m == 2 ? 8 : (m ? 1 : 0);  // 2 = invalid X (R40), other nonzero = H
 }
 
 __device__ __forceinline__ int refl101(int i, int n) {
@@ -83,11 +84,20 @@ __global__ void k_pyramid_down(const uint64_t* __restrict__ fv, const uint8_t* _
   for (int dy = 0; dy < 2; ++dy)
     for (int dx = 0; dx < 2; ++dx) {
       int fx = 2 * X + dx, fy = 2 * Y + dy;
-      if (fx < W && fy < H && (ff[base + (int64_t)fy * W + fx] & 1)) any = 1;
+      if (fx < W && fy < H) any |= ff[base + (int64_t)fy * W + fx] & 9;  // H and X: any-of 2x2
     }
   int64_t o = ((int64_t)t * Hc + Y) * Wc + X;
   cv[o] = out;
   cf[o] = (uint8_t)any;
+}
+
+__global__ void k_output_rgb(const uint64_t* __restrict__ vox, int64_t N, uint8_t* __restrict__ out) {
+  int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (i >= N) return;
+  uint32_t c = (uint32_t)vox[i];
+  out[3 * i] = (uint8_t)c;
+  out[3 * i + 1] = (uint8_t)(c >> 8);
+  out[3 * i + 2] = (uint8_t)(c >> 16);
 }
 
 // ------------------------------------------------------------------ a3: texture features
@@ -175,7 +185,7 @@ __global__ void k_sets_pass(const uint8_t* __restrict__ in, uint8_t* __restrict_
       int cc = c + d;
       if (cc < 0 || cc >= n) { a = 0; continue; }
       uint8_t v = in[o + d * stride];
-      int va = FIRST ? !(v & 1) : (v & 1);
+      int va = FIRST ? !(v & 9) : (v & 1);  // D~ seed: neither H nor X
       int vb = FIRST ? (v & 1) : ((v >> 1) & 1);
       a &= va;
       b |= vb;
@@ -183,7 +193,7 @@ __global__ void k_sets_pass(const uint8_t* __restrict__ in, uint8_t* __restrict_
   }
   if (LAST) {
     // out is flags: keep bit0 (H), set bit1 = D~, bit2 = H~
-    if (ok) out[o] = (uint8_t)((out[o] & 1) | (a << 1) | (b << 2));
+    if (ok) out[o] = (uint8_t)((out[o] & 9) | (a << 1) | (b << 2));
     int ch = __syncthreads_count(ok && b), cho = __syncthreads_count(ok && a);
     int hh = __syncthreads_count(ok && (out[o] & 1));
     if (threadIdx.x == 0 && threadIdx.y == 0) {
@@ -370,6 +380,16 @@ vinp_status vinp_build_pyramid(const uint8_t* rgb, const uint8_t* mask, vinp_lev
     count_launch();
   }
   return check_launch("vinp_build_pyramid");
+}
+
+vinp_status vinp_output_rgb(const vinp_level* lv1, uint8_t* out, void* stream) {
+  vinp_status st = check_level(lv1, "vinp_output_rgb");
+  if (st) return st;
+  VINP_REQUIRE(out, "vinp_output_rgb: null output");
+  int64_t N = (int64_t)lv1->W * lv1->H * lv1->T;
+  k_output_rgb<<<nblk(N, 256), 256, 0, S(stream)>>>(lv1->vox, N, out);
+  count_launch();
+  return check_launch("vinp_output_rgb");
 }
 
 size_t vinp_texture_ws_bytes(const vinp_level* lv1) {

@@ -35,6 +35,10 @@ class Config:
     rho: float = 0.5
     tex_half: int = -1          # R15
     onion: bool = True          # Alg. 3 initialisation at the coarsest level
+    align: bool = False         # NEXT #1: Alg. 2 realignment before, unwarp after
+    align_levels: int = 3       # R36: estimation pyramid levels
+    align_iters: int = 20       # R38: IRLS iterations per level
+    align_tol: float = 1e-4     # R38: update-norm stop
 
     def params(self) -> V.Params:
         return V.Params(lam=self.lam, tex_half=self.tex_half, seed=self.seed, rho=self.rho)
@@ -126,7 +130,8 @@ class Inpainter:
 
     # ------------------------------------------------------------------ setup (a1-a3)
     def load(self, rgb: torch.Tensor, mask: torch.Tensor):
-        """rgb u8 [T,H,W,3], mask u8 [T,H,W] (nonzero = occluded), on this device."""
+        """rgb u8 [T,H,W,3], mask u8 [T,H,W] (0 known, 2 invalid X after realignment, other
+        nonzero = occluded), on this device."""
         assert rgb.shape == (self.T, self.H, self.W, 3) and mask.shape == (self.T, self.H, self.W)
         rgb = rgb.contiguous()
         mask = mask.contiguous()
@@ -287,9 +292,30 @@ class Inpainter:
     def output(self, rgb_in: torch.Tensor) -> torch.Tensor:
         """Final video: input outside H, the best-patch u8 values inside H (device tensor)."""
         lv = self.levels[0]
+        if hasattr(self.V, "output_rgb"):  # the colour bytes of vox are exactly that video
+            return self.V.output_rgb(lv)
         vb = lv.vox.view(torch.uint8).view(self.T, self.H, self.W, 8)[..., :3]
         m = (lv.flags.view(self.T, self.H, self.W) & 1).bool()
         return torch.where(m[..., None], vb, rgb_in)
+
+    # ------------------------------------------------------------------ NEXT #1 (Alg. 2)
+    def align(self, rgb: torch.Tensor, mask: torch.Tensor):
+        """Alg. 2: theta_{n,n+1} by robust IRLS, the chain to the middle frame, bilinear warp of
+        the video and its occlusion (mask codes 0 / 1 / 2 = invalid, R40).  Device tensors."""
+        c = self.cfg
+        if getattr(self, "_align_ws", None) is None:
+            self._align_ws = torch.empty(max(self.V.affine_ws_bytes(self.W, self.H, self.T, c.align_levels), 1),
+                                         dtype=torch.uint8, device=self.device)
+            self._align_out = (torch.empty_like(rgb), torch.empty_like(mask))
+        theta, status, iters = self.V.affine_estimate(rgb, mask, c.align_levels, c.align_iters, c.align_tol,
+                                                      ws=self._align_ws)
+        fwd, inv, err = self.V.affine_chain(theta, self.T)
+        self.align_info = dict(theta=theta, status=status, iters=iters, fwd=fwd, inv=inv, err=err)
+        return self.V.align_warp(rgb, mask, inv, out=self._align_out)
+
+    def unwarp(self, aligned_out: torch.Tensor, rgb: torch.Tensor, mask: torch.Tensor) -> torch.Tensor:
+        """Inverse warp of the inpainted aligned video, pasted into the original occlusion (R40)."""
+        return self.V.unwarp(aligned_out, rgb, mask, self.align_info["fwd"])
 
 
 _PLANS = {}
@@ -306,6 +332,11 @@ def inpaint(rgb: torch.Tensor, mask: torch.Tensor, cfg: Config, device="cuda", e
         ip = _PLANS[key] = Inpainter(W, H, T, cfg, device, exchange, ops)
     rgb_d = rgb.to(device, non_blocking=True)
     mask_d = mask.to(device, non_blocking=True)
+    if cfg.align:
+        a_rgb, a_mask = ip.align(rgb_d, mask_d)
+        ip.load(a_rgb, a_mask)
+        stats = ip.run()
+        return ip.unwarp(ip.output(a_rgb), rgb_d, mask_d), stats, ip
     ip.load(rgb_d, mask_d)
     stats = ip.run()
     return ip.output(rgb_d), stats, ip

@@ -80,6 +80,12 @@ def _load():
         "vinp_philox": (I, [P, I64, U64, P, P]),
         "vinp_tc_gemm_u8": (I, [P, P, I, P, P]),
         "vinp_patch_ambiguity": (I, [I, C.c_double, U64, U64, U64, P, P]),
+        "vinp_affine_ws_bytes": (C.c_size_t, [I, I, I, I]),
+        "vinp_affine_estimate": (I, [P, P, I, I, I, I, I, C.c_double, P, P, P, P, C.c_size_t, P]),
+        "vinp_affine_chain": (I, [P, I, P, P, P, P]),
+        "vinp_align_warp": (I, [P, P, I, I, I, P, P, P, P]),
+        "vinp_unwarp": (I, [P, P, P, I, I, I, P, P, P]),
+        "vinp_output_rgb": (I, [P, P, P]),
     }
     for name, (res, args) in sigs.items():
         f = getattr(lib, name)
@@ -97,7 +103,9 @@ EXPORTED = [
     "vinp_onion_ws_bytes", "vinp_onion_peel",
     "vinp_reconstruct", "vinp_commit", "vinp_change_l1", "vinp_energy",
     "vinp_brute_force_ws_bytes", "vinp_brute_force", "vinp_patch_ssd", "vinp_philox",
-    "vinp_tc_gemm_u8", "vinp_patch_ambiguity", "vinp_brute_force_list", "vinp_brute_force_tc_ws_bytes", "vinp_brute_force_tc"]
+    "vinp_tc_gemm_u8", "vinp_patch_ambiguity", "vinp_brute_force_list", "vinp_brute_force_tc_ws_bytes", "vinp_brute_force_tc",
+    "vinp_affine_ws_bytes", "vinp_affine_estimate", "vinp_affine_chain", "vinp_align_warp", "vinp_unwarp",
+    "vinp_output_rgb"]
 
 
 def _check(rc: int, what: str):
@@ -387,3 +395,68 @@ def patch_ambiguity(N: int, n_trials: int, sigma=5.0, seed=1, trial0=0, hits=Non
     _check(_lib.vinp_patch_ambiguity(N, sigma, seed, trial0, n_trials, _ptr(hits), _stream()),
            "vinp_patch_ambiguity")
     return hits
+
+
+# ---- NEXT #1: affine realignment (Alg. 2; R36-R40) -----------------------------------------------
+def affine_ws_bytes(W: int, H: int, T: int, levels: int = 3) -> int:
+    return int(_lib.vinp_affine_ws_bytes(W, H, T, levels))
+
+
+def affine_estimate(rgb: torch.Tensor, mask: torch.Tensor, levels=3, max_iter=20, tol=1e-4, ws=None,
+                    out=None):
+    """theta_{n,n+1} for every consecutive frame pair: (theta f64 [T-1, 6], status i32 [T-1],
+    iters i32 [T-1]), device tensors.  rgb u8 [T, H, W, 3], mask u8 [T, H, W] on the device."""
+    T, H, W, _ = rgb.shape
+    dev = rgb.device
+    nb = affine_ws_bytes(W, H, T, levels)
+    if ws is None or ws.numel() < nb:
+        ws = torch.empty(max(nb, 1), dtype=torch.uint8, device=dev)
+    npairs = max(T - 1, 1)
+    if out is None:
+        out = (torch.empty((npairs, 6), dtype=torch.float64, device=dev),
+               torch.zeros(npairs, dtype=torch.int32, device=dev),
+               torch.zeros(npairs, dtype=torch.int32, device=dev))
+    theta, status, iters = out
+    _check(_lib.vinp_affine_estimate(_ptr(rgb), _ptr(mask), W, H, T, levels, max_iter, tol, _ptr(theta),
+                                     _ptr(status), _ptr(iters), _ptr(ws), ws.numel(), _stream()),
+           "vinp_affine_estimate")
+    return theta[:T - 1], status[:T - 1], iters[:T - 1]
+
+
+def affine_chain(pairs: torch.Tensor, T: int, out=None):
+    """(fwd, inv) f64 [T, 6] on the device: theta_{n,N_m} and its inverse (R39)."""
+    dev = pairs.device
+    if out is None:
+        out = (torch.empty((T, 6), dtype=torch.float64, device=dev),
+               torch.empty((T, 6), dtype=torch.float64, device=dev),
+               torch.zeros(1, dtype=torch.int32, device=dev))
+    fwd, inv, err = out
+    p = pairs.contiguous() if pairs.numel() else None
+    _check(_lib.vinp_affine_chain(_ptr(p), T, _ptr(fwd), _ptr(inv), _ptr(err), _stream()), "vinp_affine_chain")
+    return fwd, inv, err
+
+
+def align_warp(rgb: torch.Tensor, mask: torch.Tensor, inv: torch.Tensor, out=None):
+    T, H, W, _ = rgb.shape
+    if out is None:
+        out = (torch.empty_like(rgb), torch.empty_like(mask))
+    ro, mo = out
+    _check(_lib.vinp_align_warp(_ptr(rgb), _ptr(mask), W, H, T, _ptr(inv), _ptr(ro), _ptr(mo), _stream()),
+           "vinp_align_warp")
+    return ro, mo
+
+
+def unwarp(rgb_aligned: torch.Tensor, rgb_orig: torch.Tensor, mask_orig: torch.Tensor, fwd: torch.Tensor,
+           out=None):
+    T, H, W, _ = rgb_orig.shape
+    out = torch.empty_like(rgb_orig) if out is None else out
+    _check(_lib.vinp_unwarp(_ptr(rgb_aligned), _ptr(rgb_orig), _ptr(mask_orig), W, H, T, _ptr(fwd), _ptr(out),
+                            _stream()), "vinp_unwarp")
+    return out
+
+
+def output_rgb(lv1: Level, out: Optional[torch.Tensor] = None):
+    if out is None:
+        out = torch.empty((lv1.T, lv1.H, lv1.W, 3), dtype=torch.uint8, device=lv1.vox.device)
+    _check(_lib.vinp_output_rgb(lv1.struct(), _ptr(out), _stream()), "vinp_output_rgb")
+    return out
