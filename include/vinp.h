@@ -234,7 +234,7 @@ vinp_status vinp_patch_ambiguity(int N, double sigma, uint64_t seed, uint64_t tr
  *   are excluded (in frame n as voters; in frame n+1 from every sample/gradient footprint).
  *   status[n] = 0, or 1 = degenerate (fewer than 12 voters or singular normal equations), in
  *   which case theta[n] = identity; iters[n] = IRLS iterations run.  Deterministic and
- *   bit-identical to the oracle (exact fixed-point sums, no FMA contraction).  One CTA per pair.
+ *   bit-identical to the oracle (exact fixed-point sums, no FMA contraction).  One 8-CTA cluster per pair.
  *   ws: vinp_affine_ws_bytes(W, H, T, levels) (grey pyramids + |r| keys).
  * vinp_affine_chain: fwd[n] = theta_{n,N_m} (frame n -> reference frame N_m = max(T/2 - 1, 0),
  *   0-based, R39) by the products of Alg. 2, inv[n] = fwd[n]^-1; *err (device) = 1 if a map

@@ -4,8 +4,10 @@
 // (int64 of llrint(term * 2^16)), so the result is independent of the thread/block decomposition.
 //
 //   k_grey0 / k_grey_down  grey-level estimation pyramid of every frame (R36)
-//   k_irls                 one CTA per frame pair (n, n+1): coarse-to-fine IRLS with exact
-//                          radix-select median of |r| and in-CTA 6x6 solve (R37, R38)
+//   k_irls                 one 8-CTA cluster per frame pair (n, n+1), one launch per pyramid
+//                          level: IRLS with an exact radix-select median of |r| (11-bit digits,
+//                          histograms combined over DSMEM) and a redundant per-CTA 6x6 solve
+//                          (R37, R38)
 //   k_affine_chain         theta_{n,N_m} and inverses (R39), one thread
 //   k_align_warp           bilinear warp of every frame to the reference + mask codes (R40)
 //   k_unwarp               inverse warp pasted into the original occluded pixels (R40)
@@ -14,6 +16,9 @@
 namespace vinp {
 namespace {
 
+#ifndef VINP_IRLS_MINB
+#define VINP_IRLS_MINB 2
+#endif
 constexpr int kIrlsThreads = 512;
 constexpr int kIrlsWarps = kIrlsThreads / 32;
 
@@ -58,9 +63,10 @@ struct Pix {
 };
 
 // R37: a pixel of frame a votes iff unoccluded, its warp lands in [0, W-1] x [0, H-1], and no
-// pixel the bilinear sample or its gradient reads in frame b (4x4 block, clamped) is occluded.
+// pixel the bilinear sample or its gradient reads in frame b (4x4 block x0-1..x0+2, y0-1..y0+2,
+// clamped) is occluded.  Db = that 4x4 dilation of frame b's mask, precomputed (k_mask_dil).
 __device__ __forceinline__ bool irls_pixel(const double* Ia, const uint8_t* Ma, const double* Ib,
-                                           const uint8_t* Mb, int W, int H, const double* p, double cx,
+                                           const uint8_t* Db, int W, int H, const double* p, double cx,
                                            double cy, double s, int i, int j, Pix& o) {
   if (Ma[(int64_t)j * W + i]) return false;
   double X = ((double)i - cx) / s, Y = ((double)j - cy) / s;
@@ -70,13 +76,7 @@ __device__ __forceinline__ bool irls_pixel(const double* Ia, const uint8_t* Ma, 
   int x0 = (int)floor(xw), y0 = (int)floor(yw);
   if (x0 > W - 2) x0 = W - 2;
   if (y0 > H - 2) y0 = H - 2;
-  for (int yy = y0 - 1; yy <= y0 + 2; ++yy) {
-    int cy_ = yy < 0 ? 0 : (yy > H - 1 ? H - 1 : yy);
-    for (int xx = x0 - 1; xx <= x0 + 2; ++xx) {
-      int cx_ = xx < 0 ? 0 : (xx > W - 1 ? W - 1 : xx);
-      if (Mb[(int64_t)cy_ * W + cx_]) return false;
-    }
-  }
+  if (Db[(int64_t)y0 * W + x0]) return false;
   o.fx = xw - (double)x0;
   o.fy = yw - (double)y0;
   o.r = bil(Ib, W, x0, y0, o.fx, o.fy) - Ia[(int64_t)j * W + i];
@@ -85,6 +85,22 @@ __device__ __forceinline__ bool irls_pixel(const double* Ia, const uint8_t* Ma, 
   o.X = X;
   o.Y = Y;
   return true;
+}
+
+// Db(x, y) = OR of M over columns x-1..x+2 and rows y-1..y+2 (clamped), every frame of a level
+__global__ void k_mask_dil(const uint8_t* __restrict__ M, uint8_t* __restrict__ D, int W, int H) {
+  int x = blockIdx.x * blockDim.x + threadIdx.x, y = blockIdx.y, t = blockIdx.z;
+  if (x >= W) return;
+  const uint8_t* F = M + (int64_t)t * W * H;
+  uint8_t any = 0;
+  for (int yy = y - 1; yy <= y + 2; ++yy) {
+    int cy_ = yy < 0 ? 0 : (yy > H - 1 ? H - 1 : yy);
+    for (int xx = x - 1; xx <= x + 2; ++xx) {
+      int cx_ = xx < 0 ? 0 : (xx > W - 1 ? W - 1 : xx);
+      any |= F[(int64_t)cy_ * W + cx_];
+    }
+  }
+  D[(int64_t)t * W * H + (int64_t)y * W + x] = any;
 }
 
 __device__ int solve6(double M[6][7], double* x) {
@@ -124,37 +140,108 @@ __device__ __forceinline__ long long warp_sum_ll(long long v) {
 struct IrlsLevel {
   const double* I;   // [T][W*H]
   const uint8_t* M;  // [T][W*H]
+  const uint8_t* D;  // [T][W*H] 4x4 dilation of M
   int W, H;
   double* p;         // [npairs][6] parameter vectors (R37)
   int* status;       // [npairs] 0 / 1 degenerate
   int* iters;        // [npairs] running IRLS iteration count
-  uint64_t* keys;    // [npairs][keys_stride]
+  uint64_t* keys;    // [npairs][keys_stride] |r| keys, then the odd candidate lists
+  uint64_t* cand;    // [npairs][keys_stride] the even candidate lists
   int64_t keys_stride;
   int max_iter;
   double tol;
 };
 
-// R38, one level for pair n = blockIdx.x (frames n, n+1).
-__global__ void __launch_bounds__(kIrlsThreads) k_irls(IrlsLevel a) {
-  const int n = blockIdx.x, tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
-  if (a.status[n]) return;
+// R38, one level for pair n: a cluster of kCl CTAs (DSMEM) shares the pixels of the pair.  Every
+// cross-CTA quantity (voter count, median digits, the 27 exact sums) is combined by EVERY CTA from
+// all ranks' shared memory, so each CTA takes the same decisions and solves the same system
+// redundantly (bit-identical: integer sums, same fp64 code) — no broadcast step is needed.
+constexpr int kCl = 8;
+constexpr int kDigitBits = 11, kBins = 1 << kDigitBits;
+
+__device__ __forceinline__ void cl_sync() {
+  asm volatile("barrier.cluster.arrive.release.aligned;\n\tbarrier.cluster.wait.acquire.aligned;" ::: "memory");
+}
+__device__ __forceinline__ unsigned cl_rank() {
+  unsigned r;
+  asm volatile("mov.u32 %0, %%cluster_ctarank;" : "=r"(r));
+  return r;
+}
+// generic address of the same shared variable in CTA `rank` of the cluster
+template <typename Tp>
+__device__ __forceinline__ Tp* cl_map(Tp* p, unsigned rank) {
+  uint64_t out;
+  asm volatile("mapa.u64 %0, %1, %2;" : "=l"(out) : "l"((uint64_t)p), "r"(rank));
+  return reinterpret_cast<Tp*>(out);
+}
+
+// histogram of the digit (k >> sh) & dmask of keys with (k & hmask) == prefix: warp-aggregated
+__device__ __forceinline__ void hist_add(unsigned* hist, bool act, unsigned d, int lane) {
+  unsigned peers = __match_any_sync(kFull, act ? d : 0xffffffffu);
+  if (act && lane == __ffs(peers) - 1) atomicAdd(&hist[d], (unsigned)__popc(peers));
+}
+
+// Every CTA of the cluster picks the same digit from the summed histograms: the new prefix and
+// the rank within it.  Warp 0, 64 bins per lane.
+__device__ __forceinline__ void pick_digit(unsigned* hist, int lane, int sh, unsigned long long prefix,
+                                           unsigned rank, unsigned long long* s_prefix, unsigned* s_rank) {
+  constexpr int kPer = kBins / 32;
+  unsigned ls = 0;
+  unsigned tb[kPer];
+#pragma unroll 4
+  for (int q = 0; q < kPer; ++q) {
+    unsigned v = 0;
+    for (unsigned r = 0; r < kCl; ++r) v += cl_map(hist, r)[lane * kPer + q];
+    tb[q] = v;
+    ls += v;
+  }
+  unsigned incl = ls;
+#pragma unroll
+  for (int d = 1; d < 32; d <<= 1) {
+    unsigned y = __shfl_up_sync(kFull, incl, d);
+    if (lane >= d) incl += y;
+  }
+  unsigned excl = incl - ls;
+  int L = __ffs(__ballot_sync(kFull, rank < incl)) - 1;  // rank < total: some lane holds it
+  if (lane == L) {
+    unsigned cum = excl;
+    int q = 0;
+    for (; q < kPer - 1; ++q) {
+      if (rank < cum + tb[q]) break;
+      cum += tb[q];
+    }
+    *s_prefix = prefix | ((unsigned long long)(lane * kPer + q) << sh);
+    *s_rank = rank - cum;
+  }
+}
+
+__global__ void __cluster_dims__(kCl, 1, 1) __launch_bounds__(kIrlsThreads, VINP_IRLS_MINB) k_irls(IrlsLevel a) {
+  const int n = blockIdx.x / kCl, tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+  const unsigned rk = cl_rank();
+  if (a.status[n]) return;  // uniform over the cluster
   const int W = a.W, H = a.H;
   const int64_t NP = (int64_t)W * H;
   const double* Ia = a.I + (int64_t)n * NP;
   const double* Ib = Ia + NP;
   const uint8_t* Ma = a.M + (int64_t)n * NP;
-  const uint8_t* Mb = Ma + NP;
-  uint64_t* keys = a.keys + (int64_t)n * a.keys_stride;
+  const uint8_t* Db = a.D + (int64_t)(n + 1) * NP;
+  // this CTA's contiguous chunk of the pixels; its keys / candidate lists live in the chunk too
+  const int64_t chunk = (NP + kCl - 1) / kCl;
+  const int64_t c0 = (int64_t)rk * chunk, c1 = c0 + chunk < NP ? c0 + chunk : NP;
+  uint64_t* bufA = a.keys + (int64_t)n * a.keys_stride + c0;
+  uint64_t* bufB = a.cand + (int64_t)n * a.keys_stride + c0;
   const double cx = (double)(W - 1) * 0.5, cy = (double)(H - 1) * 0.5;
   const double s = (double)(W > H ? W : H) * 0.5;
 
   __shared__ double sp[6];
   __shared__ int s_stop, s_status;
   __shared__ unsigned s_cnt[kIrlsWarps];
-  __shared__ unsigned hist[256];
+  __shared__ unsigned s_nv, s_len;
+  __shared__ unsigned hist[kBins];
   __shared__ unsigned long long s_prefix;
   __shared__ unsigned s_rank;
   __shared__ long long red[kIrlsWarps][27];
+  __shared__ long long tot[27];
   if (tid < 6) sp[tid] = a.p[6 * n + tid];
   if (tid == 0) {
     s_stop = 0;
@@ -166,99 +253,141 @@ __global__ void __launch_bounds__(kIrlsThreads) k_irls(IrlsLevel a) {
     double p[6];
 #pragma unroll
     for (int k = 0; k < 6; ++k) p[k] = sp[k];
-    // pass 1: residual keys (bits of |r|; non-voting pixels sort last)
-    unsigned cnt = 0;
-    for (int64_t id = tid; id < NP; id += kIrlsThreads) {
-      int j = (int)(id / W), i = (int)(id - (int64_t)j * W);
-      Pix o;
-      bool ok = irls_pixel(Ia, Ma, Ib, Mb, W, H, p, cx, cy, s, i, j, o);
-      keys[id] = ok ? (uint64_t)__double_as_longlong(fabs(o.r)) : ~0ull;
-      cnt += ok;
-    }
-    cnt = __reduce_add_sync(kFull, cnt);
-    if (lane == 0) s_cnt[warp] = cnt;
+    // pass 1: residual keys (bits of |r|) of the voting pixels, compacted into bufA, with the
+    // histogram of their first (top 11-bit) digit
+    for (int b = tid; b < kBins; b += kIrlsThreads) hist[b] = 0;
+    if (tid == 0) s_len = 0;
     __syncthreads();
+    for (int64_t base = c0 + (tid & ~31); base < c1; base += kIrlsThreads) {
+      int64_t id = base + lane;
+      bool ok = false;
+      unsigned long long key = 0;
+      if (id < c1) {
+        int j = (int)(id / W), i = (int)(id - (int64_t)j * W);
+        Pix o;
+        ok = irls_pixel(Ia, Ma, Ib, Db, W, H, p, cx, cy, s, i, j, o);
+        key = (unsigned long long)__double_as_longlong(fabs(o.r));
+      }
+      unsigned bal = __ballot_sync(kFull, ok);
+      unsigned off = 0;
+      if (lane == 0 && bal) off = atomicAdd(&s_len, (unsigned)__popc(bal));
+      off = __shfl_sync(kFull, off, 0);
+      if (ok) bufA[off + __popc(bal & ((1u << lane) - 1u))] = key;
+      hist_add(hist, ok, (unsigned)(key >> (64 - kDigitBits)), lane);
+    }
+    __syncthreads();
+    if (tid == 0) s_nv = s_len;
+    cl_sync();
     unsigned nv = 0;
-    for (int w = 0; w < kIrlsWarps; ++w) nv += s_cnt[w];
+    for (unsigned r = 0; r < kCl; ++r) nv += *cl_map(&s_nv, r);
     if (nv < 12) {
       if (tid == 0) s_status = 1;
-      break;  // uniform
+      break;  // uniform over the cluster
     }
-    // exact lower median: rank (nv-1)/2 by 8-bit radix select over the 64-bit keys
+    // exact lower median: rank (nv-1)/2 by radix select over 11-bit digits (shifts 53..9, then
+    // the last 9 bits); each pass filters the previous candidate list by the chosen digit into
+    // the other buffer while histogramming the next digit
     unsigned long long prefix = 0ull;
     unsigned rank = (nv - 1) / 2;
-    for (int shift = 56; shift >= 0; shift -= 8) {
-      for (int b = tid; b < 256; b += kIrlsThreads) hist[b] = 0;
+    if (warp == 0) pick_digit(hist, lane, 64 - kDigitBits, prefix, rank, &s_prefix, &s_rank);
+    cl_sync();  // remote histogram reads done
+    prefix = s_prefix;
+    rank = s_rank;
+    unsigned len = s_len;
+    uint64_t* src = bufA;
+    uint64_t* dst = bufB;
+    for (int shift = 64 - 2 * kDigitBits; shift > -kDigitBits; shift -= kDigitBits) {
+      const int sh = shift < 0 ? 0 : shift;
+      const int width = shift < 0 ? kDigitBits + shift : kDigitBits;
+      const unsigned dmask = (1u << width) - 1u;
+      const unsigned long long hmask = ~0ull << (shift + kDigitBits);  // bits fixed by prefix
+      __syncthreads();  // everyone has read s_len / s_prefix / s_rank
+      for (int b = tid; b < kBins; b += kIrlsThreads) hist[b] = 0;
+      if (tid == 0) s_len = 0;
       __syncthreads();
-      unsigned long long hmask = shift == 56 ? 0ull : (~0ull << (shift + 8));
-      for (int64_t base = (int64_t)(tid & ~31); base < NP; base += kIrlsThreads) {
-        int64_t id = base + lane;
-        unsigned long long k = id < NP ? keys[id] : ~0ull;
-        bool act = id < NP && (k & hmask) == prefix;
-        unsigned d = act ? (unsigned)((k >> shift) & 255ull) : 256u;
-        unsigned peers = __match_any_sync(kFull, d);
-        if (act && lane == __ffs(peers) - 1) atomicAdd(&hist[d], (unsigned)__popc(peers));
+      for (unsigned base = (unsigned)(tid & ~31); base < len; base += kIrlsThreads) {
+        unsigned id = base + lane;
+        unsigned long long k = id < len ? src[id] : ~0ull;
+        bool act = id < len && (k & hmask) == prefix;
+        unsigned bal = __ballot_sync(kFull, act);
+        unsigned off = 0;
+        if (lane == 0 && bal) off = atomicAdd(&s_len, (unsigned)__popc(bal));
+        off = __shfl_sync(kFull, off, 0);
+        if (act) dst[off + __popc(bal & ((1u << lane) - 1u))] = k;
+        hist_add(hist, act, (unsigned)((k >> sh) & dmask), lane);
       }
-      __syncthreads();
-      if (tid == 0) {
-        unsigned cum = 0;
-        int d = 0;
-        for (; d < 255; ++d) {
-          if (rank < cum + hist[d]) break;
-          cum += hist[d];
-        }
-        s_prefix = prefix | ((unsigned long long)d << shift);
-        s_rank = rank - cum;
-      }
-      __syncthreads();
+      cl_sync();  // every rank's histogram and list complete
+      if (warp == 0) pick_digit(hist, lane, sh, prefix, rank, &s_prefix, &s_rank);
+      cl_sync();  // remote histogram reads done before the next pass clears them
       prefix = s_prefix;
       rank = s_rank;
+      len = s_len;
+      uint64_t* t_ = src;
+      src = dst;
+      dst = t_;
     }
     double sigma = 1.4826 * __longlong_as_double((long long)prefix);
     if (sigma < 1e-6) sigma = 1e-6;
     const double c = 4.6851 * sigma;
-    // pass 2: exact fixed-point normal equations
-    long long acc[27];
-#pragma unroll
-    for (int k = 0; k < 27; ++k) acc[k] = 0;
-    for (int64_t id = tid; id < NP; id += kIrlsThreads) {
-      int j = (int)(id / W), i = (int)(id - (int64_t)j * W);
-      Pix o;
-      if (!irls_pixel(Ia, Ma, Ib, Mb, W, H, p, cx, cy, s, i, j, o)) continue;
-      double u = o.r / c;
-      if (!(fabs(u) < 1.0)) continue;
-      double q = 1.0 - u * u;
-      double w = q * q;
-      int x0 = o.x0, y0 = o.y0;
-      double fx = o.fx, fy = o.fy;
-      double g00 = gradx(Ib, W, x0, y0), g10 = gradx(Ib, W, x0 + 1, y0);
-      double g01 = gradx(Ib, W, x0, y0 + 1), g11 = gradx(Ib, W, x0 + 1, y0 + 1);
-      double gx = (1.0 - fy) * ((1.0 - fx) * g00 + fx * g10) + fy * ((1.0 - fx) * g01 + fx * g11);
-      g00 = grady(Ib, W, H, x0, y0);
-      g10 = grady(Ib, W, H, x0 + 1, y0);
-      g01 = grady(Ib, W, H, x0, y0 + 1);
-      g11 = grady(Ib, W, H, x0 + 1, y0 + 1);
-      double gy = (1.0 - fy) * ((1.0 - fx) * g00 + fx * g10) + fy * ((1.0 - fx) * g01 + fx * g11);
-      double J[6] = {gx, gx * o.X, gx * o.Y, gy, gy * o.X, gy * o.Y};
+    // pass 2: exact fixed-point normal equations; each warp reduces its 32 pixels' 27 integer
+    // terms with shuffles and lane 0 accumulates the warp's row of `red` (few live registers)
+    if (lane < 27) red[warp][lane] = 0;
+    __syncwarp();
+    for (int64_t base = c0 + (tid & ~31); base < c1; base += kIrlsThreads) {
+      int64_t id = base + lane;
+      bool ok = false;
+      double w = 0.0, r = 0.0, J[6] = {0.0, 0.0, 0.0, 0.0, 0.0, 0.0};
+      if (id < c1) {
+        int j = (int)(id / W), i = (int)(id - (int64_t)j * W);
+        Pix o;
+        if (irls_pixel(Ia, Ma, Ib, Db, W, H, p, cx, cy, s, i, j, o)) {
+          double u = o.r / c;
+          if (fabs(u) < 1.0) {
+            ok = true;
+            double q = 1.0 - u * u;
+            w = q * q;
+            r = o.r;
+            int x0 = o.x0, y0 = o.y0;
+            double fx = o.fx, fy = o.fy;
+            double g00 = gradx(Ib, W, x0, y0), g10 = gradx(Ib, W, x0 + 1, y0);
+            double g01 = gradx(Ib, W, x0, y0 + 1), g11 = gradx(Ib, W, x0 + 1, y0 + 1);
+            double gx = (1.0 - fy) * ((1.0 - fx) * g00 + fx * g10) + fy * ((1.0 - fx) * g01 + fx * g11);
+            g00 = grady(Ib, W, H, x0, y0);
+            g10 = grady(Ib, W, H, x0 + 1, y0);
+            g01 = grady(Ib, W, H, x0, y0 + 1);
+            g11 = grady(Ib, W, H, x0 + 1, y0 + 1);
+            double gy = (1.0 - fy) * ((1.0 - fx) * g00 + fx * g10) + fy * ((1.0 - fx) * g01 + fx * g11);
+            J[0] = gx; J[1] = gx * o.X; J[2] = gx * o.Y;
+            J[3] = gy; J[4] = gy * o.X; J[5] = gy * o.Y;
+          }
+        }
+      }
+      if (!__any_sync(kFull, ok)) continue;
       int k = 0;
 #pragma unroll
       for (int aa = 0; aa < 6; ++aa) {
         double wa = w * J[aa];
 #pragma unroll
-        for (int bb = aa; bb < 6; ++bb) acc[k++] += __double2ll_rn(wa * J[bb] * 65536.0);
-        acc[21 + aa] += __double2ll_rn(wa * o.r * 65536.0);
+        for (int bb = aa; bb < 6; ++bb) {
+          long long t = warp_sum_ll(ok ? __double2ll_rn(wa * J[bb] * 65536.0) : 0ll);
+          if (lane == 0) red[warp][k] += t;
+          ++k;
+        }
+        long long t = warp_sum_ll(ok ? __double2ll_rn(wa * r * 65536.0) : 0ll);
+        if (lane == 0) red[warp][21 + aa] += t;
       }
-    }
-#pragma unroll
-    for (int k = 0; k < 27; ++k) {
-      long long v = warp_sum_ll(acc[k]);
-      if (lane == 0) red[warp][k] = v;
     }
     __syncthreads();
     if (tid < 27) {
       long long v = 0;
       for (int w = 0; w < kIrlsWarps; ++w) v += red[w][tid];
-      red[0][tid] = v;
+      tot[tid] = v;
+    }
+    cl_sync();
+    if (tid < 27) {
+      long long v = 0;
+      for (unsigned r = 0; r < kCl; ++r) v += cl_map(tot, r)[tid];
+      red[0][tid] = v;  // cluster total (own red row 0 is free: the warp sums are consumed)
     }
     __syncthreads();
     ++iters;
@@ -285,14 +414,16 @@ __global__ void __launch_bounds__(kIrlsThreads) k_irls(IrlsLevel a) {
         if (sqrt(nrm) < a.tol) s_stop = 1;
       }
     }
-    __syncthreads();
+    cl_sync();  // tot reads by other ranks done; sp / s_stop published in this CTA
     if (s_stop) break;
   }
-  __syncthreads();
-  if (tid < 6) a.p[6 * n + tid] = sp[tid];
-  if (tid == 0) {
-    a.status[n] = s_status;
-    a.iters[n] += iters;
+  cl_sync();  // no CTA exits while another may still read its shared memory
+  if (rk == 0) {
+    if (tid < 6) a.p[6 * n + tid] = sp[tid];
+    if (tid == 0) {
+      a.status[n] = s_status;
+      a.iters[n] += iters;
+    }
   }
 }
 
@@ -459,8 +590,10 @@ inline size_t al(size_t b) { return (b + 255) & ~(size_t)255; }
 struct AlignWs {
   double* I[8];
   uint8_t* M[8];
+  uint8_t* D[8];
   int W[8], H[8];
   uint64_t* keys;
+  uint64_t* cand;
   double* p;
   size_t bytes;
 };
@@ -477,8 +610,12 @@ AlignWs carve(void* base, int W, int H, int T, int L) {
     off += al(n * sizeof(double));
     w.M[k] = (uint8_t*)(c ? c + off : nullptr);
     off += al(n);
+    w.D[k] = (uint8_t*)(c ? c + off : nullptr);
+    off += al(n);
   }
   w.keys = (uint64_t*)(c ? c + off : nullptr);
+  off += al((size_t)W * H * (T > 1 ? T - 1 : 1) * sizeof(uint64_t));
+  w.cand = (uint64_t*)(c ? c + off : nullptr);
   off += al((size_t)W * H * (T > 1 ? T - 1 : 1) * sizeof(uint64_t));
   w.p = (double*)(c ? c + off : nullptr);
   off += al((size_t)(T > 1 ? T - 1 : 1) * 6 * sizeof(double));
@@ -518,6 +655,11 @@ vinp_status vinp_affine_estimate(const uint8_t* rgb, const uint8_t* mask, int W,
     k_grey_down<<<g, 128, 0, s>>>(w.I[k - 1], w.M[k - 1], w.W[k - 1], w.H[k - 1], w.I[k], w.M[k], w.W[k], w.H[k]);
     count_launch();
   }
+  for (int k = 0; k < L; ++k) {
+    dim3 g((w.W[k] + 127) / 128, w.H[k], T);
+    k_mask_dil<<<g, 128, 0, s>>>(w.M[k], w.D[k], w.W[k], w.H[k]);
+    count_launch();
+  }
   int np = T - 1;
   double sc = (double)(w.W[L - 1] > w.H[L - 1] ? w.W[L - 1] : w.H[L - 1]) * 0.5;
   k_affine_init<<<(np + 127) / 128, 128, 0, s>>>(w.p, status, iters, np, sc);
@@ -527,8 +669,9 @@ vinp_status vinp_affine_estimate(const uint8_t* rgb, const uint8_t* mask, int W,
       k_level_up<<<(np + 127) / 128, 128, 0, s>>>(w.p, status, np, w.W[k + 1], w.H[k + 1], w.W[k], w.H[k]);
       count_launch();
     }
-    IrlsLevel a{w.I[k], w.M[k], w.W[k], w.H[k], w.p, status, iters, w.keys, (int64_t)W * H, max_iter, tol};
-    k_irls<<<np, kIrlsThreads, 0, s>>>(a);
+    IrlsLevel a{w.I[k], w.M[k], w.D[k], w.W[k], w.H[k], w.p, status, iters, w.keys, w.cand, (int64_t)W * H,
+                max_iter, tol};
+    k_irls<<<np * kCl, kIrlsThreads, 0, s>>>(a);
     count_launch();
   }
   k_affine_finish<<<(np + 127) / 128, 128, 0, s>>>(w.p, status, np, W, H, theta);
