@@ -365,7 +365,7 @@ vinp_status vinp_commit(vinp_level* lv, const float* out_rgb, const float* out_t
 }
 
 vinp_status vinp_change_l1(const float* a, const float* b, int64_t n, int64_t* out, void* stream) {
-  VINP_REQUIRE(a && b && out && n >= 0, "vinp_change_l1: bad args");
+  VINP_REQUIRE(out && n >= 0 && (n == 0 || (a && b)), "vinp_change_l1: bad args");
   if (n > 0) {
     int g = (int)std::min<int64_t>(nblk(n, 256), 148 * 8);
     k_change_l1<<<g, 256, 0, S(stream)>>>(a, b, n, (unsigned long long*)out);

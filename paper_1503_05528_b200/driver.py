@@ -146,8 +146,9 @@ class Inpainter:
         old = {id(st.lv): st for st in self.states}
         self.states = []
         for lv in self.levels:
-            npad = self.ex.padded(lv.n_targets)
-            hpad = self.ex.padded(lv.n_holes)
+            # >= 1 row so that an empty H (nothing to inpaint) still passes valid device pointers
+            npad = max(self.ex.padded(lv.n_targets), 1)
+            hpad = max(self.ex.padded(lv.n_holes), 1)
             st = old.get(id(lv))
             if st is not None and st.a.e.numel() == npad and st.cur_rgb.shape[0] == hpad:
                 self.states.append(st)  # same sizes: reuse the buffers (repeated calls)
