@@ -109,7 +109,10 @@ __global__ void k_upsample(LevelArgs c, const uint64_t* __restrict__ ce, LevelAr
     accc = __dp4a(dc, dc, accc);                                              \
     acct = __dp4a(dx_, dx_, acct);                                            \
   }
-template <bool ABORT>
+// KB = true (kernels launched for K-restricted onion passes): the non-interior path issues all
+// gathers of a frame together (in-Omega predicates, then the layer bytes of K, then the predicated
+// voxel loads) instead of one branch-guarded voxel at a time.
+template <bool ABORT, bool KB = false>
 __device__ __forceinline__ uint32_t thread_ssd(const LevelArgs& a, int p, int px, int py, int pt,
                                                int q, int lambda, int kb, bool full, uint32_t thr,
                                                bool& alive) {
@@ -151,7 +154,7 @@ __device__ __forceinline__ uint32_t thread_ssd(const LevelArgs& a, int p, int px
         uint64_t s0 = __ldg(sr - 2), s1 = __ldg(sr - 1), s2 = __ldg(sr), s3 = __ldg(sr + 1), s4 = __ldg(sr + 2);
         VINP_ACC(t0, s0) VINP_ACC(t1, s1) VINP_ACC(t2, s2) VINP_ACC(t3, s3) VINP_ACC(t4, s4)
 #endif
-      } else {
+      } else if (!KB) {
 #pragma unroll
         for (int dx = -2; dx <= 2; ++dx) {
           if (!inside(a.g, px + dx, py + dy, pt + dt)) continue;
@@ -160,6 +163,30 @@ __device__ __forceinline__ uint32_t thread_ssd(const LevelArgs& a, int p, int px
           VINP_ACC(t, s)
         }
       }
+    }
+    if (KB && !full) {
+      bool ok[25];
+      const bool tin = (unsigned)(pt + dt) < (unsigned)a.g.T;
+#pragma unroll
+      for (int k = 0; k < 25; ++k)
+        ok[k] = tin && (unsigned)(py + k / 5 - 2) < (unsigned)a.g.H && (unsigned)(px + k % 5 - 2) < (unsigned)a.g.W;
+      if (kb >= 0) {
+        uint8_t lay[25];
+#pragma unroll
+        for (int k = 0; k < 25; ++k)
+          lay[k] = ok[k] ? a.layer[p + dt * a.g.HW + (k / 5 - 2) * a.g.W + (k % 5 - 2)] : (uint8_t)255;
+#pragma unroll
+        for (int k = 0; k < 25; ++k) ok[k] = ok[k] && (int)lay[k] < kb;
+      }
+      uint64_t tv[25], sv[25];
+#pragma unroll
+      for (int k = 0; k < 25; ++k) {
+        int off = dt * a.g.HW + (k / 5 - 2) * a.g.W + (k % 5 - 2);
+        tv[k] = ok[k] ? __ldg(v + (p + off)) : 0ull;
+        sv[k] = ok[k] ? __ldg(v + (q + off)) : 0ull;
+      }
+#pragma unroll
+      for (int k = 0; k < 25; ++k) VINP_ACC(tv[k], sv[k])
     }
     if (ABORT) {
       uint32_t part = 4u * accc + (uint32_t)lambda * acct;
@@ -172,6 +199,7 @@ __device__ __forceinline__ uint32_t thread_ssd(const LevelArgs& a, int p, int px
 }
 
 // ------------------------------------------------------------------ a5: evaluate
+template <bool KB>
 __global__ void __launch_bounds__(256) k_evaluate(LevelArgs a, uint64_t* __restrict__ ee,
                                                   uint8_t* __restrict__ en, int lambda, int kb,
                                                   int only_layer, int32_t b, int32_t e,
@@ -189,7 +217,7 @@ __global__ void __launch_bounds__(256) k_evaluate(LevelArgs a, uint64_t* __restr
     int q = e_q(ee[s]);
     bool full = kb < 0 && px >= 2 && px < a.g.W - 2 && py >= 2 && py < a.g.H - 2 && pt >= 2 && pt < a.g.T - 2;
     bool alive = true;
-    uint32_t D = thread_ssd<false>(a, p, px, py, pt, q, lambda, kb, full, 0, alive);
+    uint32_t D = thread_ssd<false, KB>(a, p, px, py, pt, q, lambda, kb, full, 0, alive);
     int n = 0;
     if (full) {
       n = 125;
@@ -213,7 +241,8 @@ __global__ void __launch_bounds__(256) k_evaluate(LevelArgs a, uint64_t* __restr
 // Lane = target (thread-per-target, coherent candidates).  Candidates of rank 1..3 are evaluated
 // one rank at a time by all lanes that have one, each against the running best of its own target
 // (strict improvement in rank order, R25).
-__global__ void __launch_bounds__(256, VINP_PROP_MINB) k_propagate(LevelArgs a, const uint64_t* __restrict__ ein,
+template <bool KB>
+__global__ void __launch_bounds__(256, KB ? 2 : VINP_PROP_MINB) k_propagate(LevelArgs a, const uint64_t* __restrict__ ein,
                                                    uint64_t* __restrict__ eout, int lambda, int step,
                                                    int sign, int kb, int only_layer, int32_t b,
                                                    int32_t e, const int32_t* __restrict__ list,
@@ -290,8 +319,8 @@ __global__ void __launch_bounds__(256, VINP_PROP_MINB) k_propagate(LevelArgs a, 
     if (!__any_sync(kFull, mine)) break;
     if (mine) {
       bool alive = true;
-      uint32_t D = allfull ? thread_ssd<true>(a, p, px, py, pt, cq[c], lambda, kb, true, bestD, alive)
-                           : thread_ssd<true>(a, p, px, py, pt, cq[c], lambda, kb, full, bestD, alive);
+      uint32_t D = allfull ? thread_ssd<true, KB>(a, p, px, py, pt, cq[c], lambda, kb, true, bestD, alive)
+                           : thread_ssd<true, KB>(a, p, px, py, pt, cq[c], lambda, kb, full, bestD, alive);
       if (alive && D < bestD) {
         bestD = D;
         bestq = cq[c];
@@ -716,8 +745,12 @@ vinp_status launch_evaluate(const vinp_level* lv, vinp_nnf* nnf, const vinp_para
   VINP_REQUIRE(nnf && nnf->e && nnf->n, "vinp_nnf_evaluate: null nnf");
   VINP_REQUIRE((kb < 0 && only_layer < 0) || lv->layer, "vinp_nnf_evaluate: layer map required");
   if (e > b) {
-    k_evaluate<<<nblk(e - b, 256), 256, 0, S(stream)>>>(
-        args_of(lv), nnf->e, nnf->n, prm->lambda, kb, only_layer, b, e, list, counter);
+    if (kb >= 0)
+      k_evaluate<true><<<nblk(e - b, 256), 256, 0, S(stream)>>>(
+          args_of(lv), nnf->e, nnf->n, prm->lambda, kb, only_layer, b, e, list, counter);
+    else
+      k_evaluate<false><<<nblk(e - b, 256), 256, 0, S(stream)>>>(
+          args_of(lv), nnf->e, nnf->n, prm->lambda, kb, only_layer, b, e, list, counter);
     count_launch();
   }
   return check_launch("vinp_nnf_evaluate");
@@ -732,8 +765,12 @@ vinp_status launch_propagate(const vinp_level* lv, const vinp_nnf* in, vinp_nnf*
   VINP_REQUIRE(step >= 1 && sign >= -1 && sign <= 1, "vinp_propagate: bad step/sign");
   VINP_REQUIRE((kb < 0 && only_layer < 0) || lv->layer, "vinp_propagate: layer map required");
   if (e > b) {
-    k_propagate<<<nblk(e - b, 256), 256, 0, S(stream)>>>(
-        args_of(lv), in->e, out->e, prm->lambda, step, sign, kb, only_layer, b, e, list, counter);
+    if (kb >= 0)
+      k_propagate<true><<<nblk(e - b, 256), 256, 0, S(stream)>>>(
+          args_of(lv), in->e, out->e, prm->lambda, step, sign, kb, only_layer, b, e, list, counter);
+    else
+      k_propagate<false><<<nblk(e - b, 256), 256, 0, S(stream)>>>(
+          args_of(lv), in->e, out->e, prm->lambda, step, sign, kb, only_layer, b, e, list, counter);
     count_launch();
   }
   return check_launch("vinp_propagate");
