@@ -219,6 +219,11 @@ def main():
         levels[-1]["onion_s"] = stats.onion_ms / 1000.0
         # dominant-kernel roofline: one instrumented step with events around every pass
         roof = measure_roofline(ip, v, m, dev)
+        # SURVEY §8(d)'s whole-step model: (625 N_pu + 29 N_tp + 662 N_hole) / (t_step x peak)
+        sb = roof.pop("_step_bytes")
+        gbs = sb / (ms / args.steps / 1000.0) / 1e9
+        roof["step_model"] = {"bytes": sb, "GB/s": round(gbs, 1), "frac": round(gbs / roof["peak"], 4),
+                              "note": "all PatchMatch + reconstruction passes of the step over the timed ms_per_step"}
 
     e2e = None
     if not args.no_e2e and not args.no_extra:
@@ -344,7 +349,7 @@ def measure_roofline(ip, v, m, dev):
             "peak_kind": kind, "unit": "GB/s", "frac": round(achieved / peak, 4),
             "traffic": traffic, "bytes_per_launch": a["bytes"] / a["launches"],
             "avg_launch_ms": a["ms"] / a["launches"], "share_of_step": round(a["ms"] / tot, 4),
-            "kernels": kernels,
+            "kernels": kernels, "_step_bytes": int(sum(x["bytes"] for x in agg.values())),
             "by_level": {k: {"ms": round(x["ms"], 2), "GB/s": round(x["bytes"] / (x["ms"] / 1000) / 1e9, 1),
                              "launches": x["launches"], "patch_updates": x["pu"]}
                          for k, x in sorted(per_level.items())}}
