@@ -442,18 +442,18 @@ __device__ __forceinline__ uint32_t sum5(uint32_t x, int base, int k) {
   return s2 + __shfl_sync(kFull, x, base + (k + 4) % 5);
 }
 
-template <int NC, int WPB, bool KNOWN>
+template <int NC, int WPB, bool KNOWN, int TPW>
 __global__ void __launch_bounds__(32 * WPB, VINP_MINB * 8 / WPB) k_random_search(
     LevelArgs a, const uint64_t* __restrict__ ein, uint64_t* __restrict__ eout, int lambda, Radii rad,
     uint64_t seed, uint32_t oc, int pm_iter, int kb, int only_layer, int32_t b, int32_t e,
-    const int32_t* __restrict__ list, unsigned long long* counter, int tpw) {
-  // tpw targets per warp (32; 8 for small launches, e.g. onion layers, so that more warps share
+    const int32_t* __restrict__ list, unsigned long long* counter) {
+  // TPW targets per warp (32; 8 for small launches, e.g. onion layers, so that more warps share
   // the pair evaluations — the result does not depend on it)
   int lane = threadIdx.x & 31;
-  int i0 = b + (blockIdx.x * WPB + (threadIdx.x >> 5)) * tpw;
+  int i0 = b + (blockIdx.x * WPB + (threadIdx.x >> 5)) * TPW;
   if (i0 >= e) return;
   int idx = i0 + lane;
-  bool have = lane < tpw && idx < e;
+  bool have = (TPW == 32 || lane < TPW) && idx < e;
   int s = have ? (list ? __ldg(list + idx) : idx) : 0;
   int p = have ? __ldg(a.targets + s) : 0;
   uint64_t inc = have ? __ldg(reinterpret_cast<const unsigned long long*>(ein) + s) : 0ull;
@@ -812,16 +812,25 @@ vinp_status launch_random_search(const vinp_level* lv, const vinp_nnf* in, vinp_
   if (e > b) {
     cudaStream_t cs = S(stream);
     LevelArgs la = args_of(lv);
-    const int tpw = (e - b) < 148 * 32 * 8 ? 8 : 32;
+    const bool small = (e - b) < 148 * 32 * 8;
+#define VINP_RS2(NC, WPB, KN, TPW)                                                                 \
+  k_random_search<NC, WPB, KN, TPW><<<nblk(e - b, TPW * WPB), 32 * WPB, 0, cs>>>(                   \
+      la, in->e, out->e, prm->lambda, r, prm->seed, outer_code, pm_iter, kb, only_layer, b, e, list, \
+      counter)
 #define VINP_RS(NC, WPB)                                                                           \
-  if (kb >= 0)                                                                                     \
-    k_random_search<NC, WPB, true><<<nblk(e - b, tpw * WPB), 32 * WPB, 0, cs>>>(                    \
-        la, in->e, out->e, prm->lambda, r, prm->seed, outer_code, pm_iter, kb, only_layer, b, e,     \
-        list, counter, tpw);                                                                       \
-  else                                                                                             \
-    k_random_search<NC, WPB, false><<<nblk(e - b, tpw * WPB), 32 * WPB, 0, cs>>>(                   \
-        la, in->e, out->e, prm->lambda, r, prm->seed, outer_code, pm_iter, kb, only_layer, b, e,     \
-        list, counter, tpw)
+  do {                                                                                             \
+    if (kb >= 0) {                                                                                 \
+      if (small)                                                                                   \
+        VINP_RS2(NC, WPB, true, 8);                                                                \
+      else                                                                                         \
+        VINP_RS2(NC, WPB, true, 32);                                                               \
+    } else {                                                                                       \
+      if (small)                                                                                   \
+        VINP_RS2(NC, WPB, false, 8);                                                               \
+      else                                                                                         \
+        VINP_RS2(NC, WPB, false, 32);                                                              \
+    }                                                                                              \
+  } while (0)
     if (r.M <= 8)
       VINP_RS(8, 8);
     else if (r.M <= 12)
@@ -831,6 +840,7 @@ vinp_status launch_random_search(const vinp_level* lv, const vinp_nnf* in, vinp_
     else
       VINP_RS(32, 2);
 #undef VINP_RS
+#undef VINP_RS2
     count_launch();
   }
   return check_launch("vinp_random_search");
