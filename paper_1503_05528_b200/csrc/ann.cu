@@ -81,6 +81,9 @@ __global__ void k_upsample(LevelArgs c, const uint64_t* __restrict__ ce, LevelAr
   fn[s] = 0;
 }
 
+#ifndef VINP_RS_QUEUE
+#define VINP_RS_QUEUE 1
+#endif
 #ifndef VINP_MINB
 #define VINP_MINB 3
 #endif
@@ -498,6 +501,96 @@ __global__ void __launch_bounds__(32 * WPB, VINP_MINB * 8 / WPB) k_random_search
   int bestq = e_q(inc);
   const int g = lane / 5, k = lane - 5 * (lane / 5), gbase = 5 * g, dx = k - 2;
   const unsigned long long* v = reinterpret_cast<const unsigned long long*>(a.vox);
+#if VINP_RS_QUEUE
+  // Each 5-lane group g < 6 walks the warp's pair list on its own: one frame of its current pair
+  // per loop iteration, and as soon as the pair aborts or completes the group takes the next
+  // unassigned pair, so a surviving pair never holds other groups idle.  Sequential application
+  // in rank order with strict improvement (R25) equals the lexicographic minimum of (D, pair index)
+  // over {incumbent (D_inc, -1)} + candidates; a pair is dropped once its partial sum proves it
+  // cannot reach that minimum (partial > best D, or == best D with a later index): exact (R35).
+  int bestJ = -1;
+  int j = -1, dtc = -2, t = 0, pi = 0, ty = 0, tt = 0, sq = 0;
+  bool colok = false;
+  uint32_t accc = 0, acct = 0;
+  int next = 0;
+  const int gsrc = gbase < 30 ? gbase : 0;
+  for (;;) {
+    // hand out pairs to the groups that need one (in group order)
+    bool need = g < 6 && j < 0 && next < P;
+    unsigned nb = __ballot_sync(kFull, need && k == 0);
+    if (nb) {
+      int jj = next + __popc(nb & ((1u << gbase) - 1u));
+      bool take = need && jj < P;
+      int2 pr = take ? pairs[jj] : make_int2(0, lane);
+      int src = take ? pr.y : lane;
+      int npi = __shfl_sync(kFull, p, src), ntx = __shfl_sync(kFull, px, src);
+      int nty = __shfl_sync(kFull, py, src), ntt = __shfl_sync(kFull, pt, src);
+      if (take) {
+        j = jj;
+        t = pr.y;
+        sq = pr.x;
+        pi = npi;
+        ty = nty;
+        tt = ntt;
+        colok = (unsigned)(ntx + dx) < (unsigned)a.g.W;
+        dtc = -2;
+        accc = acct = 0;
+      }
+      next = min(P, next + __popc(nb));
+    }
+    bool active = j >= 0;
+    if (!__any_sync(kFull, active)) break;
+    // one frame of the current pair: all 10 gathers first, then the arithmetic
+    bool tok = active && colok && (unsigned)(tt + dtc) < (unsigned)a.g.T;
+    int ro[5];
+    bool okr[5];
+#pragma unroll
+    for (int r = 0; r < 5; ++r) {
+      ro[r] = dtc * a.g.HW + (r - 2) * a.g.W + dx;
+      okr[r] = tok && (unsigned)(ty + r - 2) < (unsigned)a.g.H;
+      if (KNOWN) okr[r] = okr[r] && a.layer[pi + (okr[r] ? ro[r] : 0)] < kb;
+    }
+    uint64_t tv[5], sv[5];
+#pragma unroll
+    for (int r = 0; r < 5; ++r) {
+      tv[r] = __ldg(v + pi + (okr[r] ? ro[r] : 0));
+      sv[r] = __ldg(v + sq + (okr[r] ? ro[r] : 0));
+    }
+    uint32_t tD = __shfl_sync(kFull, bestD, active ? t : lane);
+    int tJ = __shfl_sync(kFull, bestJ, active ? t : lane);
+#pragma unroll
+    for (int r = 0; r < 5; ++r) {
+      uint64_t tw = okr[r] ? tv[r] : 0ull, sw = okr[r] ? sv[r] : 0ull;
+      uint32_t dc = __vabsdiffu4((uint32_t)tw, (uint32_t)sw);
+      uint32_t dtx = __vabsdiffu4((uint32_t)(tw >> 32), (uint32_t)(sw >> 32));
+      accc = __dp4a(dc, dc, accc);
+      acct = __dp4a(dtx, dtx, acct);
+    }
+    uint32_t tot = sum5(4u * accc + (uint32_t)lambda * acct, gsrc, k);
+    bool dead = active && (tot > tD || (tot == tD && j > tJ));
+    bool win = active && !dead && dtc == 2;
+    unsigned wb = __ballot_sync(kFull, win && k == 0);
+    while (wb) {  // apply this iteration's completed pairs (several may share an owner)
+      int src = __ffs(wb) - 1;
+      wb &= wb - 1u;
+      uint32_t D = __shfl_sync(kFull, tot, src);
+      int jw = __shfl_sync(kFull, j, src);
+      int qw = __shfl_sync(kFull, sq, src);
+      int own = __shfl_sync(kFull, t, src);
+      if (lane == own && (D < bestD || (D == bestD && jw < bestJ))) {
+        bestD = D;
+        bestJ = jw;
+        bestq = qw;
+      }
+    }
+    if (active) {
+      if (dead || dtc == 2)
+        j = -1;
+      else
+        ++dtc;
+    }
+  }
+#else
   for (int base = 0; base < P; base += 6) {
     int j = base + g;
     bool valid = g < 6 && j < P;
@@ -557,6 +650,7 @@ __global__ void __launch_bounds__(32 * WPB, VINP_MINB * 8 / WPB) k_random_search
       }
     }
   }
+#endif
   if (have) eout[s] = pack_e(bestD, bestq);
   if (lane == 0) flush_count(counter, (unsigned)P);
 }
