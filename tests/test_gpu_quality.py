@@ -52,6 +52,49 @@ def _quality(name, max_targets=None, steps=(8, 4, 2, 1), sign_policy=0):
                 ratio_minus_1=d_pm / d_bf - 1 if d_bf > 0 else 0.0, frac_exact=same)
 
 
+def _quality_final(name):
+    """Steady state: after the whole configured Alg. 4, one more ANN search (the configured PM
+    iterations) from the final level-1 NNF on the final video u, against the exact NN of that u.
+    (`reeval_*`: the final NNF itself re-evaluated on the final u, before that search.)"""
+    from paper_1503_05528_b200 import Config, Inpainter, vinp as V
+    c = CONFIGS[name]
+    v, m, _ = generate(name, device="cuda")
+    ip = Inpainter(c.W, c.H, c.T, Config(levels=c.levels, pm_iters=c.pm_iters, fixed_outer=c.fixed_outer,
+                                         max_outer=c.max_outer, lam=c.lam, seed=c.seed), "cuda")
+    ip.load(v, m)
+    stats = ip.run()
+    st = ip.states[0]
+    lv = st.lv
+    V.nnf_evaluate(lv, st.a, ip.prm)
+    bf = V.NNF.alloc(lv.n_targets, "cuda")
+    V.brute_force_tc(lv, bf, ip.prm, 0, lv.n_targets)
+    torch.cuda.synchronize()
+    n = lv.n_targets
+    re_pm = ((st.a.e[:n] >> 32).double() / (4 * st.a.n[:n].double())).mean().item()
+    V.ann_search(lv, st.a, st.b, ip.prm, 1 << 20, c.pm_iters, (8, 4, 2, 1))
+    torch.cuda.synchronize()
+    Dp, Db = (st.a.e[:n] >> 32).double(), (bf.e[:n] >> 32).double()
+    npm, nbf = st.a.n[:n].double(), bf.n[:n].double()
+    assert torch.all(Dp >= Db) and torch.equal(npm, nbf)
+    d_pm, d_bf = (Dp / (4 * npm)).mean().item(), (Db / (4 * nbf)).mean().item()
+    return dict(config=name, stage="steady state (one more ANN search after Alg. 4)",
+                outer_l1=stats.levels[0]["outer"], targets=n, reeval_mean_d2=re_pm,
+                reeval_ratio_minus_1=re_pm / d_bf - 1 if d_bf > 0 else 0.0,
+                mean_d2_patchmatch=d_pm, mean_d2_bruteforce=d_bf,
+                ratio_minus_1=d_pm / d_bf - 1 if d_bf > 0 else 0.0,
+                frac_exact=(st.a.e[:n] == bf.e[:n]).double().mean().item())
+
+
+@pytest.mark.parametrize("name", ["c1", "c2", "c3"])
+def test_patchmatch_quality_after_full_run(name):
+    q = _quality_final(name)
+    os.makedirs(os.path.join(ROOT, "gpurun_out"), exist_ok=True)
+    with open(os.path.join(ROOT, "gpurun_out", f"quality_final_{name}.json"), "w") as f:
+        json.dump(q, f)
+    print(json.dumps(q))
+    assert q["ratio_minus_1"] <= 0.25
+
+
 @pytest.mark.parametrize("name", ["c1", "c2", "c3"])
 def test_patchmatch_quality_vs_brute_force(name):
     q = _quality(name)
