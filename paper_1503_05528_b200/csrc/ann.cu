@@ -81,17 +81,11 @@ __global__ void k_upsample(LevelArgs c, const uint64_t* __restrict__ ce, LevelAr
   fn[s] = 0;
 }
 
-#ifndef VINP_RS_QUEUE
-#define VINP_RS_QUEUE 1
-#endif
 #ifndef VINP_MINB
 #define VINP_MINB 3
 #endif
 #ifndef VINP_PROP_MINB
 #define VINP_PROP_MINB 4
-#endif
-#ifndef VINP_FRAME_BATCH
-#define VINP_FRAME_BATCH 1
 #endif
 #ifndef VINP_GROUP
 #define VINP_GROUP 8
@@ -123,7 +117,6 @@ __device__ __forceinline__ uint32_t thread_ssd(const LevelArgs& a, int p, int px
   uint32_t accc = 0, acct = 0;
 #pragma unroll 1
   for (int dt = -2; dt <= 2; ++dt) {
-#if VINP_FRAME_BATCH
     if (full) {  // all 50 gathers of the frame in flight, then the arithmetic
       uint64_t tv[25], sv[25];
 #pragma unroll
@@ -142,22 +135,12 @@ __device__ __forceinline__ uint32_t thread_ssd(const LevelArgs& a, int p, int px
         accc = __dp4a(dc, dc, accc);
         acct = __dp4a(dx_, dx_, acct);
       }
-    }
-#endif
+    } else if (!KB) {  // border target: one branch-guarded voxel at a time (rare)
 #pragma unroll
-    for (int dy = -2; dy <= 2; ++dy) {
-      int ro = dt * a.g.HW + dy * a.g.W;
-      const unsigned long long* tr = v + (p + ro);
-      const unsigned long long* sr = v + (q + ro);
-      if (full) {
-#if VINP_FRAME_BATCH
-        continue;  // handled per frame below
-#else
-        uint64_t t0 = __ldg(tr - 2), t1 = __ldg(tr - 1), t2 = __ldg(tr), t3 = __ldg(tr + 1), t4 = __ldg(tr + 2);
-        uint64_t s0 = __ldg(sr - 2), s1 = __ldg(sr - 1), s2 = __ldg(sr), s3 = __ldg(sr + 1), s4 = __ldg(sr + 2);
-        VINP_ACC(t0, s0) VINP_ACC(t1, s1) VINP_ACC(t2, s2) VINP_ACC(t3, s3) VINP_ACC(t4, s4)
-#endif
-      } else if (!KB) {
+      for (int dy = -2; dy <= 2; ++dy) {
+        int ro = dt * a.g.HW + dy * a.g.W;
+        const unsigned long long* tr = v + (p + ro);
+        const unsigned long long* sr = v + (q + ro);
 #pragma unroll
         for (int dx = -2; dx <= 2; ++dx) {
           if (!inside(a.g, px + dx, py + dy, pt + dt)) continue;
@@ -316,9 +299,6 @@ __global__ void __launch_bounds__(256, KB ? 2 : VINP_PROP_MINB) k_propagate(Leve
 #pragma unroll
   for (int c = 0; c < NCMAX; ++c) {
     bool mine = c < ncand;
-#ifdef VINP_DIAG_NOSSD
-    mine = false;  // diagnostic timing build only: candidate generation without evaluation
-#endif
     if (!__any_sync(kFull, mine)) break;
     if (mine) {
       bool alive = true;
@@ -501,7 +481,6 @@ __global__ void __launch_bounds__(32 * WPB, VINP_MINB * 8 / WPB) k_random_search
   int bestq = e_q(inc);
   const int g = lane / 5, k = lane - 5 * (lane / 5), gbase = 5 * g, dx = k - 2;
   const unsigned long long* v = reinterpret_cast<const unsigned long long*>(a.vox);
-#if VINP_RS_QUEUE
   // Each 5-lane group g < 6 walks the warp's pair list on its own: one frame of its current pair
   // per loop iteration, and as soon as the pair aborts or completes the group takes the next
   // unassigned pair, so a surviving pair never holds other groups idle.  Sequential application
@@ -590,67 +569,6 @@ __global__ void __launch_bounds__(32 * WPB, VINP_MINB * 8 / WPB) k_random_search
         ++dtc;
     }
   }
-#else
-  for (int base = 0; base < P; base += 6) {
-    int j = base + g;
-    bool valid = g < 6 && j < P;
-    int2 pr = valid ? pairs[j] : make_int2(0, 0);
-    int t = pr.y;
-    int pi = __shfl_sync(kFull, p, t);
-    int tx = __shfl_sync(kFull, px, t), ty = __shfl_sync(kFull, py, t), tt = __shfl_sync(kFull, pt, t);
-    uint32_t thr = __shfl_sync(kFull, bestD, t);
-    bool colok = valid && (unsigned)(tx + dx) < (unsigned)a.g.W;
-    bool alive = valid;
-    uint32_t accc = 0, acct = 0, tot = 0;
-#pragma unroll 1
-    for (int dt = -2; dt <= 2; ++dt) {
-      bool tok = alive && colok && (unsigned)(tt + dt) < (unsigned)a.g.T;
-      // predicates first, then all 10 gathers of the frame (invalid rows read the target's own
-      // centre voxel and are masked), then the arithmetic: one memory round trip per frame
-      int ro[5];
-      bool okr[5];
-#pragma unroll
-      for (int r = 0; r < 5; ++r) {
-        ro[r] = dt * a.g.HW + (r - 2) * a.g.W + dx;
-        okr[r] = tok && (unsigned)(ty + r - 2) < (unsigned)a.g.H;
-        if (KNOWN) okr[r] = okr[r] && a.layer[pi + (okr[r] ? ro[r] : 0)] < kb;
-      }
-      uint64_t tv[5], sv[5];
-#pragma unroll
-      for (int r = 0; r < 5; ++r) {
-        tv[r] = __ldg(v + pi + (okr[r] ? ro[r] : 0));
-        sv[r] = __ldg(v + pr.x + (okr[r] ? ro[r] : 0));
-      }
-#pragma unroll
-      for (int r = 0; r < 5; ++r) {
-        uint64_t tw = okr[r] ? tv[r] : 0ull, sw = okr[r] ? sv[r] : 0ull;
-        uint32_t dc = __vabsdiffu4((uint32_t)tw, (uint32_t)sw);
-        uint32_t dtx = __vabsdiffu4((uint32_t)(tw >> 32), (uint32_t)(sw >> 32));
-        accc = __dp4a(dc, dc, accc);
-        acct = __dp4a(dtx, dtx, acct);
-      }
-      tot = sum5(4u * accc + (uint32_t)lambda * acct, gbase < 30 ? gbase : 0, k);
-      if (tot >= thr) alive = false;
-      if (!__any_sync(kFull, alive)) break;
-    }
-    // apply the surviving pairs of this batch in order
-#pragma unroll
-    for (int g2 = 0; g2 < 6; ++g2) {
-      int src = 5 * g2;
-      bool al = __shfl_sync(kFull, (int)alive, src);
-      if (al) {
-        uint32_t D = __shfl_sync(kFull, tot, src);
-        int tq = __shfl_sync(kFull, pr.x, src);
-        int towner = __shfl_sync(kFull, t, src);
-        uint32_t cur = __shfl_sync(kFull, bestD, towner);
-        if (D < cur && lane == towner) {
-          bestD = D;
-          bestq = tq;
-        }
-      }
-    }
-  }
-#endif
   if (have) eout[s] = pack_e(bestD, bestq);
   if (lane == 0) flush_count(counter, (unsigned)P);
 }
