@@ -85,12 +85,12 @@ class Clocks:
                 "reasons": sorted(reasons), "samples": len(self.rows)}
 
 
-def _cfg(name):
+def _cfg(name, exchange="allgather"):
     from gen.synth import CONFIGS
     from paper_1503_05528_b200 import Config
     c = CONFIGS[name]
     return Config(levels=c.levels, pm_iters=c.pm_iters, fixed_outer=c.fixed_outer, max_outer=c.max_outer,
-                  lam=c.lam, seed=c.seed)
+                  lam=c.lam, seed=c.seed, exchange=exchange)
 
 
 # ----------------------------------------------------------------------------- oracle sample
@@ -152,6 +152,8 @@ def main():
     ap.add_argument("--warmup", type=int, default=3)
     ap.add_argument("--impl", default="vinp", choices=["vinp", "reference"])
     ap.add_argument("--config", default="c5")
+    ap.add_argument("--exchange", default="allgather", choices=["allgather", "halo"],
+                    help="multi-GPU NNF / hole-value exchange (halo = NEXT #4 point-to-point, N > 1 only)")
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--no-cpu", action="store_true")
     ap.add_argument("--no-extra", action="store_true",
@@ -173,7 +175,7 @@ def main():
     if world > 1:
         dist.init_process_group("nccl", device_id=dev)
     ex = Exchange()
-    cfg = _cfg(args.config)
+    cfg = _cfg(args.config, args.exchange)
     c = CONFIGS[args.config]
     v, m, _ = generate(args.config, device=dev)
     torch.cuda.synchronize()
@@ -267,7 +269,8 @@ def main():
                 "config": {"workload": args.config, "dims": [c.W, c.H, c.T], "levels": c.levels,
                            "pm_iters": c.pm_iters, "patch": "5x5x5", "lambda": c.lam,
                            "l2": "inputs larger than L2 (level-1 volume 1.66 GB)",
-                           "parallelism": f"target slabs x{world}"},
+                           "parallelism": f"target slabs x{world}",
+                           "exchange": args.exchange if world > 1 else None},
                 "patch_updates_per_step": pu // args.steps, "sec_per_level": levels,
                 "roofline": roof, "cpu_baseline": cpu, "e2e": e2e, "gpu_launches": launches,
                 "clocks": clk.summary()}

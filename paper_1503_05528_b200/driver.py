@@ -39,6 +39,7 @@ class Config:
     align_levels: int = 3       # R36: estimation pyramid levels
     align_iters: int = 20       # R38: IRLS iterations per level
     align_tol: float = 1e-4     # R38: update-norm stop
+    exchange: str = "allgather"  # multi-GPU: "allgather" every pass, or "halo" (NEXT #4, P2P)
 
     def params(self) -> V.Params:
         return V.Params(lam=self.lam, tex_half=self.tex_half, seed=self.seed, rho=self.rho)
@@ -72,6 +73,36 @@ class Exchange:
     def allreduce_sum(self, t: torch.Tensor):
         if self.world > 1:
             self.dist.all_reduce(t, group=self.group)
+
+    def slabs(self, n: int):
+        c = self.padded(n) // self.world
+        return [(min(n, r * c), min(n, (r + 1) * c)) for r in range(self.world)]
+
+    def halo(self, t: torch.Tensor, n: int, need):
+        """Point-to-point halo exchange (NEXT #4): need[r] = (lo, hi), the rows rank r reads.  Every
+        rank sends the part of its slab that each other rank needs and receives the parts of the
+        other slabs it needs; all ranks derive the same ranges, so sends and receives pair up."""
+        if self.world == 1:
+            return
+        sl = self.slabs(n)
+        me = self.rank
+        b, e = sl[me]
+        ops = []
+        for r in range(self.world):
+            if r == me:
+                continue
+            lo, hi = need[r]
+            s0, s1 = max(b, lo), min(e, hi)
+            if s1 > s0:
+                ops.append(self.dist.P2POp(self.dist.isend, t[s0:s1], r, self.group))
+            rb, re_ = sl[r]
+            lo2, hi2 = need[me]
+            r0, r1 = max(rb, lo2), min(re_, hi2)
+            if r1 > r0:
+                ops.append(self.dist.P2POp(self.dist.irecv, t[r0:r1], r, self.group))
+        if ops:
+            for q in self.dist.batch_isend_irecv(ops):
+                q.wait()
 
 
 @dataclass
@@ -159,12 +190,47 @@ class Inpainter:
             b = V.NNF.alloc(npad, self.device, n=a.n, zero=False)
             z = lambda k: torch.empty((hpad, k), dtype=torch.float32, device=self.device)
             self.states.append(LevelState(lv, a, b, z(3), z(2), z(3), z(2)))
+        self.halo = self.cfg.exchange == "halo" and self.ex.world > 1
+        if self.halo:
+            self._halo_ranges()
         top = self.levels[-1]
         if top.layer is None:
             top.layer = torch.empty(top.N, dtype=torch.uint8, device=self.device)
         self.n_layers = self.V.layers(top, self.ws)
         self.stats.onion_layers = self.n_layers
         return counts
+
+    def _halo_ranges(self):
+        """Per level and rank: the NNF rows (targets within max(step) frames of the rank's target slab,
+        or within 2 frames of its hole slab) and the hole rows (within 2 frames of its target slab)
+        the rank reads.  Targets and holes are sorted t-major, so each is one contiguous range."""
+        smax = max(max(self.cfg.steps), 2)
+        for st in self.states:
+            lv = st.lv
+            hw = lv.W * lv.H
+            tf = (lv.targets[:lv.n_targets].cpu().to(torch.int64) // hw)
+            hf = (lv.holes[:lv.n_holes].cpu().to(torch.int64) // hw)
+
+            def rng(frames, f0, f1):
+                lo = int(torch.searchsorted(frames, torch.tensor(f0), right=False))
+                hi = int(torch.searchsorted(frames, torch.tensor(f1), right=True))
+                return lo, hi
+
+            nnf, hole = [], []
+            for (b, e), (hb, he) in zip(self.ex.slabs(lv.n_targets), self.ex.slabs(lv.n_holes)):
+                lo, hi = (0, 0)
+                hlo, hhi = (0, 0)
+                if e > b:
+                    f0, f1 = int(tf[b]), int(tf[e - 1])
+                    lo, hi = rng(tf, f0 - smax, f1 + smax)
+                    hlo, hhi = rng(hf, f0 - 2, f1 + 2)
+                if he > hb:
+                    g0, g1 = int(hf[hb]), int(hf[he - 1])
+                    l2, h2 = rng(tf, g0 - 2, g1 + 2)
+                    lo, hi = (l2, h2) if hi <= lo else (min(lo, l2), max(hi, h2))
+                nnf.append((lo, hi))
+                hole.append((hlo, hhi))
+            st.halo_nnf, st.halo_hole = nnf, hole
 
     # ------------------------------------------------------------------ ANN search (a5-a8)
     def ann_search(self, st: LevelState, outer_code: int, kb=-1, only_layer=-1, replicated=False):
@@ -175,7 +241,12 @@ class Inpainter:
                               self.counter, sign_policy=cfg.sign_policy)
             return
         b, e = self.ex.slab(n)
-        gather = (lambda t: None) if replicated else (lambda t: self.ex.gather(t, n))
+        if replicated:
+            gather = lambda t: None  # noqa: E731
+        elif self.halo:
+            gather = lambda t: self.ex.halo(t, n, st.halo_nnf)  # noqa: E731
+        else:
+            gather = lambda t: self.ex.gather(t, n)  # noqa: E731
         self.V.nnf_evaluate(lv, st.a, prm, kb, only_layer, b, e, self.counter)
         gather(st.a.e)
         gather(st.a.n)
@@ -189,15 +260,23 @@ class Inpainter:
             st.a, st.b = st.b, st.a
             gather(st.a.e)
 
-    def reconstruct(self, st: LevelState, mode: int, layer_j=-1, replicated=False):
+    def reconstruct(self, st: LevelState, mode: int, layer_j=-1, replicated=False, full=False):
         lv = st.lv
         n = lv.n_holes
         hb, he = (0, n) if replicated else self.ex.slab(n)
         self.V.reconstruct(lv, st.a, mode, st.cur_rgb, st.cur_tex, layer_j, hb, he, commit=True)
         if not replicated and self.ex.world > 1:
-            self.ex.gather(st.cur_rgb, n)
-            self.ex.gather(st.cur_tex, n)
-            self.V.commit(lv, st.cur_rgb, st.cur_tex, layer_j, 0, n)
+            if self.halo and not full:
+                # only the hole values this rank's target patches read (holes outside that range
+                # are never read here: sources lie in D~, which excludes H)
+                self.ex.halo(st.cur_rgb, n, st.halo_hole)
+                self.ex.halo(st.cur_tex, n, st.halo_hole)
+                lo, hi = st.halo_hole[self.ex.rank]
+                self.V.commit(lv, st.cur_rgb, st.cur_tex, layer_j, lo, hi)
+            else:
+                self.ex.gather(st.cur_rgb, n)
+                self.ex.gather(st.cur_tex, n)
+                self.V.commit(lv, st.cur_rgb, st.cur_tex, layer_j, 0, n)
 
     # ------------------------------------------------------------------ Alg. 3 onion peel
     def onion_peel(self):
@@ -264,8 +343,11 @@ class Inpainter:
                     if 10 * e_fixed <= 3 * lv.n_holes * (1 << 20) or k >= cfg.max_outer:
                         break
             if l == 1:
-                self.reconstruct(st, V.BEST_PATCH)  # Eq. 6
+                self.reconstruct(st, V.BEST_PATCH, full=True)  # Eq. 6; every rank gets u
             else:
+                if self.halo:  # upsampling reads the coarse NNF of any frame of the fine slab
+                    self.ex.gather(st.a.e, lv.n_targets)
+                    self.ex.gather(st.a.n, lv.n_targets)
                 f = self.states[l - 2]
                 fb, fe = self.ex.slab(f.lv.n_targets)
                 self.V.nnf_upsample(lv, st.a, f.lv, f.a, self.prm, fb, fe)

@@ -25,14 +25,19 @@ def _free_port():
     return p
 
 
-def _run(rank, world, port, out_path):
+def _vol(T):
+    return random_volume(40, 32, T, seed=4, hole_frac=0.06)
+
+
+def _run(rank, world, port, out_path, T=10, exchange="allgather"):
     os.environ.update(MASTER_ADDR="127.0.0.1", MASTER_PORT=str(port))
     dist.init_process_group("gloo", rank=rank, world_size=world)
     try:
         import oracle_ops
         from paper_1503_05528_b200 import Config, Exchange, inpaint
-        v, m, _ = random_volume(40, 32, 10, seed=4, hole_frac=0.06)
-        out, stats, ip = inpaint(v, m, Config(**CFG), device="cpu", exchange=Exchange(), ops=oracle_ops)
+        v, m, _ = _vol(T)
+        out, stats, ip = inpaint(v, m, Config(exchange=exchange, **CFG), device="cpu", exchange=Exchange(),
+                                 ops=oracle_ops)
         if rank == 0:
             np.save(out_path, out.numpy())
             np.save(out_path + ".stats.npy", np.array([l["outer"] for l in stats.levels] +
@@ -41,9 +46,9 @@ def _run(rank, world, port, out_path):
         dist.destroy_process_group()
 
 
-def _spawn(world, tmp_path):
-    out = str(tmp_path / f"out_w{world}.npy")
-    mp.spawn(_run, args=(world, _free_port(), out), nprocs=world, join=True)
+def _spawn(world, tmp_path, T=10, exchange="allgather"):
+    out = str(tmp_path / f"out_w{world}_{T}_{exchange}.npy")
+    mp.spawn(_run, args=(world, _free_port(), out, T, exchange), nprocs=world, join=True)
     return np.load(out), np.load(out + ".stats.npy")
 
 
@@ -71,3 +76,35 @@ def test_exchange_slabs_cover_and_pad():
     assert ex.padded(10) == 12 and spans == [(0, 4), (4, 8), (8, 10)]
     ex.rank = 2
     assert ex.slab(0) == (0, 0)
+
+
+@pytest.mark.parametrize("world", [2, 3])
+def test_halo_exchange_bit_identical(tmp_path, orc, world):
+    """NEXT #4 halo exchange: with 36 frames the slabs are ~12-18 frames, so every rank receives
+    only part of the other slabs (+-8 frames of NNF, +-2 frames of hole values); the result must
+    still equal the single-rank run and the oracle bit for bit."""
+    T = 36
+    o1, s1 = _spawn(1, tmp_path, T)
+    oh, sh = _spawn(world, tmp_path, T, "halo")
+    assert np.array_equal(o1, oh) and np.array_equal(s1, sh)
+    v, m, _ = _vol(T)
+    ref, st = orc.inpaint(v.numpy(), m.numpy(), CFG["levels"], pm_iters=CFG["pm_iters"],
+                          max_outer=CFG["max_outer"])
+    assert np.array_equal(o1, ref)
+
+
+def test_halo_ranges_are_partial():
+    """the halo really is partial for the test geometry (the exchange is exercised)"""
+    import torch
+    from paper_1503_05528_b200 import Config
+    from paper_1503_05528_b200.driver import Exchange, Inpainter
+    import oracle_ops
+    v, m, _ = _vol(36)
+    ex = Exchange()
+    ex.world, ex.rank = 3, 0
+    ip = Inpainter(40, 32, 36, Config(exchange="halo", **CFG), "cpu", ex, oracle_ops)
+    ip.load(v, m)
+    st = ip.states[0]
+    n = st.lv.n_targets
+    spans = [hi - lo for lo, hi in st.halo_nnf]
+    assert all(sp > 0 for sp in spans) and sum(sp < n for sp in spans) >= 2, (spans, n)
