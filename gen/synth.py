@@ -334,3 +334,18 @@ def camera_video(W, H, T, seed, cams, noise=0.0, block=None, device="cpu", cell=
             img = [v + noise * normal(pix, t, 90 + k, 3, seed) for k, v in enumerate(img)]
         out[t] = _round_u8(torch.stack(img, -1))
     return out
+
+
+def random_holes(W, H, T, seed, n=2, device="cpu"):
+    """Union of n seeded axis-aligned ellipsoids (random centre, radii 1..W/4 etc.; may touch or
+    cross the volume border) as a u8 [T, H, W] occlusion mask: fuzz inputs for parity tests."""
+    t = torch.arange(T, dtype=torch.float64, device=device).view(T, 1, 1)
+    y = torch.arange(H, dtype=torch.float64, device=device).view(1, H, 1)
+    x = torch.arange(W, dtype=torch.float64, device=device).view(1, 1, W)
+    m = torch.zeros((T, H, W), dtype=torch.bool, device=device)
+    for i in range(n):
+        u = [_scalar_uniform(10 + i, k, 77, 5, seed) for k in range(6)]
+        cx, cy, ct = u[0] * W, u[1] * H, u[2] * T
+        rx, ry, rt = 1 + u[3] * W / 4, 1 + u[4] * H / 4, 1 + u[5] * T / 3
+        m |= ((x - cx) / rx) ** 2 + ((y - cy) / ry) ** 2 + ((t - ct) / rt) ** 2 <= 1
+    return m.to(torch.uint8)
