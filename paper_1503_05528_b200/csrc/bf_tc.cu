@@ -71,7 +71,10 @@ __global__ void __launch_bounds__(128) k_tc_gemm_probe(const uint8_t* __restrict
 constexpr int kRow = 640;       // bytes per patch row: colour 384 (125*3 + 9 pad), texture 256 (250 + 6)
 constexpr int kColK = 384, kTexK = 256;
 constexpr int kTile = 128;      // M (targets) and N (sources) per tile
-constexpr int64_t kEPad = 1ll << 40;  // energy of padded source rows: never the minimum
+// Energies and distances fit in int32: D <= 4*125*3*255^2 + 126*125*2*255^2 = 2,145,825,000 < 2^31
+// for lambda <= 126 (vinp.h), hence also E(q) - 2X = D - E(p).  Padded rows get 2^31 - 1, which
+// no real E(q) - 2X reaches, so they never win (X = 0 for their zero operands).
+constexpr int32_t kEPad = 0x7fffffff;
 
 __device__ __forceinline__ bool full_patch(const Geo& g, int x, int y, int t) {
   return x >= 2 && x < g.W - 2 && y >= 2 && y < g.H - 2 && t >= 2 && t < g.T - 2;
@@ -81,7 +84,7 @@ __device__ __forceinline__ bool full_patch(const Geo& g, int x, int y, int t) {
 // grouped in tiles of TR rows; a tile is [colour: 24 K-chunks x TR/8 core matrices][texture: 16 x
 // TR/8], K byte k of row r at  part + (k/16)*TR*16 + (r/8)*128 + (r%8)*16 + k%16, so that a whole tile
 // is one contiguous block that a bulk (TMA) copy lands in shared memory ready for tcgen05.mma.
-// energy[i] = 4 sum c^2 + lambda sum t^2 (padded rows: zeros, energy kEPad).
+// energy[i] = 4 sum c^2 + lambda sum t^2 (int32, see kEPad; padded rows: zeros, energy kEPad).
 __device__ __forceinline__ size_t tiled_off(int i, int k, int TR) {
   int tile = i / TR, r = i % TR;
   size_t base = (size_t)tile * TR * kRow;
@@ -94,7 +97,7 @@ __device__ __forceinline__ size_t tiled_off(int i, int k, int TR) {
 
 __global__ void k_im2col_tiled(const uint64_t* __restrict__ vox, Geo g, const int32_t* __restrict__ pos,
                                const int32_t* __restrict__ idx, int32_t n, int32_t npad, int lambda, int TR,
-                               uint8_t* __restrict__ rows, int64_t* __restrict__ energy) {
+                               uint8_t* __restrict__ rows, int32_t* __restrict__ energy) {
   int i = blockIdx.x;  // one block (128 threads) per row
   if (i >= npad) return;
   if (i >= n) {
@@ -131,7 +134,7 @@ __global__ void k_im2col_tiled(const uint64_t* __restrict__ vox, Geo g, const in
   if (threadIdx.x == 0) {
     uint64_t c = 0, t = 0;
     for (int w = 0; w < (int)(blockDim.x >> 5); ++w) { c += sc[w]; t += st[w]; }
-    energy[i] = (int64_t)(4 * c + (uint64_t)lambda * t);
+    energy[i] = (int32_t)(4 * c + (uint64_t)lambda * t);
   }
 }
 
@@ -144,29 +147,40 @@ __global__ void k_im2col_tiled(const uint64_t* __restrict__ vox, Geo g, const in
 // Barriers: a_full; b_full[2] / b_empty[2] (producer <-> MMA); acc_full[2] / acc_empty[2] (MMA <->
 // epilogue, 128 arrivals).  All waits are bounded (trap instead of hang).
 constexpr int kTA = 128, kTB = 64;
+constexpr int kEpiWarps = 8, kBfThreads = 64 + 32 * kEpiWarps;  // producer, MMA, 8 epilogue warps
+#ifndef VINP_BF_BS
+#define VINP_BF_BS 2
+#endif
+#ifndef VINP_BF_AS
+#define VINP_BF_AS 2
+#endif
+constexpr int kBS = VINP_BF_BS, kAS = VINP_BF_AS;  // B smem ring / TMEM accumulator ring depths
 constexpr uint32_t kABytes = kTA * kRow, kBBytes = kTB * kRow;
 
-__global__ void __launch_bounds__(192, 1) k_bf_tc2(const uint8_t* __restrict__ A, const int64_t* __restrict__ Ep,
-                                                   const uint8_t* __restrict__ B, const int64_t* __restrict__ Eq,
-                                                   int nb_tiles, int tiles_per_chunk, int lambda, int32_t mpad,
-                                                   uint64_t* __restrict__ out) {
+__global__ void __launch_bounds__(kBfThreads, 1) k_bf_tc2(const uint8_t* __restrict__ A, const int32_t* __restrict__ Ep,
+                                                          const uint8_t* __restrict__ B, const int32_t* __restrict__ Eq,
+                                                          int nb_tiles, int tiles_per_chunk, int lambda, int32_t mpad,
+                                                          int32_t nsrc, uint64_t* __restrict__ out) {
   extern __shared__ __align__(1024) uint8_t sm[];
   uint8_t* sA = sm;
   uint8_t* sB0 = sm + kABytes;
-  __shared__ uint64_t bar[9];  // 0 a_full, 1-2 b_full, 3-4 b_empty, 5-6 acc_full, 7-8 acc_empty
+  // barriers: a_full; b_full[kBS]; b_empty[kBS]; acc_full[kAS]; acc_empty[kAS]
+  __shared__ uint64_t bar[1 + 2 * kBS + 2 * kAS];
+  uint64_t* const bfull = bar + 1;
+  uint64_t* const bempty = bar + 1 + kBS;
+  uint64_t* const afull = bar + 1 + 2 * kBS;
+  uint64_t* const aempty = bar + 1 + 2 * kBS + kAS;
   __shared__ uint32_t tmem_base;
   int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
   int mt = blockIdx.x;
   int t0 = blockIdx.y * tiles_per_chunk, t1 = min(nb_tiles, t0 + tiles_per_chunk);
   int nt = max(0, t1 - t0);
   if (tid == 0) {
-    tc::mbar_init(&bar[0], 1);
-    for (int k = 1; k <= 6; ++k) tc::mbar_init(&bar[k], 1);
-    tc::mbar_init(&bar[7], 128);
-    tc::mbar_init(&bar[8], 128);
+    for (int k = 0; k < 1 + 2 * kBS + kAS; ++k) tc::mbar_init(&bar[k], 1);
+    for (int k = 0; k < kAS; ++k) tc::mbar_init(&aempty[k], 32 * kEpiWarps);
     tc::fence_mbar_init();
   }
-  if (warp == 1) tc::tmem_alloc(&tmem_base, 256);
+  if (warp == 1) tc::tmem_alloc(&tmem_base, 128 * kAS);
   tc::fence_before();
   __syncthreads();
   tc::fence_after();
@@ -177,13 +191,13 @@ __global__ void __launch_bounds__(192, 1) k_bf_tc2(const uint8_t* __restrict__ A
       tc::mbar_expect_tx(&bar[0], kABytes);
       for (uint32_t o = 0; o < kABytes; o += 16384) tc::bulk_g2s(sA + o, ga + o, min(16384u, kABytes - o), &bar[0]);
       for (int i = 0; i < nt; ++i) {
-        int st = i & 1;
-        uint32_t ph = (i >> 1) & 1;
-        tc::mbar_wait(&bar[3 + st], ph ^ 1);
+        int st = i % kBS;
+        uint32_t ph = (i / kBS) & 1;
+        tc::mbar_wait(&bempty[st], ph ^ 1);
         uint8_t* sb = sB0 + st * kBBytes;
         const uint8_t* gb = B + (size_t)(t0 + i) * kBBytes;
-        tc::mbar_expect_tx(&bar[1 + st], kBBytes);
-        for (uint32_t o = 0; o < kBBytes; o += 16384) tc::bulk_g2s(sb + o, gb + o, min(16384u, kBBytes - o), &bar[1 + st]);
+        tc::mbar_expect_tx(&bfull[st], kBBytes);
+        for (uint32_t o = 0; o < kBBytes; o += 16384) tc::bulk_g2s(sb + o, gb + o, min(16384u, kBBytes - o), &bfull[st]);
       }
     }
   } else if (warp == 1) {
@@ -192,13 +206,12 @@ __global__ void __launch_bounds__(192, 1) k_bf_tc2(const uint8_t* __restrict__ A
       const uint32_t ac = tc::smem_u32(sA), at = ac + kTA * kColK;
       tc::mbar_wait(&bar[0], 0);
       for (int i = 0; i < nt; ++i) {
-        int st = i & 1;
-        uint32_t ph = (i >> 1) & 1;
-        tc::mbar_wait(&bar[1 + st], ph);
-        tc::mbar_wait(&bar[7 + st], ph ^ 1);
+        int st = i % kBS, sa = i % kAS;
+        tc::mbar_wait(&bfull[st], (i / kBS) & 1);
+        tc::mbar_wait(&aempty[sa], ((i / kAS) & 1) ^ 1);
         tc::fence_after();
         uint32_t bc = tc::smem_u32(sB0 + st * kBBytes), bt = bc + kTB * kColK;
-        uint32_t dc = tm + st * 128, dt = dc + 64;
+        uint32_t dc = tm + sa * 128, dt = dc + 64;
 #pragma unroll
         for (int j = 0; j < kColK / 32; ++j)
           tc::mma_u8(dc, tc::desc_kmajor(ac + 2 * j * (kTA * 16), kTA * 16, 128),
@@ -207,48 +220,78 @@ __global__ void __launch_bounds__(192, 1) k_bf_tc2(const uint8_t* __restrict__ A
         for (int j = 0; j < kTexK / 32; ++j)
           tc::mma_u8(dt, tc::desc_kmajor(at + 2 * j * (kTA * 16), kTA * 16, 128),
                      tc::desc_kmajor(bt + 2 * j * (kTB * 16), kTB * 16, 128), id, j > 0);
-        tc::commit(&bar[3 + st]);  // B stage free once these MMAs have read it
-        tc::commit(&bar[5 + st]);  // accumulator stage ready
+        tc::commit(&bempty[st]);  // B stage free once these MMAs have read it
+        tc::commit(&afull[sa]);   // accumulator stage ready
       }
     }
   } else {
-    const int q = warp & 3;  // TMEM lane quarter accessible to this warp
+    // 8 epilogue warps: warp w reads TMEM lane quarter w % 4 (the hardware rule), and the two warps
+    // of a quarter split each tile's 64 columns.  D = E(p) + E(q) - 2 (4 X_c + lambda X_t) is
+    // evaluated mod 2^32, which is exact because 0 <= D < 2^32 for lambda <= 126 (vinp.h).
+    const int q = warp & 3;
+    const int h = warp >= 2 + kEpiWarps / 2 ? 1 : 0;
     const int row = 32 * q + lane;
-    int64_t bestD = INT64_MAX;
+    // per row: the minimum over sources of s = E(q) - 2 (4 X_c + lambda X_t) = D - E(p) (int32,
+    // exact), first index on ties; per tile one min per column, and the first-index search only
+    // when the tile improves the running minimum (strict, so earlier tiles win ties)
+    int32_t bestS = 0x7fffffff;
     int bestI = 0x7fffffff;
     for (int i = 0; i < nt; ++i) {
-      int st = i & 1;
-      uint32_t ph = (i >> 1) & 1;
-      tc::mbar_wait(&bar[5 + st], ph);
+      int sa = i % kAS;
+      tc::mbar_wait(&afull[sa], (i / kAS) & 1);
       tc::fence_after();
-      uint32_t c0[32], c1[32], x0[32], x1[32];
-      uint32_t base = tm + ((uint32_t)(32 * q) << 16) + st * 128;
-      tc::tmem_ld32(base + 0, c0);
-      tc::tmem_ld32(base + 32, c1);
-      tc::tmem_ld32(base + 64, x0);
-      tc::tmem_ld32(base + 96, x1);
+      uint32_t c[32], x[32];
+      uint32_t base = tm + ((uint32_t)(32 * q) << 16) + sa * 128 + 32 * h;
+      tc::tmem_ld32x2(base + 0, base + 64, c, x);
       tc::fence_before();
-      tc::mbar_arrive(&bar[7 + st]);  // accumulator stage drained
-      const int64_t* E = Eq + (size_t)(t0 + i) * kTB;
-      int cbase = (t0 + i) * kTB;
+      tc::mbar_arrive(&aempty[sa]);  // accumulator stage drained (by this thread)
+      const int cbase = (t0 + i) * kTB + 32 * h;
+      const int4* E4 = reinterpret_cast<const int4*>(Eq + cbase);  // 16-B aligned: cbase % 4 == 0
+      int32_t sv[32];
+      int32_t tmin = 0x7fffffff;
 #pragma unroll
-      for (int j = 0; j < 32; ++j) {
-        int64_t d = __ldg(E + j) - 2 * (4 * (int64_t)c0[j] + (int64_t)lambda * (int64_t)x0[j]);
-        if (d < bestD) { bestD = d; bestI = cbase + j; }
+      for (int j4 = 0; j4 < 8; ++j4) {
+        int4 ev = __ldg(E4 + j4);
+        const int32_t e4[4] = {ev.x, ev.y, ev.z, ev.w};
+#pragma unroll
+        for (int u = 0; u < 4; ++u) {
+          const int j = 4 * j4 + u;
+          sv[j] = (int32_t)((uint32_t)e4[u] - 2u * (4u * c[j] + (uint32_t)lambda * x[j]));  // exact mod 2^32
+          tmin = min(tmin, sv[j]);
+        }
       }
+      if (tmin < bestS) {
+        int jf = 31;
 #pragma unroll
-      for (int j = 0; j < 32; ++j) {
-        int64_t d = __ldg(E + 32 + j) - 2 * (4 * (int64_t)c1[j] + (int64_t)lambda * (int64_t)x1[j]);
-        if (d < bestD) { bestD = d; bestI = cbase + 32 + j; }
+        for (int j = 31; j >= 0; --j)
+          if (sv[j] == tmin) jf = j;
+        bestS = tmin;
+        bestI = cbase + jf;
       }
     }
-    int64_t D = bestD + Ep[(size_t)mt * kTA + row];
-    uint64_t packed = bestI == 0x7fffffff ? ~0ull : (((uint64_t)(uint32_t)D << 32) | (uint32_t)bestI);
-    out[(size_t)blockIdx.y * mpad + (size_t)mt * kTA + row] = packed;
+    uint32_t bestD = (uint32_t)Ep[(size_t)mt * kTA + row] + (uint32_t)bestS;  // = D, exact mod 2^32
+    // merge the two column halves of each row: lexicographic (D, index) minimum
+    __shared__ uint32_t mD[kTA];
+    __shared__ int mI[kTA];
+    if (h == 1) {
+      mD[row] = bestD;
+      mI[row] = bestI;
+    }
+    asm volatile("bar.sync 1, %0;" ::"r"(32 * kEpiWarps));  // epilogue warps only
+    if (h == 0) {
+      uint32_t D2 = mD[row];
+      int I2 = mI[row];
+      if (D2 < bestD || (D2 == bestD && I2 < bestI)) {
+        bestD = D2;
+        bestI = I2;
+      }
+      uint64_t packed = bestI == 0x7fffffff ? ~0ull : (((uint64_t)bestD << 32) | (uint32_t)bestI);
+      out[(size_t)blockIdx.y * mpad + (size_t)mt * kTA + row] = packed;
+    }
   }
   tc::fence_before();
   __syncthreads();
-  if (warp == 1) tc::tmem_free(tm, 256);
+  if (warp == 1) tc::tmem_free(tm, 128 * kAS);
 }
 
 // Clip pattern of a target patch: how many voxel layers fall outside Omega on each side of each
@@ -279,7 +322,7 @@ __global__ void k_pid_scatter(const int32_t* __restrict__ targets, Geo g, int32_
 }
 // per-source energy over the sub-box of a clip pattern: 4 sum c^2 + lambda sum t^2
 __global__ void k_energy_box(const uint64_t* __restrict__ vox, Geo g, const int32_t* __restrict__ sources,
-                             int32_t n, int32_t npad, int lambda, int pid, int64_t* __restrict__ E) {
+                             int32_t n, int32_t npad, int lambda, int pid, int32_t* __restrict__ E) {
   int i = blockIdx.x * blockDim.x + threadIdx.x;
   if (i >= npad) return;
   if (i >= n) { E[i] = kEPad; return; }
@@ -294,7 +337,7 @@ __global__ void k_energy_box(const uint64_t* __restrict__ vox, Geo g, const int3
         c += c0 * c0 + c1 * c1 + c2 * c2;
         tt += t0 * t0 + t1 * t1;
       }
-  E[i] = (int64_t)(4 * c + (uint64_t)lambda * tt);
+  E[i] = (int32_t)(4 * c + (uint64_t)lambda * tt);
 }
 
 // merge the split minima (lexicographic (D, index) = smallest D, then smallest source index)
@@ -352,9 +395,9 @@ vinp_status vinp_brute_force_tc(const vinp_level* lv, vinp_nnf* out, const vinp_
   char* w = (char*)(((uintptr_t)ws + 1023) & ~(uintptr_t)1023);
   uint8_t* A = (uint8_t*)w; w += (mpad + kTA * 8) * kRow;
   uint8_t* B = (uint8_t*)w; w += npad * kRow;
-  int64_t* Ep = (int64_t*)w; w += (mpad + kTA * 8) * 8;
-  int64_t* Eq = (int64_t*)w; w += npad * 8;
-  int64_t* Eb = (int64_t*)w; w += npad * 8;  // per-pattern source energies
+  int32_t* Ep = (int32_t*)w; w += (mpad + kTA * 8) * 8;
+  int32_t* Eq = (int32_t*)w; w += npad * 8;
+  int32_t* Eb = (int32_t*)w; w += npad * 8;  // per-pattern source energies
   int32_t* list = (int32_t*)w; w += mpad * 4;
   int32_t* cnt = (int32_t*)(((uintptr_t)w + 63) & ~(uintptr_t)63); w = (char*)(cnt + 2 * kPids);
   uint64_t* part = (uint64_t*)(((uintptr_t)w + 63) & ~(uintptr_t)63);
@@ -377,7 +420,7 @@ vinp_status vinp_brute_force_tc(const vinp_level* lv, vinp_nnf* out, const vinp_
   int nb_tiles = (int)(np / kTB);
   int per = std::max(1, std::min(nb_tiles, (int)((64ll << 20) / kBBytes)));
   int chunks = (nb_tiles + per - 1) / per;
-  size_t smem = kABytes + 2 * (size_t)kBBytes;
+  size_t smem = kABytes + kBS * (size_t)kBBytes;
   cudaFuncSetAttribute(k_bf_tc2, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
   // 3. one warp-specialised tensor-core GEMM + exact argmin per clip pattern
   for (int pid = 0; pid < kPids; ++pid) {
@@ -385,7 +428,7 @@ vinp_status vinp_brute_force_tc(const vinp_level* lv, vinp_nnf* out, const vinp_
     if (m == 0) continue;
     int32_t mp = (m + kTA - 1) / kTA * kTA;
     const int32_t* lst = list + off[pid];
-    const int64_t* E = Eq;
+    const int32_t* E = Eq;
     if (pid != 0) {
       k_energy_box<<<nblk(np, 256), 256, 0, s>>>(lv->vox, g, lv->sources, lv->n_sources, (int)np, prm->lambda, pid, Eb);
       count_launch();
@@ -393,7 +436,8 @@ vinp_status vinp_brute_force_tc(const vinp_level* lv, vinp_nnf* out, const vinp_
     }
     int nvox = (5 - pid % 3 - pid / 3 % 3) * (5 - pid / 9 % 3 - pid / 27 % 3) * (5 - pid / 81 % 3 - pid / 243);
     k_im2col_tiled<<<mp, 128, 0, s>>>(lv->vox, g, lv->targets, lst, m, mp, prm->lambda, kTA, A, Ep);
-    k_bf_tc2<<<dim3(mp / kTA, chunks), 192, smem, s>>>(A, Ep, B, E, nb_tiles, per, prm->lambda, mp, part);
+    k_bf_tc2<<<dim3(mp / kTA, chunks), kBfThreads, smem, s>>>(A, Ep, B, E, nb_tiles, per, prm->lambda, mp,
+                                                           lv->n_sources, part);
     k_bf_merge<<<nblk(m, 256), 256, 0, s>>>(part, chunks, mp, m, lst, lv->sources, out->e, out->n, nvox);
     count_launch(3);
   }
