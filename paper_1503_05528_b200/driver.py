@@ -413,8 +413,10 @@ def inpaint(rgb: torch.Tensor, mask: torch.Tensor, cfg: Config, device="cuda", e
     ip = _PLANS.get(key)
     if ip is None:
         ip = _PLANS[key] = Inpainter(W, H, T, cfg, device, exchange, ops)
-    rgb_d = rgb.to(device, non_blocking=True)
-    mask_d = mask.to(device, non_blocking=True)
+    if rgb.dtype != torch.uint8 or tuple(rgb.shape[3:]) != (3,) or tuple(mask.shape) != (T, H, W):
+        raise ValueError("inpaint: rgb must be u8 [T, H, W, 3] and mask [T, H, W]")
+    rgb_d = rgb.to(device, non_blocking=True).contiguous()
+    mask_d = mask.to(device, dtype=torch.uint8, non_blocking=True).contiguous()
     if cfg.align:
         a_rgb, a_mask = ip.align(rgb_d, mask_d)
         ip.load(a_rgb, a_mask)
