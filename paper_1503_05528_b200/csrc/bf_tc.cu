@@ -146,41 +146,40 @@ __global__ void k_im2col_tiled(const uint64_t* __restrict__ vox, Geo g, const in
 //         (D, index) minimum per target row (strict <, ascending sources: first minimum).
 // Barriers: a_full; b_full[2] / b_empty[2] (producer <-> MMA); acc_full[2] / acc_empty[2] (MMA <->
 // epilogue, 128 arrivals).  All waits are bounded (trap instead of hang).
-constexpr int kTA = 128, kTB = 64;
+constexpr int kTA = 128, kTB = 128;
 constexpr int kEpiWarps = 8, kBfThreads = 64 + 32 * kEpiWarps;  // producer, MMA, 8 epilogue warps
-#ifndef VINP_BF_BS
-#define VINP_BF_BS 2
-#endif
-#ifndef VINP_BF_AS
-#define VINP_BF_AS 2
-#endif
-constexpr int kBS = VINP_BF_BS, kAS = VINP_BF_AS;  // B smem ring / TMEM accumulator ring depths
 constexpr uint32_t kABytes = kTA * kRow, kBBytes = kTB * kRow;
+constexpr uint32_t kBColBytes = kTB * kColK, kBTexBytes = kTB * kTexK;  // the two parts of a B tile
 
+// N = 128 source columns per MMA (M128 N128 K32: half the A re-reads from shared memory per MAC
+// of N = 64).  A source tile (80 KB) is streamed in its two parts — colour (48 KB) into shared
+// stage 0, texture (32 KB) into stage 1 — so the next tile's colour part loads while this tile's
+// texture MMAs run: 80 KB (A) + 2 x 48 KB of shared memory.  TMEM: 2 accumulator stages x (128
+// colour + 128 texture columns) = 512 columns.
 __global__ void __launch_bounds__(kBfThreads, 1) k_bf_tc2(const uint8_t* __restrict__ A, const int32_t* __restrict__ Ep,
                                                           const uint8_t* __restrict__ B, const int32_t* __restrict__ Eq,
                                                           int nb_tiles, int tiles_per_chunk, int lambda, int32_t mpad,
                                                           int32_t nsrc, uint64_t* __restrict__ out) {
   extern __shared__ __align__(1024) uint8_t sm[];
   uint8_t* sA = sm;
-  uint8_t* sB0 = sm + kABytes;
-  // barriers: a_full; b_full[kBS]; b_empty[kBS]; acc_full[kAS]; acc_empty[kAS]
-  __shared__ uint64_t bar[1 + 2 * kBS + 2 * kAS];
+  uint8_t* sB[2] = {sm + kABytes, sm + kABytes + kBColBytes};  // colour part, texture part
+  // barriers: a_full; b_full[2] / b_empty[2] (colour / texture part); acc_full[2] / acc_empty[2]
+  __shared__ uint64_t bar[9];
   uint64_t* const bfull = bar + 1;
-  uint64_t* const bempty = bar + 1 + kBS;
-  uint64_t* const afull = bar + 1 + 2 * kBS;
-  uint64_t* const aempty = bar + 1 + 2 * kBS + kAS;
+  uint64_t* const bempty = bar + 3;
+  uint64_t* const afull = bar + 5;
+  uint64_t* const aempty = bar + 7;
   __shared__ uint32_t tmem_base;
   int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
   int mt = blockIdx.x;
   int t0 = blockIdx.y * tiles_per_chunk, t1 = min(nb_tiles, t0 + tiles_per_chunk);
   int nt = max(0, t1 - t0);
   if (tid == 0) {
-    for (int k = 0; k < 1 + 2 * kBS + kAS; ++k) tc::mbar_init(&bar[k], 1);
-    for (int k = 0; k < kAS; ++k) tc::mbar_init(&aempty[k], 32 * kEpiWarps);
+    for (int k = 0; k < 7; ++k) tc::mbar_init(&bar[k], 1);
+    for (int k = 0; k < 2; ++k) tc::mbar_init(&aempty[k], 32 * kEpiWarps);
     tc::fence_mbar_init();
   }
-  if (warp == 1) tc::tmem_alloc(&tmem_base, 128 * kAS);
+  if (warp == 1) tc::tmem_alloc(&tmem_base, 512);
   tc::fence_before();
   __syncthreads();
   tc::fence_after();
@@ -191,83 +190,91 @@ __global__ void __launch_bounds__(kBfThreads, 1) k_bf_tc2(const uint8_t* __restr
       tc::mbar_expect_tx(&bar[0], kABytes);
       for (uint32_t o = 0; o < kABytes; o += 16384) tc::bulk_g2s(sA + o, ga + o, min(16384u, kABytes - o), &bar[0]);
       for (int i = 0; i < nt; ++i) {
-        int st = i % kBS;
-        uint32_t ph = (i / kBS) & 1;
-        tc::mbar_wait(&bempty[st], ph ^ 1);
-        uint8_t* sb = sB0 + st * kBBytes;
         const uint8_t* gb = B + (size_t)(t0 + i) * kBBytes;
-        tc::mbar_expect_tx(&bfull[st], kBBytes);
-        for (uint32_t o = 0; o < kBBytes; o += 16384) tc::bulk_g2s(sb + o, gb + o, min(16384u, kBBytes - o), &bfull[st]);
+#pragma unroll
+        for (int part = 0; part < 2; ++part) {
+          const uint32_t nb = part ? kBTexBytes : kBColBytes;
+          const uint8_t* src = gb + (part ? kBColBytes : 0);
+          tc::mbar_wait(&bempty[part], (i & 1) ^ 1);
+          tc::mbar_expect_tx(&bfull[part], nb);
+          for (uint32_t o = 0; o < nb; o += 16384) tc::bulk_g2s(sB[part] + o, src + o, min(16384u, nb - o), &bfull[part]);
+        }
       }
     }
   } else if (warp == 1) {
     if (lane == 0) {
       const uint32_t id = tc::idesc_u8(kTA, kTB);
       const uint32_t ac = tc::smem_u32(sA), at = ac + kTA * kColK;
+      const uint32_t bc = tc::smem_u32(sB[0]), bt = tc::smem_u32(sB[1]);
       tc::mbar_wait(&bar[0], 0);
       for (int i = 0; i < nt; ++i) {
-        int st = i % kBS, sa = i % kAS;
-        tc::mbar_wait(&bfull[st], (i / kBS) & 1);
-        tc::mbar_wait(&aempty[sa], ((i / kAS) & 1) ^ 1);
+        const int sa = i & 1;
+        const uint32_t dc = tm + sa * 256, dt = dc + 128;
+        tc::mbar_wait(&aempty[sa], ((i >> 1) & 1) ^ 1);
+        tc::mbar_wait(&bfull[0], i & 1);
         tc::fence_after();
-        uint32_t bc = tc::smem_u32(sB0 + st * kBBytes), bt = bc + kTB * kColK;
-        uint32_t dc = tm + sa * 128, dt = dc + 64;
 #pragma unroll
         for (int j = 0; j < kColK / 32; ++j)
           tc::mma_u8(dc, tc::desc_kmajor(ac + 2 * j * (kTA * 16), kTA * 16, 128),
                      tc::desc_kmajor(bc + 2 * j * (kTB * 16), kTB * 16, 128), id, j > 0);
+        tc::commit(&bempty[0]);  // colour part free once these MMAs have read it
+        tc::mbar_wait(&bfull[1], i & 1);
+        tc::fence_after();
 #pragma unroll
         for (int j = 0; j < kTexK / 32; ++j)
           tc::mma_u8(dt, tc::desc_kmajor(at + 2 * j * (kTA * 16), kTA * 16, 128),
                      tc::desc_kmajor(bt + 2 * j * (kTB * 16), kTB * 16, 128), id, j > 0);
-        tc::commit(&bempty[st]);  // B stage free once these MMAs have read it
-        tc::commit(&afull[sa]);   // accumulator stage ready
+        tc::commit(&bempty[1]);  // texture part free
+        tc::commit(&afull[sa]);  // accumulator stage ready
       }
     }
   } else {
-    // 8 epilogue warps: warp w reads TMEM lane quarter w % 4 (the hardware rule), and the two warps
-    // of a quarter split each tile's 64 columns.  D = E(p) + E(q) - 2 (4 X_c + lambda X_t) is
-    // evaluated mod 2^32, which is exact because 0 <= D < 2^32 for lambda <= 126 (vinp.h).
+    // 8 epilogue warps: warp w reads TMEM lane quarter w % 4 (the hardware rule); the two warps of
+    // a quarter take 64 of the tile's 128 columns each, in two chunks of 32.  Per row the minimum
+    // over sources of s = E(q) - 2 (4 X_c + lambda X_t) = D - E(p) (int32, exact: D < 2^31 for
+    // lambda <= 126), first index on ties; per chunk one min per column, and the first-index search
+    // only when the chunk improves the running minimum (strict, so earlier columns win ties).
     const int q = warp & 3;
     const int h = warp >= 2 + kEpiWarps / 2 ? 1 : 0;
     const int row = 32 * q + lane;
-    // per row: the minimum over sources of s = E(q) - 2 (4 X_c + lambda X_t) = D - E(p) (int32,
-    // exact), first index on ties; per tile one min per column, and the first-index search only
-    // when the tile improves the running minimum (strict, so earlier tiles win ties)
     int32_t bestS = 0x7fffffff;
     int bestI = 0x7fffffff;
     for (int i = 0; i < nt; ++i) {
-      int sa = i % kAS;
-      tc::mbar_wait(&afull[sa], (i / kAS) & 1);
+      const int sa = i & 1;
+      tc::mbar_wait(&afull[sa], (i >> 1) & 1);
       tc::fence_after();
-      uint32_t c[32], x[32];
-      uint32_t base = tm + ((uint32_t)(32 * q) << 16) + sa * 128 + 32 * h;
-      tc::tmem_ld32x2(base + 0, base + 64, c, x);
-      tc::fence_before();
-      tc::mbar_arrive(&aempty[sa]);  // accumulator stage drained (by this thread)
-      const int cbase = (t0 + i) * kTB + 32 * h;
-      const int4* E4 = reinterpret_cast<const int4*>(Eq + cbase);  // 16-B aligned: cbase % 4 == 0
-      int32_t sv[32];
-      int32_t tmin = 0x7fffffff;
+#pragma unroll 1
+      for (int ch = 0; ch < 2; ++ch) {
+        const int col = 64 * h + 32 * ch;
+        uint32_t c[32], x[32];
+        uint32_t base = tm + ((uint32_t)(32 * q) << 16) + sa * 256 + col;
+        tc::tmem_ld32x2(base, base + 128, c, x);
+        const int cbase = (t0 + i) * kTB + col;
+        const int4* E4 = reinterpret_cast<const int4*>(Eq + cbase);  // 16-B aligned: cbase % 4 == 0
+        int32_t sv[32];
+        int32_t tmin = 0x7fffffff;
 #pragma unroll
-      for (int j4 = 0; j4 < 8; ++j4) {
-        int4 ev = __ldg(E4 + j4);
-        const int32_t e4[4] = {ev.x, ev.y, ev.z, ev.w};
+        for (int j4 = 0; j4 < 8; ++j4) {
+          int4 ev = __ldg(E4 + j4);
+          const int32_t e4[4] = {ev.x, ev.y, ev.z, ev.w};
 #pragma unroll
-        for (int u = 0; u < 4; ++u) {
-          const int j = 4 * j4 + u;
-          sv[j] = (int32_t)((uint32_t)e4[u] - 2u * (4u * c[j] + (uint32_t)lambda * x[j]));  // exact mod 2^32
-          tmin = min(tmin, sv[j]);
+          for (int u = 0; u < 4; ++u) {
+            const int j = 4 * j4 + u;
+            sv[j] = (int32_t)((uint32_t)e4[u] - 2u * (4u * c[j] + (uint32_t)lambda * x[j]));  // exact mod 2^32
+            tmin = min(tmin, sv[j]);
+          }
+        }
+        if (tmin < bestS) {
+          int jf = 31;
+#pragma unroll
+          for (int j = 31; j >= 0; --j)
+            if (sv[j] == tmin) jf = j;
+          bestS = tmin;
+          bestI = cbase + jf;
         }
       }
-      if (tmin < bestS) {
-        int jf = 31;
-#pragma unroll
-        for (int j = 31; j >= 0; --j)
-          if (sv[j] == tmin) jf = j;
-        bestS = tmin;
-        bestI = cbase + jf;
-      }
+      tc::fence_before();
+      tc::mbar_arrive(&aempty[sa]);  // accumulator stage drained (by this thread)
     }
     uint32_t bestD = (uint32_t)Ep[(size_t)mt * kTA + row] + (uint32_t)bestS;  // = D, exact mod 2^32
     // merge the two column halves of each row: lexicographic (D, index) minimum
@@ -291,7 +298,7 @@ __global__ void __launch_bounds__(kBfThreads, 1) k_bf_tc2(const uint8_t* __restr
   }
   tc::fence_before();
   __syncthreads();
-  if (warp == 1) tc::tmem_free(tm, 128 * kAS);
+  if (warp == 1) tc::tmem_free(tm, 512);
 }
 
 // Clip pattern of a target patch: how many voxel layers fall outside Omega on each side of each
@@ -420,7 +427,7 @@ vinp_status vinp_brute_force_tc(const vinp_level* lv, vinp_nnf* out, const vinp_
   int nb_tiles = (int)(np / kTB);
   int per = std::max(1, std::min(nb_tiles, (int)((64ll << 20) / kBBytes)));
   int chunks = (nb_tiles + per - 1) / per;
-  size_t smem = kABytes + kBS * (size_t)kBBytes;
+  size_t smem = kABytes + 2 * (size_t)kBColBytes;
   cudaFuncSetAttribute(k_bf_tc2, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
   // 3. one warp-specialised tensor-core GEMM + exact argmin per clip pattern
   for (int pid = 0; pid < kPids; ++pid) {
