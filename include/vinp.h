@@ -235,6 +235,8 @@ vinp_status vinp_patch_ambiguity(int N, double sigma, uint64_t seed, uint64_t tr
  *   status[n] = 0, or 1 = degenerate (fewer than 12 voters or singular normal equations), in
  *   which case theta[n] = identity; iters[n] = IRLS iterations run.  Deterministic and
  *   bit-identical to the oracle (exact fixed-point sums, no FMA contraction).  One 8-CTA cluster per pair.
+ *   Only pairs n in [pair_b, pair_e) are estimated (pair_e < 0: up to T-1), so ranks can split the
+ *   independent pairs; rows outside the range are not written.
  *   ws: vinp_affine_ws_bytes(W, H, T, levels) (grey pyramids + |r| keys).
  * vinp_affine_chain: fwd[n] = theta_{n,N_m} (frame n -> reference frame N_m = max(T/2 - 1, 0),
  *   0-based, R39) by the products of Alg. 2, inv[n] = fwd[n]^-1; *err (device) = 1 if a map
@@ -246,8 +248,8 @@ vinp_status vinp_patch_ambiguity(int N, double sigma, uint64_t seed, uint64_t tr
  *   aligned video sampled bilinearly at fwd[n](x) (clamp-to-edge, rounded half up) (R40). */
 size_t vinp_affine_ws_bytes(int W, int H, int T, int levels);
 vinp_status vinp_affine_estimate(const uint8_t* rgb, const uint8_t* mask, int W, int H, int T, int levels,
-                                 int max_iter, double tol, double* theta, int32_t* status, int32_t* iters,
-                                 void* ws, size_t ws_bytes, void* stream);
+                                 int max_iter, double tol, int32_t pair_b, int32_t pair_e, double* theta,
+                                 int32_t* status, int32_t* iters, void* ws, size_t ws_bytes, void* stream);
 vinp_status vinp_affine_chain(const double* pairs, int T, double* fwd, double* inv, int32_t* err,
                               void* stream);
 vinp_status vinp_align_warp(const uint8_t* rgb, const uint8_t* mask, int W, int H, int T, const double* inv,

@@ -343,6 +343,14 @@ def sets_x(occ, inv):
     return src, tgt
 
 
+def mask_down(m):
+    T, H, W = m.shape
+    out = np.zeros((T, (H + 1) // 2, (W + 1) // 2), np.uint8)
+    m = np.ascontiguousarray(m, np.uint8)
+    lib().or_mask_down(_p(m), W, H, T, _p(out))
+    return out
+
+
 def affine_compose(t2, t1):
     out = np.zeros(6)
     a, b = _th(t2), _th(t1)

@@ -636,8 +636,8 @@ size_t vinp_affine_ws_bytes(int W, int H, int T, int levels) {
 }
 
 vinp_status vinp_affine_estimate(const uint8_t* rgb, const uint8_t* mask, int W, int H, int T, int levels,
-                                 int max_iter, double tol, double* theta, int32_t* status, int32_t* iters,
-                                 void* ws, size_t ws_bytes, void* stream) {
+                                 int max_iter, double tol, int32_t pair_b, int32_t pair_e, double* theta,
+                                 int32_t* status, int32_t* iters, void* ws, size_t ws_bytes, void* stream) {
   VINP_REQUIRE(rgb && mask && theta && status && iters && ws, "vinp_affine_estimate: null argument");
   VINP_REQUIRE(W >= 2 && H >= 2 && T >= 1 && levels >= 1 && levels <= 8 && max_iter >= 0,
                "vinp_affine_estimate: bad sizes");
@@ -660,21 +660,24 @@ vinp_status vinp_affine_estimate(const uint8_t* rgb, const uint8_t* mask, int W,
     k_mask_dil<<<g, 128, 0, s>>>(w.M[k], w.D[k], w.W[k], w.H[k]);
     count_launch();
   }
-  int np = T - 1;
+  const int p0 = pair_b < 0 ? 0 : pair_b, p1 = (pair_e < 0 || pair_e > T - 1) ? T - 1 : pair_e;
+  const int np = p1 - p0;  // pairs [p0, p1): theta/status/iters rows p0.., internal state 0..np-1
+  if (np <= 0) return check_launch("vinp_affine_estimate");
   double sc = (double)(w.W[L - 1] > w.H[L - 1] ? w.W[L - 1] : w.H[L - 1]) * 0.5;
-  k_affine_init<<<(np + 127) / 128, 128, 0, s>>>(w.p, status, iters, np, sc);
+  k_affine_init<<<(np + 127) / 128, 128, 0, s>>>(w.p, status + p0, iters + p0, np, sc);
   count_launch();
   for (int k = L - 1; k >= 0; --k) {
     if (k < L - 1) {
-      k_level_up<<<(np + 127) / 128, 128, 0, s>>>(w.p, status, np, w.W[k + 1], w.H[k + 1], w.W[k], w.H[k]);
+      k_level_up<<<(np + 127) / 128, 128, 0, s>>>(w.p, status + p0, np, w.W[k + 1], w.H[k + 1], w.W[k], w.H[k]);
       count_launch();
     }
-    IrlsLevel a{w.I[k], w.M[k], w.D[k], w.W[k], w.H[k], w.p, status, iters, w.keys, w.cand, (int64_t)W * H,
-                max_iter, tol};
+    const int64_t fk = (int64_t)w.W[k] * w.H[k] * p0;  // first frame of the range at level k
+    IrlsLevel a{w.I[k] + fk, w.M[k] + fk, w.D[k] + fk, w.W[k], w.H[k], w.p, status + p0, iters + p0, w.keys,
+                w.cand, (int64_t)W * H, max_iter, tol};
     k_irls<<<np * kCl, kIrlsThreads, 0, s>>>(a);
     count_launch();
   }
-  k_affine_finish<<<(np + 127) / 128, 128, 0, s>>>(w.p, status, np, W, H, theta);
+  k_affine_finish<<<(np + 127) / 128, 128, 0, s>>>(w.p, status + p0, np, W, H, theta + 6 * (int64_t)p0);
   count_launch();
   return check_launch("vinp_affine_estimate");
 }

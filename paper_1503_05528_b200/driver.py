@@ -386,12 +386,23 @@ class Inpainter:
         """Alg. 2: theta_{n,n+1} by robust IRLS, the chain to the middle frame, bilinear warp of
         the video and its occlusion (mask codes 0 / 1 / 2 = invalid, R40).  Device tensors."""
         c = self.cfg
+        npairs = self.T - 1
         if getattr(self, "_align_ws", None) is None:
             self._align_ws = torch.empty(max(self.V.affine_ws_bytes(self.W, self.H, self.T, c.align_levels), 1),
                                          dtype=torch.uint8, device=self.device)
             self._align_out = (torch.empty_like(rgb), torch.empty_like(mask))
-        theta, status, iters = self.V.affine_estimate(rgb, mask, c.align_levels, c.align_iters, c.align_tol,
-                                                      ws=self._align_ws)
+            k = self.ex.padded(max(npairs, 1))
+            self._align_est = (torch.empty((k, 6), dtype=torch.float64, device=self.device),
+                               torch.zeros(k, dtype=torch.int32, device=self.device),
+                               torch.zeros(k, dtype=torch.int32, device=self.device))
+        # the frame pairs are independent: each rank estimates its slab, then an all-gather
+        pairs = self.ex.slab(npairs) if npairs > 0 else (0, 0)
+        self.V.affine_estimate(rgb, mask, c.align_levels, c.align_iters, c.align_tol, ws=self._align_ws,
+                               out=self._align_est, pairs=pairs)
+        if npairs > 0:
+            for t in self._align_est:
+                self.ex.gather(t, npairs)
+        theta, status, iters = (t[:npairs] for t in self._align_est)
         fwd, inv, err = self.V.affine_chain(theta, self.T)
         self.align_info = dict(theta=theta, status=status, iters=iters, fwd=fwd, inv=inv, err=err)
         return self.V.align_warp(rgb, mask, inv, out=self._align_out)

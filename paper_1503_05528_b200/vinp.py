@@ -81,7 +81,7 @@ def _load():
         "vinp_tc_gemm_u8": (I, [P, P, I, P, P]),
         "vinp_patch_ambiguity": (I, [I, C.c_double, U64, U64, U64, P, P]),
         "vinp_affine_ws_bytes": (C.c_size_t, [I, I, I, I]),
-        "vinp_affine_estimate": (I, [P, P, I, I, I, I, I, C.c_double, P, P, P, P, C.c_size_t, P]),
+        "vinp_affine_estimate": (I, [P, P, I, I, I, I, I, C.c_double, I32, I32, P, P, P, P, C.c_size_t, P]),
         "vinp_affine_chain": (I, [P, I, P, P, P, P]),
         "vinp_align_warp": (I, [P, P, I, I, I, P, P, P, P]),
         "vinp_unwarp": (I, [P, P, P, I, I, I, P, P, P]),
@@ -403,9 +403,10 @@ def affine_ws_bytes(W: int, H: int, T: int, levels: int = 3) -> int:
 
 
 def affine_estimate(rgb: torch.Tensor, mask: torch.Tensor, levels=3, max_iter=20, tol=1e-4, ws=None,
-                    out=None):
-    """theta_{n,n+1} for every consecutive frame pair: (theta f64 [T-1, 6], status i32 [T-1],
-    iters i32 [T-1]), device tensors.  rgb u8 [T, H, W, 3], mask u8 [T, H, W] on the device."""
+                    out=None, pairs=None):
+    """theta_{n,n+1} for the consecutive frame pairs n in `pairs` = (b, e) (default: all): (theta
+    f64 [T-1, 6], status i32 [T-1], iters i32 [T-1]), device tensors; rows outside the range are
+    left as they were.  rgb u8 [T, H, W, 3], mask u8 [T, H, W] on the device."""
     T, H, W, _ = rgb.shape
     dev = rgb.device
     nb = affine_ws_bytes(W, H, T, levels)
@@ -417,7 +418,8 @@ def affine_estimate(rgb: torch.Tensor, mask: torch.Tensor, levels=3, max_iter=20
                torch.zeros(npairs, dtype=torch.int32, device=dev),
                torch.zeros(npairs, dtype=torch.int32, device=dev))
     theta, status, iters = out
-    _check(_lib.vinp_affine_estimate(_ptr(rgb), _ptr(mask), W, H, T, levels, max_iter, tol, _ptr(theta),
+    pb, pe = pairs if pairs is not None else (0, -1)
+    _check(_lib.vinp_affine_estimate(_ptr(rgb), _ptr(mask), W, H, T, levels, max_iter, tol, pb, pe, _ptr(theta),
                                      _ptr(status), _ptr(iters), _ptr(ws), ws.numel(), _stream()),
            "vinp_affine_estimate")
     return theta[:T - 1], status[:T - 1], iters[:T - 1]

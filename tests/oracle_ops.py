@@ -93,14 +93,17 @@ def sets_ws_bytes(lv1):
 
 
 def build_pyramid(rgb, mask, levels):
-    r, m = rgb.numpy(), (mask.numpy() != 0).astype(np.uint8)
+    mk = mask.numpy()
+    r, m = rgb.numpy(), ((mk != 0) & (mk != 2)).astype(np.uint8)  # codes: 2 = invalid X (R40)
+    x = (mk == 2).astype(np.uint8)
     for i, lv in enumerate(levels):
         if i > 0:
             r, m = orc.pyramid_down(r, m)
+            x = orc.mask_down(x)
         vb = lv.vox.view(torch.uint8).view(lv.N, 8)
         vb.zero_()
         vb[:, :3] = torch.from_numpy(np.ascontiguousarray(r).reshape(-1, 3))
-        lv.flags.copy_(torch.from_numpy(m.reshape(-1)))
+        lv.flags.copy_(torch.from_numpy((m | (x << 3)).reshape(-1)))
 
 
 def texture_features(prm, levels, ws):
@@ -118,9 +121,10 @@ def texture_features(prm, levels, ws):
 def build_sets(levels, ws):
     out = []
     for lv in levels:
-        occ = (lv.flags.numpy() & 1).reshape(lv.T, lv.H, lv.W)
-        src, tgt = orc.sets(np.ascontiguousarray(occ))
-        lv.flags.copy_(torch.from_numpy((occ | (src << 1) | (tgt << 2)).reshape(-1)))
+        f = lv.flags.numpy().reshape(lv.T, lv.H, lv.W)
+        occ, inv = np.ascontiguousarray(f & 1), np.ascontiguousarray((f >> 3) & 1)
+        src, tgt = orc.sets_x(occ, inv)
+        lv.flags.copy_(torch.from_numpy((occ | (src << 1) | (tgt << 2) | (inv << 3)).reshape(-1)))
         lv.n_targets, lv.n_holes, lv.n_sources = int(tgt.sum()), int(occ.sum()), int(src.sum())
         out.append((lv.n_targets, lv.n_holes, lv.n_sources))
     return out
@@ -241,3 +245,42 @@ def commit(lv, out_rgb, out_tex, layer_j=-1, hb=0, he=None):
 
 def change_l1(a, b, out):
     out += int(orc.change_l1(a.numpy(), b.numpy()))
+
+
+# ----------------------------------------------------------------------------- realignment (NEXT #1)
+def affine_ws_bytes(W, H, T, levels=3):
+    return 1
+
+
+def affine_estimate(rgb, mask, levels=3, max_iter=20, tol=1e-4, ws=None, out=None, pairs=None):
+    T = rgb.shape[0]
+    r, m = rgb.numpy(), mask.numpy()
+    if out is None:
+        k = max(T - 1, 1)
+        out = (torch.zeros((k, 6), dtype=torch.float64), torch.zeros(k, dtype=torch.int32),
+               torch.zeros(k, dtype=torch.int32))
+    theta, status, iters = out
+    b, e = pairs if pairs is not None else (0, T - 1)
+    for n in range(b, e):
+        th, st, it = orc.affine_estimate(r[n], r[n + 1], m[n], m[n + 1], levels, max_iter, tol)
+        theta[n] = torch.from_numpy(th)
+        status[n], iters[n] = st, it
+    return theta[:T - 1], status[:T - 1], iters[:T - 1]
+
+
+def affine_chain(pairs, T, out=None):
+    fwd, inv = orc.affine_chain(pairs.numpy(), T)
+    return torch.from_numpy(fwd), torch.from_numpy(inv), torch.zeros(1, dtype=torch.int32)
+
+
+def align_warp(rgb, mask, inv, out=None):
+    ar, am = orc.align_warp(rgb.numpy(), mask.numpy(), inv.numpy())
+    if out is not None:
+        out[0].copy_(torch.from_numpy(ar))
+        out[1].copy_(torch.from_numpy(am))
+        return out
+    return torch.from_numpy(ar), torch.from_numpy(am)
+
+
+def unwarp(rgb_aligned, rgb_orig, mask_orig, fwd, out=None):
+    return torch.from_numpy(orc.unwarp(rgb_aligned.numpy(), rgb_orig.numpy(), mask_orig.numpy(), fwd.numpy()))

@@ -108,3 +108,41 @@ def test_halo_ranges_are_partial():
     n = st.lv.n_targets
     spans = [hi - lo for lo, hi in st.halo_nnf]
     assert all(sp > 0 for sp in spans) and sum(sp < n for sp in spans) >= 2, (spans, n)
+
+
+def _run_aligned(rank, world, port, out_path):
+    os.environ.update(MASTER_ADDR="127.0.0.1", MASTER_PORT=str(port))
+    dist.init_process_group("gloo", rank=rank, world_size=world)
+    try:
+        import oracle_ops
+        from paper_1503_05528_b200 import Config, Exchange, inpaint
+        v, m = _aligned_video()
+        out, stats, ip = inpaint(v, m, Config(align=True, **CFG), device="cpu", exchange=Exchange(), ops=oracle_ops)
+        if rank == 0:
+            np.save(out_path, out.numpy())
+            np.save(out_path + ".theta.npy", ip.align_info["theta"].numpy())
+    finally:
+        dist.destroy_process_group()
+
+
+def _aligned_video():
+    from gen.synth import camera_video
+    T = 9
+    cams = [np.array([1.5 * t, 1, 0, -0.5 * t, 0, 1]) for t in range(T)]
+    v = camera_video(48, 40, T, 6, cams, noise=1.0)
+    m = torch.zeros((T, 40, 48), dtype=torch.uint8)
+    m[:, 15:23, 20:28] = 1
+    v[m.bool()] = 0
+    return v, m
+
+
+def test_aligned_two_ranks_split_pairs(tmp_path, orc):
+    """realignment under torch.distributed: each rank estimates its slab of the frame pairs and the
+    estimates are all-gathered; the result equals the oracle's align -> inpaint -> unwarp"""
+    out = str(tmp_path / "aligned_w2.npy")
+    mp.spawn(_run_aligned, args=(2, _free_port(), out), nprocs=2, join=True)
+    v, m = _aligned_video()
+    ar, am, fwd, inv, pairs, st = orc.align_pipeline(v.numpy(), m.numpy())
+    assert np.array_equal(np.load(out + ".theta.npy"), pairs)
+    o, _ = orc.inpaint(ar, am, CFG["levels"], pm_iters=CFG["pm_iters"], max_outer=CFG["max_outer"])
+    assert np.array_equal(np.load(out), orc.unwarp(o, v.numpy(), m.numpy(), fwd))
