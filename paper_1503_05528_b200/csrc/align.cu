@@ -235,7 +235,6 @@ __global__ void __cluster_dims__(kCl, 1, 1) __launch_bounds__(kIrlsThreads, VINP
 
   __shared__ double sp[6];
   __shared__ int s_stop, s_status;
-  __shared__ unsigned s_cnt[kIrlsWarps];
   __shared__ unsigned s_nv, s_len;
   __shared__ unsigned hist[kBins];
   __shared__ unsigned long long s_prefix;

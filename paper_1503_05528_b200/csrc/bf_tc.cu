@@ -370,9 +370,7 @@ size_t vinp_brute_force_tc_ws_bytes(const vinp_level* lv, int32_t b, int32_t e) 
   if (!lv) return 0;
   int64_t m = std::max<int64_t>(0, e - b), mpad = (m + kTile - 1) / kTile * kTile;
   int64_t npad = ((int64_t)lv->n_sources + kTile - 1) / kTile * kTile;
-  int64_t nb = (m + 255) / 256 + 1;
-  int64_t splits = (npad / 64) / ((64ll << 20) / (64 * kRow)) + 2;  // source chunks of 64 MB
-  (void)nb;
+  int64_t splits = (npad / 64) / ((64ll << 20) / (64 * kRow)) + 2;  // >= the number of 64 MB source chunks
   return (size_t)((mpad + 128 * 8) * kRow + (mpad + 128 * 8) * 8 + npad * kRow + 2 * npad * 8 + mpad * 4 +
                   2 * 729 * 4 + 64 + splits * (mpad + 128 * 8) * 8 + 4096);
 }
