@@ -131,10 +131,12 @@ __device__ int solve6(double M[6][7], double* x) {
   return 0;
 }
 
+// exact warp sum of per-lane int64 terms with |v| < 2^40 (the IRLS terms are < 2^32): a signed
+// high part and a 16-bit low part, each summed by one REDUX (no partial sum can overflow int32)
 __device__ __forceinline__ long long warp_sum_ll(long long v) {
-#pragma unroll
-  for (int d = 16; d >= 1; d >>= 1) v += __shfl_xor_sync(kFull, v, d);
-  return v;
+  const int hi = __reduce_add_sync(kFull, (int)(v >> 16));
+  const unsigned lo = __reduce_add_sync(kFull, (unsigned)(v & 0xffff));
+  return (long long)hi * 65536 + (long long)lo;
 }
 
 struct IrlsLevel {
