@@ -228,8 +228,11 @@ __global__ void __cluster_dims__(kCl, 1, 1) __launch_bounds__(kIrlsThreads, VINP
   const uint8_t* Ma = a.M + (int64_t)n * NP;
   const uint8_t* Db = a.D + (int64_t)(n + 1) * NP;
   // this CTA's contiguous chunk of the pixels; its keys / candidate lists live in the chunk too
-  const int64_t chunk = (NP + kCl - 1) / kCl;
-  const int64_t c0 = (int64_t)rk * chunk, c1 = c0 + chunk < NP ? c0 + chunk : NP;
+  // this CTA's pixels: rows j = rk, rk + kCl, ... (row-interleaved, so occlusions and frame-edge
+  // effects spread evenly over the cluster); its keys / candidate lists live in its own region
+  const int rows_per = (H + kCl - 1) / kCl;
+  const int64_t myN = (int64_t)((H - (int)rk + kCl - 1) / kCl) * W;
+  const int64_t c0 = (int64_t)rk * rows_per * W;
   uint64_t* bufA = a.keys + (int64_t)n * a.keys_stride + c0;
   uint64_t* bufB = a.cand + (int64_t)n * a.keys_stride + c0;
   const double cx = (double)(W - 1) * 0.5, cy = (double)(H - 1) * 0.5;
@@ -259,12 +262,12 @@ __global__ void __cluster_dims__(kCl, 1, 1) __launch_bounds__(kIrlsThreads, VINP
     for (int b = tid; b < kBins; b += kIrlsThreads) hist[b] = 0;
     if (tid == 0) s_len = 0;
     __syncthreads();
-    for (int64_t base = c0 + (tid & ~31); base < c1; base += kIrlsThreads) {
+    for (int64_t base = (tid & ~31); base < myN; base += kIrlsThreads) {
       int64_t id = base + lane;
       bool ok = false;
       unsigned long long key = 0;
-      if (id < c1) {
-        int j = (int)(id / W), i = (int)(id - (int64_t)j * W);
+      if (id < myN) {
+        int jr = (int)(id / W), i = (int)(id - (int64_t)jr * W), j = (int)rk + kCl * jr;
         Pix o;
         ok = irls_pixel(Ia, Ma, Ib, Db, W, H, p, cx, cy, s, i, j, o);
         key = (unsigned long long)__double_as_longlong(fabs(o.r));
@@ -334,12 +337,12 @@ __global__ void __cluster_dims__(kCl, 1, 1) __launch_bounds__(kIrlsThreads, VINP
     // terms with shuffles and lane 0 accumulates the warp's row of `red` (few live registers)
     if (lane < 27) red[warp][lane] = 0;
     __syncwarp();
-    for (int64_t base = c0 + (tid & ~31); base < c1; base += kIrlsThreads) {
+    for (int64_t base = (tid & ~31); base < myN; base += kIrlsThreads) {
       int64_t id = base + lane;
       bool ok = false;
       double w = 0.0, r = 0.0, J[6] = {0.0, 0.0, 0.0, 0.0, 0.0, 0.0};
-      if (id < c1) {
-        int j = (int)(id / W), i = (int)(id - (int64_t)j * W);
+      if (id < myN) {
+        int jr = (int)(id / W), i = (int)(id - (int64_t)jr * W), j = (int)rk + kCl * jr;
         Pix o;
         if (irls_pixel(Ia, Ma, Ib, Db, W, H, p, cx, cy, s, i, j, o)) {
           double u = o.r / c;
@@ -595,6 +598,7 @@ struct AlignWs {
   int W[8], H[8];
   uint64_t* keys;
   uint64_t* cand;
+  int64_t stride;
   double* p;
   size_t bytes;
 };
@@ -614,10 +618,11 @@ AlignWs carve(void* base, int W, int H, int T, int L) {
     w.D[k] = (uint8_t*)(c ? c + off : nullptr);
     off += al(n);
   }
+  w.stride = (int64_t)W * ((H + kCl - 1) / kCl) * kCl;  // >= each level's kCl row-interleaved regions
   w.keys = (uint64_t*)(c ? c + off : nullptr);
-  off += al((size_t)W * H * (T > 1 ? T - 1 : 1) * sizeof(uint64_t));
+  off += al((size_t)w.stride * (T > 1 ? T - 1 : 1) * sizeof(uint64_t));
   w.cand = (uint64_t*)(c ? c + off : nullptr);
-  off += al((size_t)W * H * (T > 1 ? T - 1 : 1) * sizeof(uint64_t));
+  off += al((size_t)w.stride * (T > 1 ? T - 1 : 1) * sizeof(uint64_t));
   w.p = (double*)(c ? c + off : nullptr);
   off += al((size_t)(T > 1 ? T - 1 : 1) * 6 * sizeof(double));
   w.bytes = off;
@@ -674,7 +679,7 @@ vinp_status vinp_affine_estimate(const uint8_t* rgb, const uint8_t* mask, int W,
     }
     const int64_t fk = (int64_t)w.W[k] * w.H[k] * p0;  // first frame of the range at level k
     IrlsLevel a{w.I[k] + fk, w.M[k] + fk, w.D[k] + fk, w.W[k], w.H[k], w.p, status + p0, iters + p0, w.keys,
-                w.cand, (int64_t)W * H, max_iter, tol};
+                w.cand, w.stride, max_iter, tol};
     k_irls<<<np * kCl, kIrlsThreads, 0, s>>>(a);
     count_launch();
   }
