@@ -53,14 +53,17 @@ struct ReconArgs {
   const uint8_t* n;
 };
 
-__global__ void __launch_bounds__(256) k_reconstruct(ReconArgs a, int mode, int layer_j, int32_t hb,
-                                                     int32_t he, const int32_t* __restrict__ list,
-                                                     float* __restrict__ out_rgb,
-                                                     float* __restrict__ out_tex, int commit) {
-  int lane = threadIdx.x & 31;
-  int idx = hb + blockIdx.x * kWPB + (threadIdx.x >> 5);
-  if (idx >= he) return;
-  int h = list ? __ldg(list + idx) : idx;
+// Per-lane contributor geometry, the same for every hole: contributor v = lane + 32 i of N_p is the
+// patch voxel (vdx, vdy, vdt), at linear offset off from p.
+struct LaneVox {
+  int off[4];
+  int8_t dx[4], dy[4], dt[4];
+  bool real[4];  // v < 125
+};
+
+__device__ __forceinline__ void recon_hole(const ReconArgs& a, const LaneVox& LV, int lane, int mode, int layer_j,
+                                           int h, float* __restrict__ out_rgb, float* __restrict__ out_tex,
+                                           int commit) {
   int p = a.holes[h];
   if (layer_j >= 0 && a.layer[p] != layer_j) return;
   int px, py, pt;
@@ -72,16 +75,10 @@ __global__ void __launch_bounds__(256) k_reconstruct(ReconArgs a, int mode, int 
   uint64_t val[4];
   unsigned valid = 0;
   bool n125 = true;
-  int off[4];
+  const int* off = LV.off;
   bool cand[4];
 #pragma unroll
-  for (int i = 0; i < 4; ++i) {
-    int v = lane + 32 * i;
-    int dx, dy, dt;
-    voff(v < kPatch ? v : 62, dx, dy, dt);
-    off[i] = dt * a.g.HW + dy * a.g.W + dx;
-    cand[i] = v < kPatch && inside(a.g, px + dx, py + dy, pt + dt);
-  }
+  for (int i = 0; i < 4; ++i) cand[i] = LV.real[i] && inside(a.g, px + LV.dx[i], py + LV.dy[i], pt + LV.dt[i]);
   if (layer_j >= 0) {
 #pragma unroll
     for (int i = 0; i < 4; ++i) cand[i] = cand[i] && a.layer[p + (cand[i] ? off[i] : 0)] < layer_j;
@@ -262,6 +259,29 @@ __global__ void __launch_bounds__(256) k_reconstruct(ReconArgs a, int mode, int 
   }
 }
 
+// persistent warps over the holes [hb, he) (or list[hb..he)): the lane geometry is set up once
+__global__ void __launch_bounds__(256, 4) k_reconstruct(ReconArgs a, int mode, int layer_j, int32_t hb,
+                                                     int32_t he, const int32_t* __restrict__ list,
+                                                     float* __restrict__ out_rgb,
+                                                     float* __restrict__ out_tex, int commit) {
+  const int lane = threadIdx.x & 31;
+  LaneVox LV;
+#pragma unroll
+  for (int i = 0; i < 4; ++i) {
+    int v = lane + 32 * i;
+    int dx, dy, dt;
+    voff(v < kPatch ? v : 62, dx, dy, dt);
+    LV.off[i] = dt * a.g.HW + dy * a.g.W + dx;
+    LV.dx[i] = (int8_t)dx;
+    LV.dy[i] = (int8_t)dy;
+    LV.dt[i] = (int8_t)dt;
+    LV.real[i] = v < kPatch;
+  }
+  const int nw = gridDim.x * kWPB;
+  for (int idx = hb + blockIdx.x * kWPB + (threadIdx.x >> 5); idx < he; idx += nw)
+    recon_hole(a, LV, lane, mode, layer_j, list ? __ldg(list + idx) : idx, out_rgb, out_tex, commit);
+}
+
 __global__ void k_commit(Geo g, uint64_t* __restrict__ vox, const uint8_t* __restrict__ layer,
                          const int32_t* __restrict__ holes, const float* __restrict__ rgb,
                          const float* __restrict__ tex, int layer_j, int32_t hb, int32_t he) {
@@ -335,7 +355,8 @@ vinp_status launch_reconstruct(vinp_level* lv, const vinp_nnf* nnf, int mode, in
   VINP_REQUIRE(layer_j < 0 || lv->layer, "vinp_reconstruct: layer map required");
   if (he > hb) {
     ReconArgs a{geo_of(lv), lv->vox, lv->layer, lv->slot, lv->holes, nnf->e, nnf->n};
-    k_reconstruct<<<nblk(he - hb, kWPB), 32 * kWPB, 0, S(stream)>>>(a, mode, layer_j, hb, he, list,
+    const int grid = (int)std::min<int64_t>(nblk(he - hb, kWPB), 148 * 8);  // persistent warps
+    k_reconstruct<<<grid, 32 * kWPB, 0, S(stream)>>>(a, mode, layer_j, hb, he, list,
                                                                   out_rgb, out_tex, commit);
     count_launch();
   }
