@@ -1,7 +1,8 @@
 """Seeded fuzz of the whole pipeline (Alg. 4), GPU through the C ABI vs the oracle, bit for bit:
 random odd sizes, ellipsoidal holes that may cross the volume border, lambda in [0, 126], 1-3
-pyramid levels, jump-step schedules and both sign policies, the stopping rule or fixed outer
-iteration counts.  Cases whose D~ is empty must be refused by both sides."""
+pyramid levels, jump-step schedules and both sign policies, random-search ratios rho (so every
+candidate-count instantiation of the random-search kernel runs), texture window widths, the
+stopping rule or fixed outer iteration counts.  Cases whose D~ is empty must be refused by both sides."""
 import numpy as np
 import pytest
 import torch
@@ -20,7 +21,8 @@ def _case(i):
     return dict(W=W, H=H, T=T, levels=levels, lam=int(rng.choice([0, 1, 50, 126, int(rng.integers(0, 127))])),
                 steps=STEPS[int(rng.integers(0, len(STEPS)))], sign_policy=int(rng.integers(0, 2)),
                 pm_iters=int(rng.integers(1, 4)), fixed_outer=int(rng.choice([0, 0, 2])),
-                nholes=int(rng.integers(1, 4)), seed=int(rng.integers(1, 1 << 30)))
+                nholes=int(rng.integers(1, 4)), seed=int(rng.integers(1, 1 << 30)),
+                rho=float(rng.choice([0.5, 0.5, 0.62, 0.75, 0.85])), tex_half=int(rng.choice([-1, -1, 0, 2])))
 
 
 @pytest.mark.parametrize("i", range(24))
@@ -33,11 +35,13 @@ def test_pipeline_fuzz(orc, i):
     v = v.clone()
     v[m.bool()] = 0
     cfg = Config(levels=c["levels"], pm_iters=c["pm_iters"], fixed_outer=c["fixed_outer"], max_outer=4,
-                 lam=c["lam"], seed=c["seed"], steps=c["steps"], sign_policy=c["sign_policy"])
+                 lam=c["lam"], seed=c["seed"], steps=c["steps"], sign_policy=c["sign_policy"], rho=c["rho"],
+                 tex_half=c["tex_half"])
     try:
         ref, st = orc.inpaint(v.numpy(), m.numpy(), c["levels"], pm_iters=c["pm_iters"],
                               fixed_outer=c["fixed_outer"], max_outer=4, lam=c["lam"], seed=c["seed"],
-                              steps=c["steps"], sign_policy=c["sign_policy"])
+                              steps=c["steps"], sign_policy=c["sign_policy"], rho=c["rho"],
+                              tex_half=c["tex_half"])
     except RuntimeError:
         with pytest.raises(VinpError):
             inpaint(v, m, cfg, device="cuda")
