@@ -87,9 +87,6 @@ __global__ void k_upsample(LevelArgs c, const uint64_t* __restrict__ ce, LevelAr
 #ifndef VINP_PROP_MINB
 #define VINP_PROP_MINB 4
 #endif
-#ifndef VINP_GROUP
-#define VINP_GROUP 8
-#endif
 
 // ------------------------------------------------------------------ thread-per-target SSD
 // Used where candidates are spatially coherent (evaluate, propagation): lane l of a warp owns
@@ -317,96 +314,6 @@ __global__ void __launch_bounds__(256, KB ? 2 : VINP_PROP_MINB) k_propagate(Leve
 }
 
 // ------------------------------------------------------------------ a7: random search pass
-// Candidates are incoherent (independent Philox offsets per voxel), so the evaluation is
-// warp-cooperative: lane l holds voxel l + 32k of the target patch, every gather of a candidate
-// is one warp load of 32 consecutive patch voxels (~8 L1 lines), and a group of up to G candidates
-// of one target has all its gathers in flight.  Exact partial-distance elimination after each
-// chunk of 32 voxels against the best distance at the start of the group.
-__device__ __forceinline__ uint64_t shfl64(uint64_t v, int src) {
-  uint32_t lo = __shfl_sync(kFull, (uint32_t)v, src), hi = __shfl_sync(kFull, (uint32_t)(v >> 32), src);
-  return ((uint64_t)hi << 32) | lo;
-}
-
-template <int G>
-__device__ __forceinline__ void eval_group(const LevelArgs& a, const PatchLanes& L, unsigned tmask,
-                                           int lambda, int pi, const int* cand, int i, int base,
-                                           int k, uint32_t& bestD, int& bestq, uint32_t (&tw)[4][2],
-                                           unsigned& tloaded) {
-  const unsigned long long* v = reinterpret_cast<const unsigned long long*>(a.vox);
-  int q[G];
-  uint32_t part[G];
-#pragma unroll
-  for (int c = 0; c < G; ++c) {
-    q[c] = c < k ? cand[(base + c) * 32 + i] : 0;
-    part[c] = 0;
-  }
-  unsigned alive = (1u << k) - 1;
-  uint32_t thr = bestD;
-#pragma unroll
-  for (int ch = 0; ch < 4; ++ch) {
-    if (!alive) break;  // warp-uniform
-    bool m = (tmask >> ch) & 1;
-    if (!((tloaded >> ch) & 1)) {  // target chunk, loaded on first use
-      uint64_t w = m ? __ldg(v + pi + L.off[ch]) : 0ull;
-      tw[ch][0] = (uint32_t)w;
-      tw[ch][1] = (uint32_t)(w >> 32);
-      tloaded |= 1u << ch;
-    }
-    uint64_t sv[G];
-#pragma unroll
-    for (int c = 0; c < G; ++c) sv[c] = (m && ((alive >> c) & 1)) ? __ldg(v + q[c] + L.off[ch]) : 0ull;
-#pragma unroll
-    for (int c = 0; c < G; ++c) {
-      if ((alive >> c) & 1) {
-        uint32_t x = m ? voxel_cost(tw[ch][0], tw[ch][1], sv[c], lambda) : 0u;
-        part[c] += __reduce_add_sync(kFull, x);
-        if (part[c] >= thr) alive &= ~(1u << c);
-      }
-    }
-  }
-#pragma unroll
-  for (int c = 0; c < G; ++c)
-    if (((alive >> c) & 1) && part[c] < bestD) {
-      bestD = part[c];
-      bestq = q[c];
-    }
-}
-
-template <int NC>
-__device__ __forceinline__ void phase2(const LevelArgs& a, int lane, int lambda, int kb, int p,
-                                       uint64_t inc, const int* cand, int ncand, uint64_t& result,
-                                       unsigned& cnt) {
-  constexpr int G = NC < VINP_GROUP ? NC : VINP_GROUP;
-  result = inc;
-  unsigned work = __ballot_sync(kFull, ncand != 0);
-  if (!work) return;
-  PatchLanes L;
-  init_lanes(L, a.g, lane);
-  while (work) {
-    int i = __ffs(work) - 1;
-    work &= work - 1;
-    int pi = __shfl_sync(kFull, p, i);
-    int ni = __shfl_sync(kFull, ncand, i);
-    uint64_t inci = shfl64(inc, i);
-    int px, py, pt;
-    decode(a.g, pi, px, py, pt);
-    unsigned tmask = 0;  // per-lane validity of the 4 owned target voxels (Omega and K)
-#pragma unroll
-    for (int ch = 0; ch < 4; ++ch)
-      if (L.live[ch] && inside(a.g, px + L.dx[ch], py + L.dy[ch], pt + L.dt[ch]) &&
-          (kb < 0 || a.layer[pi + L.off[ch]] < kb))
-        tmask |= 1u << ch;
-    uint32_t bestD = e_D(inci);
-    int bestq = e_q(inci);
-    uint32_t tw[4][2];
-    unsigned tloaded = 0;
-    for (int base = 0; base < ni; base += G)
-      eval_group<G>(a, L, tmask, lambda, pi, cand, i, base, min(G, ni - base), bestD, bestq, tw, tloaded);
-    if (lane == i) result = pack_e(bestD, bestq);
-    cnt += ni;
-  }
-}
-
 struct Radii {
   double R[32];
   int M;
@@ -414,11 +321,10 @@ struct Radii {
 
 // Random search, evaluation by 5-lane column groups: lanes 5g..5g+4 (g < 6) evaluate one
 // (target, candidate) pair, lane k owning patch column dx = k - 2, so every row of a patch is one
-// 40-byte gather per group and 6 pairs share each warp instruction.  Pairs come from the warp's
-// flattened candidate list (owner lane = target, rank order).  Exact partial-distance elimination
-// after every frame dt (25 voxels): the group sum is all-reduced over its 5 lanes (3 shuffles) and
-// the pair is dropped once it reaches its target's best at the start of the batch.  Survivors are
-// applied in pair order (rank order within a target) with strict improvement (R25).
+// 40-byte gather per group.  Pairs come from the warp's flattened candidate list (owner lane =
+// target, rank order); each group takes the next unassigned pair as soon as its own aborts or
+// completes.  Exact partial-distance elimination after every frame dt (25 voxels): the group sum
+// is all-reduced over its 5 lanes (3 shuffles) and checked against the owner's current minimum.
 __device__ __forceinline__ uint32_t sum5(uint32_t x, int base, int k) {
   uint32_t s1 = x + __shfl_sync(kFull, x, base + (k + 1) % 5);
   uint32_t s2 = s1 + __shfl_sync(kFull, s1, base + (k + 2) % 5);

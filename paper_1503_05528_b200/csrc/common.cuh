@@ -197,50 +197,6 @@ __device__ __forceinline__ uint32_t warp_ssd(const TargetPatch& tp, const PatchL
   return __reduce_add_sync(kFull, acc);
 }
 
-// Two candidates at once (more loads in flight per warp).
-__device__ __forceinline__ void warp_ssd2(const TargetPatch& tp, const PatchLanes& L,
-                                          const uint64_t* __restrict__ vox, int q0, int q1,
-                                          int lambda, uint32_t& D0, uint32_t& D1) {
-  uint32_t a0 = 0, a1 = 0;
-  const unsigned long long* v = reinterpret_cast<const unsigned long long*>(vox);
-  uint64_t s0[4], s1[4];
-#pragma unroll
-  for (int i = 0; i < 4; ++i) {
-    bool m = tp.mask & (1u << i);
-    s0[i] = m ? __ldg(v + q0 + L.off[i]) : 0ull;
-    s1[i] = m ? __ldg(v + q1 + L.off[i]) : 0ull;
-  }
-#pragma unroll
-  for (int i = 0; i < 4; ++i) {
-    if (tp.mask & (1u << i)) {
-      a0 += voxel_cost(tp.c[i], tp.t[i], s0[i], lambda);
-      a1 += voxel_cost(tp.c[i], tp.t[i], s1[i], lambda);
-    }
-  }
-  D0 = __reduce_add_sync(kFull, a0);
-  D1 = __reduce_add_sync(kFull, a1);
-}
-
-// N candidates at once (N*4 gathers in flight per lane).
-template <int N>
-__device__ __forceinline__ void warp_ssdN(const TargetPatch& tp, const PatchLanes& L,
-                                          const uint64_t* __restrict__ vox, const int* q, int lambda,
-                                          uint32_t* D) {
-  const unsigned long long* v = reinterpret_cast<const unsigned long long*>(vox);
-  uint64_t s[N][4];
-#pragma unroll
-  for (int c = 0; c < N; ++c)
-#pragma unroll
-    for (int i = 0; i < 4; ++i) s[c][i] = (tp.mask & (1u << i)) ? __ldg(v + q[c] + L.off[i]) : 0ull;
-#pragma unroll
-  for (int c = 0; c < N; ++c) {
-    uint32_t a = 0;
-#pragma unroll
-    for (int i = 0; i < 4; ++i)
-      if (tp.mask & (1u << i)) a += voxel_cost(tp.c[i], tp.t[i], s[c][i], lambda);
-    D[c] = __reduce_add_sync(kFull, a);
-  }
-}
 
 __device__ __forceinline__ bool is_source(const Geo& g, const uint8_t* __restrict__ flags, int x,
                                           int y, int t) {
