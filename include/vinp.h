@@ -85,6 +85,11 @@ typedef struct {
 
 const char* vinp_last_error(void);
 int vinp_version(void);
+/* Pyramid dimensions: dims_out[3l .. 3l+2] = (W_l, H_l, T) for l = 1..L, with
+ * W_l = ceil(W_{l-1} / 2), H_l likewise and T never subsampled.  Host-only; VINP_E_INVALID for
+ * non-positive sizes or L outside [1, 16], VINP_E_UNSUPPORTED if W*H*T >= 2^31. */
+vinp_status vinp_level_dims(int W, int H, int T, int L, int32_t* dims_out);
+
 /* Number of kernels this library has launched since it was loaded (evidence counter). */
 uint64_t vinp_launch_count(void);
 

@@ -357,6 +357,22 @@ const char* vinp_last_error(void) { return g_err.c_str(); }
 int vinp_version(void) { return 1; }
 uint64_t vinp_launch_count(void) { return g_launches.load(); }
 
+vinp_status vinp_level_dims(int W, int H, int T, int L, int32_t* dims_out) {
+  VINP_REQUIRE(dims_out && W >= 1 && H >= 1 && T >= 1 && L >= 1 && L <= 16, "vinp_level_dims: bad arguments");
+  if ((int64_t)W * H * T >= (1ll << 31)) {
+    set_error("vinp_level_dims: %dx%dx%d voxels exceed the 2^31 limit", W, H, T);
+    return VINP_E_UNSUPPORTED;
+  }
+  for (int l = 0; l < L; ++l) {
+    dims_out[3 * l] = W;
+    dims_out[3 * l + 1] = H;
+    dims_out[3 * l + 2] = T;
+    W = (W + 1) / 2;
+    H = (H + 1) / 2;
+  }
+  return VINP_OK;
+}
+
 vinp_status vinp_build_pyramid(const uint8_t* rgb, const uint8_t* mask, vinp_level* lv, int L,
                                void* stream) {
   VINP_REQUIRE(rgb && mask && lv && L >= 1 && L <= 16, "vinp_build_pyramid: bad arguments");

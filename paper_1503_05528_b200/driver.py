@@ -145,10 +145,8 @@ class Inpainter:
         self.ex = exchange or Exchange()
         self.prm = cfg.params()
         self.levels: List[V.Level] = []
-        w, h = W, H
-        for l in range(1, cfg.levels + 1):
+        for l, (w, h, _) in enumerate(V.level_dims(W, H, T, cfg.levels), start=1):
             self.levels.append(V.Level.alloc(w, h, T, l, self.device))
-            w, h = (w + 1) // 2, (h + 1) // 2
         n1 = W * H * T
         self.ws = torch.empty(max(self.V.texture_ws_bytes(self.levels[0]), self.V.sets_ws_bytes(self.levels[0])) + 256,
                               dtype=torch.uint8, device=self.device)

@@ -86,6 +86,7 @@ def _load():
         "vinp_align_warp": (I, [P, P, I, I, I, P, P, P, P]),
         "vinp_unwarp": (I, [P, P, P, I, I, I, P, P, P]),
         "vinp_output_rgb": (I, [P, P, P]),
+        "vinp_level_dims": (I, [I, I, I, I, P]),
     }
     for name, (res, args) in sigs.items():
         f = getattr(lib, name)
@@ -105,7 +106,7 @@ EXPORTED = [
     "vinp_brute_force_ws_bytes", "vinp_brute_force", "vinp_patch_ssd", "vinp_philox",
     "vinp_tc_gemm_u8", "vinp_patch_ambiguity", "vinp_brute_force_list", "vinp_brute_force_tc_ws_bytes", "vinp_brute_force_tc",
     "vinp_affine_ws_bytes", "vinp_affine_estimate", "vinp_affine_chain", "vinp_align_warp", "vinp_unwarp",
-    "vinp_output_rgb"]
+    "vinp_output_rgb", "vinp_level_dims"]
 
 
 def _check(rc: int, what: str):
@@ -462,3 +463,10 @@ def output_rgb(lv1: Level, out: Optional[torch.Tensor] = None):
         out = torch.empty((lv1.T, lv1.H, lv1.W, 3), dtype=torch.uint8, device=lv1.vox.device)
     _check(_lib.vinp_output_rgb(lv1.struct(), _ptr(out), _stream()), "vinp_output_rgb")
     return out
+
+
+def level_dims(W: int, H: int, T: int, L: int):
+    """[(W_l, H_l, T)] for l = 1..L (ceil halving of W, H; T unchanged)."""
+    out = (C.c_int32 * (3 * L))()
+    _check(_lib.vinp_level_dims(W, H, T, L, out), "vinp_level_dims")
+    return [tuple(out[3 * l:3 * l + 3]) for l in range(L)]

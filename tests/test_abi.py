@@ -3,6 +3,8 @@ import os
 import re
 import subprocess
 
+import pytest
+
 ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
 
 
@@ -40,3 +42,15 @@ def test_argument_errors_are_synchronous():
             vinp._lib.vinp_build_pyramid(None, None, None, 1, None), "vinp_build_pyramid")
     rc = vinp._lib.vinp_change_l1(None, None, 1, None, None)
     assert rc == 1 and b"bad args" in vinp._lib.vinp_last_error()
+
+
+def test_level_dims_host_only():
+    """vinp_level_dims is host-only (no GPU): ceil halving of W and H, T unchanged."""
+    from paper_1503_05528_b200 import vinp
+    assert vinp.level_dims(1920, 1080, 100, 4) == [(1920, 1080, 100), (960, 540, 100), (480, 270, 100),
+                                                   (240, 135, 100)]
+    assert vinp.level_dims(854, 480, 7, 3) == [(854, 480, 7), (427, 240, 7), (214, 120, 7)]
+    with pytest.raises(vinp.VinpError):
+        vinp.level_dims(4096, 4096, 200, 1)  # >= 2^31 voxels
+    with pytest.raises(vinp.VinpError):
+        vinp.level_dims(10, 10, 10, 0)
