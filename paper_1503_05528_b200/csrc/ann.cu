@@ -81,6 +81,9 @@ __global__ void k_upsample(LevelArgs c, const uint64_t* __restrict__ ce, LevelAr
   fn[s] = 0;
 }
 
+#ifndef VINP_KB_BLOCK
+#define VINP_KB_BLOCK 64  // onion (K-restricted) passes: small layers, spread over more SMs
+#endif
 #ifndef VINP_MINB
 #define VINP_MINB 3
 #endif
@@ -666,7 +669,7 @@ vinp_status launch_evaluate(const vinp_level* lv, vinp_nnf* nnf, const vinp_para
   VINP_REQUIRE((kb < 0 && only_layer < 0) || lv->layer, "vinp_nnf_evaluate: layer map required");
   if (e > b) {
     if (kb >= 0)
-      k_evaluate<true><<<nblk(e - b, 256), 256, 0, S(stream)>>>(
+      k_evaluate<true><<<nblk(e - b, VINP_KB_BLOCK), VINP_KB_BLOCK, 0, S(stream)>>>(
           args_of(lv), nnf->e, nnf->n, prm->lambda, kb, only_layer, b, e, list, counter);
     else
       k_evaluate<false><<<nblk(e - b, 256), 256, 0, S(stream)>>>(
@@ -686,7 +689,7 @@ vinp_status launch_propagate(const vinp_level* lv, const vinp_nnf* in, vinp_nnf*
   VINP_REQUIRE((kb < 0 && only_layer < 0) || lv->layer, "vinp_propagate: layer map required");
   if (e > b) {
     if (kb >= 0)
-      k_propagate<true><<<nblk(e - b, 256), 256, 0, S(stream)>>>(
+      k_propagate<true><<<nblk(e - b, VINP_KB_BLOCK), VINP_KB_BLOCK, 0, S(stream)>>>(
           args_of(lv), in->e, out->e, prm->lambda, step, sign, kb, only_layer, b, e, list, counter);
     else
       k_propagate<false><<<nblk(e - b, 256), 256, 0, S(stream)>>>(
