@@ -15,7 +15,10 @@
 namespace vinp {
 
 static inline int nblk(int64_t n, int t) { return (int)((n + t - 1) / t); }
-constexpr int kWPB = 8;
+#ifndef VINP_REC_WPB
+#define VINP_REC_WPB 8
+#endif
+constexpr int kWPB = VINP_REC_WPB;
 
 __device__ __forceinline__ uint64_t shfl_xor64(uint64_t v, int m) {
   uint32_t lo = __shfl_xor_sync(kFull, (uint32_t)v, m), hi = __shfl_xor_sync(kFull, (uint32_t)(v >> 32), m);
@@ -355,7 +358,7 @@ vinp_status launch_reconstruct(vinp_level* lv, const vinp_nnf* nnf, int mode, in
   VINP_REQUIRE(layer_j < 0 || lv->layer, "vinp_reconstruct: layer map required");
   if (he > hb) {
     ReconArgs a{geo_of(lv), lv->vox, lv->layer, lv->slot, lv->holes, nnf->e, nnf->n};
-    const int grid = (int)std::min<int64_t>(nblk(he - hb, kWPB), 148 * 8);  // persistent warps
+    const int grid = (int)std::min<int64_t>(nblk(he - hb, kWPB), 148 * (64 / kWPB));  // persistent warps
     k_reconstruct<<<grid, 32 * kWPB, 0, S(stream)>>>(a, mode, layer_j, hb, he, list,
                                                                   out_rgb, out_tex, commit);
     count_launch();
