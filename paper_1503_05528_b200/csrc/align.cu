@@ -19,7 +19,10 @@ namespace {
 #ifndef VINP_IRLS_MINB
 #define VINP_IRLS_MINB 2
 #endif
-constexpr int kIrlsThreads = 512;
+#ifndef VINP_IRLS_THREADS
+#define VINP_IRLS_THREADS 512
+#endif
+constexpr int kIrlsThreads = VINP_IRLS_THREADS;
 constexpr int kIrlsWarps = kIrlsThreads / 32;
 
 __global__ void k_grey0(const uint8_t* __restrict__ rgb, const uint8_t* __restrict__ mask, int64_t N,
