@@ -107,26 +107,41 @@ __device__ __forceinline__ int luma(uint64_t w) {  // exact x1000 Rec.601 (R14)
 }
 
 // horizontal window sums of masked |dY_x| and |dY_y|: ws[p] = {(sx << 8) | cx, (sy << 8) | cy}
-__global__ void k_tex_rows(const uint64_t* __restrict__ vox, const uint8_t* __restrict__ flags,
-                           int W, int H, int T, int h, uint2* __restrict__ ws) {
-  int x = blockIdx.x * blockDim.x + threadIdx.x;
-  int y = blockIdx.y;
-  int t = blockIdx.z;
+// horizontal window sums of masked |dY_x| and |dY_y|: ws[p] = {(sx << 8) | cx, (sy << 8) | cy}.
+// A block owns 128 voxels of a row: the per-position terms (|dY|, valid) of its window range
+// [x0 - h, x0 + 127 + h] are computed once into shared memory, then each thread sums 2h + 1 of them
+// (the same integer sums as per-voxel loops, in any order).
+constexpr int kTexTile = 128, kTexMaxH = 32;
+__global__ void __launch_bounds__(kTexTile) k_tex_rows(const uint64_t* __restrict__ vox, const uint8_t* __restrict__ flags,
+                                                       int W, int H, int T, int h, uint2* __restrict__ ws) {
+  __shared__ uint32_t gx[kTexTile + 2 * kTexMaxH], gy[kTexTile + 2 * kTexMaxH];  // (|dY| << 1) | valid
+  const int x0 = blockIdx.x * kTexTile, y = blockIdx.y, t = blockIdx.z;
+  const int64_t row = ((int64_t)t * H + y) * W;
+  const int ya = refl101(y - 1, H), yb = refl101(y + 1, H);
+  const int64_t rowa = ((int64_t)t * H + ya) * W, rowb = ((int64_t)t * H + yb) * W;
+  const int n = kTexTile + 2 * h;
+  for (int k = threadIdx.x; k < n; k += kTexTile) {
+    const int qx = x0 - h + k;
+    uint32_t vx = 0, vy = 0;
+    if (qx >= 0 && qx < W) {
+      const int xa = refl101(qx - 1, W), xb = refl101(qx + 1, W);
+      if (!(flags[row + xa] & 1) && !(flags[row + xb] & 1))
+        vx = ((uint32_t)abs(luma(vox[row + xb]) - luma(vox[row + xa])) << 1) | 1u;
+      if (!(flags[rowa + qx] & 1) && !(flags[rowb + qx] & 1))
+        vy = ((uint32_t)abs(luma(vox[rowb + qx]) - luma(vox[rowa + qx])) << 1) | 1u;
+    }
+    gx[k] = vx;
+    gy[k] = vy;
+  }
+  __syncthreads();
+  const int x = x0 + threadIdx.x;
   if (x >= W) return;
-  int64_t row = ((int64_t)t * H + y) * W;
-  int ya = refl101(y - 1, H), yb = refl101(y + 1, H);
-  int64_t rowa = ((int64_t)t * H + ya) * W, rowb = ((int64_t)t * H + yb) * W;
   uint32_t sx = 0, cx = 0, sy = 0, cy = 0;
-  for (int qx = max(0, x - h); qx <= min(W - 1, x + h); ++qx) {
-    int xa = refl101(qx - 1, W), xb = refl101(qx + 1, W);
-    if (!(flags[row + xa] & 1) && !(flags[row + xb] & 1)) {
-      sx += (uint32_t)abs(luma(vox[row + xb]) - luma(vox[row + xa]));
-      cx += 1;
-    }
-    if (!(flags[rowa + qx] & 1) && !(flags[rowb + qx] & 1)) {
-      sy += (uint32_t)abs(luma(vox[rowb + qx]) - luma(vox[rowa + qx]));
-      cy += 1;
-    }
+  for (int k = threadIdx.x; k <= threadIdx.x + 2 * h; ++k) {  // qx = x - h .. x + h (outside W: 0)
+    sx += gx[k] >> 1;
+    cx += gx[k] & 1u;
+    sy += gy[k] >> 1;
+    cy += gy[k] & 1u;
   }
   ws[row + x] = make_uint2((sx << 8) | cx, (sy << 8) | cy);
 }
@@ -421,7 +436,7 @@ vinp_status vinp_texture_features(const vinp_params* prm, vinp_level* lv, int L,
   cudaStream_t s = S(stream);
   const vinp_level& a = lv[0];
   dim3 grd(nblk(a.W, 128), a.H, a.T);
-  k_tex_rows<<<grd, 128, 0, s>>>(a.vox, a.flags, a.W, a.H, a.T, h, (uint2*)ws);
+  k_tex_rows<<<dim3(nblk(a.W, kTexTile), a.H, a.T), kTexTile, 0, s>>>(a.vox, a.flags, a.W, a.H, a.T, h, (uint2*)ws);
   k_tex_cols<<<grd, 128, 0, s>>>((const uint2*)ws, a.W, a.H, a.T, h, a.vox);
   count_launch(2);
   for (int l = 1; l < L; ++l) {
