@@ -147,23 +147,41 @@ __global__ void __launch_bounds__(kTexTile) k_tex_rows(const uint64_t* __restric
 }
 
 // vertical window sums -> T_q = floor((S + 500c)/(1000c)) into level-1 texture bytes
+// A thread walks kColChunk rows of one column with a running window sum (add the entering row,
+// subtract the leaving one: the same exact integer sums as summing the 2h + 1 rows afresh).
+constexpr int kColChunk = 64;
 __global__ void k_tex_cols(const uint2* __restrict__ ws, int W, int H, int T, int h,
                            uint64_t* __restrict__ vox) {
-  int x = blockIdx.x * blockDim.x + threadIdx.x;
-  int y = blockIdx.y;
-  int t = blockIdx.z;
+  const int x = blockIdx.x * blockDim.x + threadIdx.x;
+  const int y0 = blockIdx.y * kColChunk, t = blockIdx.z;
   if (x >= W) return;
+  const int y1 = min(H, y0 + kColChunk);
+  const int64_t col = (int64_t)t * H * W + x;
   uint64_t sx = 0, cx = 0, sy = 0, cy = 0;
-  for (int qy = max(0, y - h); qy <= min(H - 1, y + h); ++qy) {
-    uint2 v = ws[((int64_t)t * H + qy) * W + x];
+  for (int qy = max(0, y0 - h); qy <= min(H - 1, y0 + h); ++qy) {
+    uint2 v = ws[col + (int64_t)qy * W];
     sx += v.x >> 8; cx += v.x & 255;
     sy += v.y >> 8; cy += v.y & 255;
   }
-  uint32_t tx = cx ? (uint32_t)((sx + 500 * cx) / (1000 * cx)) : 0;
-  uint32_t ty = cy ? (uint32_t)((sy + 500 * cy) / (1000 * cy)) : 0;
-  int64_t o = ((int64_t)t * H + y) * W + x;
-  uint64_t w = vox[o] & 0xffffffffull;
-  vox[o] = w | ((uint64_t)(tx | (ty << 8)) << 32);
+  for (int y = y0; y < y1; ++y) {
+    if (y > y0) {
+      if (y + h < H) {
+        uint2 v = ws[col + (int64_t)(y + h) * W];
+        sx += v.x >> 8; cx += v.x & 255;
+        sy += v.y >> 8; cy += v.y & 255;
+      }
+      if (y - h - 1 >= 0) {
+        uint2 v = ws[col + (int64_t)(y - h - 1) * W];
+        sx -= v.x >> 8; cx -= v.x & 255;
+        sy -= v.y >> 8; cy -= v.y & 255;
+      }
+    }
+    uint32_t tx = cx ? (uint32_t)((sx + 500 * cx) / (1000 * cx)) : 0;
+    uint32_t ty = cy ? (uint32_t)((sy + 500 * cy) / (1000 * cy)) : 0;
+    int64_t o = col + (int64_t)y * W;
+    uint64_t w = vox[o] & 0xffffffffull;
+    vox[o] = w | ((uint64_t)(tx | (ty << 8)) << 32);
+  }
 }
 
 // Eq. 10 with R16: T^l(x,y,t) = T(2^(l-1) x, 2^(l-1) y, t)
@@ -435,9 +453,9 @@ vinp_status vinp_texture_features(const vinp_params* prm, vinp_level* lv, int L,
   VINP_REQUIRE(h <= 32, "vinp_texture_features: tex_half > 32 unsupported");
   cudaStream_t s = S(stream);
   const vinp_level& a = lv[0];
-  dim3 grd(nblk(a.W, 128), a.H, a.T);
   k_tex_rows<<<dim3(nblk(a.W, kTexTile), a.H, a.T), kTexTile, 0, s>>>(a.vox, a.flags, a.W, a.H, a.T, h, (uint2*)ws);
-  k_tex_cols<<<grd, 128, 0, s>>>((const uint2*)ws, a.W, a.H, a.T, h, a.vox);
+  k_tex_cols<<<dim3(nblk(a.W, 128), nblk(a.H, kColChunk), a.T), 128, 0, s>>>((const uint2*)ws, a.W, a.H, a.T, h,
+                                                                             a.vox);
   count_launch(2);
   for (int l = 1; l < L; ++l) {
     dim3 g2(nblk(lv[l].W, 128), lv[l].H, lv[l].T);
