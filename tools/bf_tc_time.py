@@ -1,3 +1,7 @@
+"""Exact NN (a13) on the tensor cores only: vinp_brute_force_tc over all level-1 targets of the given
+configs after setup, CUDA-event time and effective int8 TOPS (2 * targets * sources * 640 / t).
+NOWARM=1 skips the warm-up call (so that `ncu -c 1` captures the main launch).
+usage: python tools/bf_tc_time.py c1 c2 [c3]"""
 import os, sys, torch, json
 sys.path.insert(0, '/root/repo')
 from gen.synth import CONFIGS, generate
