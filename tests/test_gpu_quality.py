@@ -92,7 +92,8 @@ def test_patchmatch_quality_after_full_run(name):
     with open(os.path.join(ROOT, "gpurun_out", f"quality_final_{name}.json"), "w") as f:
         json.dump(q, f)
     print(json.dumps(q))
-    assert q["ratio_minus_1"] <= 0.25
+    # measured (deterministic): c1 +2.8%, c2 +5.4%, c3 +2.3%; the bounds catch regressions
+    assert q["ratio_minus_1"] <= {"c1": 0.04, "c2": 0.065, "c3": 0.035}[name]
 
 
 @pytest.mark.parametrize("name", ["c1", "c2", "c3"])
@@ -102,5 +103,6 @@ def test_patchmatch_quality_vs_brute_force(name):
     with open(os.path.join(ROOT, "gpurun_out", f"quality_{name}.json"), "w") as f:
         json.dump(q, f)
     print(json.dumps(q))
-    # The north_star target is 5%; the test guards the measured level (DESIGN.md §6 reports it).
-    assert q["ratio_minus_1"] <= 0.25
+    # The north_star target is 5%; at this hardest point (right after upsampling) the measured
+    # levels are c1 +5.4%, c2 +7.3%, c3 +20.4%; the bounds catch regressions
+    assert q["ratio_minus_1"] <= {"c1": 0.065, "c2": 0.085, "c3": 0.22}[name]
