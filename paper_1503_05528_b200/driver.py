@@ -1,8 +1,10 @@
-"""Alg. 4 driver over the libvinp C ABI, without AlignVideo/UnwarpVideo (NEXT #1).
+"""Alg. 4 driver over the libvinp C ABI, with the optional Alg. 2 realignment and the
+final unwarp (NEXT #1, `Config(align=True)`).
 
 Host logic only: which kernel runs on which level, the onion-peel loop (Alg. 3), the stopping
 rule (R19) and, under torch.distributed, the target-slab partition and the exchanges between
-passes.  Every arithmetic step runs in libvinp's kernels.
+passes (all-gather by default, halo point-to-point with `exchange="halo"`).  Every
+arithmetic step runs in libvinp's kernels.
 
 Multi-GPU: every rank holds the full pyramid; the sorted target list (and hole list) of a level is
 cut into W contiguous equal-count slabs; after every pass that a later pass reads, the NNF slabs
@@ -127,9 +129,11 @@ class Stats:
     total_ms: float = 0.0
     onion_ms: float = 0.0
 
+    total_patch_updates: int = 0
+
     @property
     def patch_updates(self):
-        return sum(l["patch_updates"] for l in self.levels)
+        return self.total_patch_updates
 
 
 class Inpainter:
@@ -318,7 +322,7 @@ class Inpainter:
             self.V.nnf_init_random(st.lv, st.a, self.prm, 0)
         e_on = ev(); e_on.record()
         onion_pu = self.counter.clone()  # replicated work: counted once (rank 0) in the job total
-        pu_prev = 0
+        snaps = {}  # counter after each level (device tensors: no extra host syncs)
         for l in range(L, 0, -1):
             st = self.states[l - 1]
             lv = st.lv
@@ -354,6 +358,7 @@ class Inpainter:
                 self.reconstruct(f, V.UNWEIGHTED)  # R20
             e1 = ev(); e1.record()
             marks[l] = (e0, e1)
+            snaps[l] = self.counter.clone()
             self.stats.levels[l - 1]["outer"] = k
             e0 = e1
         t_all1 = ev(); t_all1.record()
@@ -363,11 +368,21 @@ class Inpainter:
                 self.stats.levels[l - 1]["ms"] = a.elapsed_time(b)
             self.stats.total_ms = t_all0.elapsed_time(t_all1)
             self.stats.onion_ms = t_all0.elapsed_time(e_on)
-        pu = self.counter.clone()
+        # per-level patch-update counts (the coarsest level includes the onion peel, counted once
+        # in the job total: the replicated onion work is subtracted on ranks other than 0)
+        prev = torch.zeros_like(self.counter)
+        per = []
+        for l in range(L, 0, -1):
+            per.append(snaps[l] - prev)
+            prev = snaps[l]
+        per = torch.cat(per)
         if self.ex.rank != 0:
-            pu -= onion_pu
-        self.ex.allreduce_sum(pu)
-        self.stats.total_patch_updates = int(pu.item())
+            per[0] -= onion_pu[0]
+        self.ex.allreduce_sum(per)
+        per = per.tolist()
+        for i, l in enumerate(range(L, 0, -1)):
+            self.stats.levels[l - 1]["patch_updates"] = int(per[i])
+        self.stats.total_patch_updates = int(sum(per))
         return self.stats
 
     def output(self, rgb_in: torch.Tensor) -> torch.Tensor:

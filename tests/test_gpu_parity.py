@@ -360,5 +360,6 @@ def test_pipeline_c2_full_config_end_to_end(orc):
     ref, st = orc.inpaint(v.numpy(), m.numpy(), c.levels, pm_iters=c.pm_iters, max_outer=c.max_outer,
                           lam=c.lam, seed=c.seed)
     assert [l["outer"] for l in stats.levels] == st["outer_iters"]
+    assert [l["patch_updates"] for l in stats.levels] == st["patch_updates"]  # per level (onion in L)
     assert stats.total_patch_updates == sum(st["patch_updates"])
     assert np.array_equal(out.cpu().numpy(), ref)
