@@ -217,7 +217,9 @@ def main():
         # per-level seconds (one timed run with per-level events)
         ip.load(v, m)
         stats = ip.run(timing=True)
-        levels = [{"level": l["level"], "outer": l["outer"], "s": l["ms"] / 1000.0} for l in stats.levels]
+        levels = [{"level": l["level"], "outer": l["outer"], "s": l["ms"] / 1000.0,
+                   "ms_per_outer": l["ms"] / max(l["outer"], 1), "patch_updates": l["patch_updates"]}
+                  for l in stats.levels]
         levels[-1]["onion_s"] = stats.onion_ms / 1000.0
         # dominant-kernel roofline: one instrumented step with events around every pass
         roof = measure_roofline(ip, v, m, dev)
