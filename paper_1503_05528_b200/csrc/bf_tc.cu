@@ -239,6 +239,7 @@ __global__ void __launch_bounds__(kBfThreads, 1) k_bf_tc2(const uint8_t* __restr
     const int row = 32 * q + lane;
     int32_t bestS = 0x7fffffff;
     int bestI = 0x7fffffff;
+    const uint32_t lam2 = 2u * (uint32_t)lambda;
     for (int i = 0; i < nt; ++i) {
       const int sa = i & 1;
       tc::mbar_wait(&afull[sa], (i >> 1) & 1);
@@ -260,7 +261,7 @@ __global__ void __launch_bounds__(kBfThreads, 1) k_bf_tc2(const uint8_t* __restr
 #pragma unroll
           for (int u = 0; u < 4; ++u) {
             const int j = 4 * j4 + u;
-            sv[j] = (int32_t)((uint32_t)e4[u] - 2u * (4u * c[j] + (uint32_t)lambda * x[j]));  // exact mod 2^32
+            sv[j] = (int32_t)((uint32_t)e4[u] - lam2 * x[j] - 8u * c[j]);  // exact mod 2^32 (2 IMADs)
             tmin = min(tmin, sv[j]);
           }
         }
