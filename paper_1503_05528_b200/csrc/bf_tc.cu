@@ -289,7 +289,8 @@ __global__ void __launch_bounds__(kBfThreads, 1) k_bf_tc2(const uint8_t* __restr
     if (h == 0) {
       uint32_t D2 = mD[row];
       int I2 = mI[row];
-      if (D2 < bestD || (D2 == bestD && I2 < bestI)) {
+      // (a half that saw only padding columns has no index: skip it)
+      if (I2 != 0x7fffffff && (bestI == 0x7fffffff || D2 < bestD || (D2 == bestD && I2 < bestI))) {
         bestD = D2;
         bestI = I2;
       }
