@@ -53,3 +53,34 @@ def test_ambiguity_gpu_statistics(orc):
         p = orc.ambiguity_exact(N)
         h = int(V.patch_ambiguity(N, n, 5.0, 11).item())
         assert abs(h / n - p) < 5 * math.sqrt(p * (1 - p) / n)
+
+
+@pytest.mark.parametrize("dims,hf,seed", [((16, 14, 7), 0.3, 1), ((20, 12, 7), 0.3, 4), ((18, 16, 8), 0.25, 2)])
+def test_brute_force_tc_few_sources(orc, dims, hf, seed):
+    """48-144 sources: one or two source tiles, mostly padding (masked columns, padding-only column
+    halves), and fewer targets than a 128-row tile.  Tensor cores == CUDA cores == oracle."""
+    from gen.synth import random_volume
+    from paper_1503_05528_b200 import Config, Inpainter, vinp as V
+    import oracle_ops as OO
+    W, H, T = dims
+    v, m, _ = random_volume(W, H, T, seed=seed, hole_frac=hf)
+    ip = Inpainter(W, H, T, Config(levels=1), "cuda")
+    ip.load(v.cuda(), m.cuda())
+    lv = ip.levels[0]
+    assert lv.n_sources < 160
+    x = V.NNF.alloc(lv.n_targets, "cuda")
+    y = V.NNF.alloc(lv.n_targets, "cuda")
+    V.brute_force(lv, x, ip.prm, 0, lv.n_targets)
+    V.brute_force_tc(lv, y, ip.prm, 0, lv.n_targets)
+    torch.cuda.synchronize()
+    assert torch.equal(x.e[:lv.n_targets], y.e[:lv.n_targets]) and torch.equal(x.n[:lv.n_targets], y.n[:lv.n_targets])
+    host = V.Level(lv.W, lv.H, lv.T, 1, torch.device("cpu"))
+    for name in ("vox", "flags", "slot", "targets", "holes", "sources"):
+        setattr(host, name, getattr(lv, name).cpu())
+    host.n_targets, host.n_holes, host.n_sources = lv.n_targets, lv.n_holes, lv.n_sources
+    ol = OO._OLevel(host)
+    f = orc.NNF.empty(lv.n_targets)
+    orc.brute_force(ol, f, ip.prm.lam)
+    g = OO._to_orc(host, V.NNF(y.e.cpu(), y.n.cpu()))
+    for arr in ("dx", "dy", "dt", "D", "n"):
+        assert np.array_equal(getattr(f, arr)[:lv.n_targets], getattr(g, arr)[:lv.n_targets]), arr
