@@ -65,6 +65,20 @@ struct Pix {
   int x0, y0;
 };
 
+// R37: warped position of pixel (i, j) and the top-left corner of its bilinear footprint
+__device__ __forceinline__ void irls_pos(int W, int H, const double* p, double cx, double cy, double s, int i,
+                                         int j, double& X, double& Y, double& xw, double& yw, int& x0,
+                                         int& y0) {
+  X = ((double)i - cx) / s;
+  Y = ((double)j - cy) / s;
+  xw = ((p[0] + p[1] * X) + p[2] * Y) + cx;
+  yw = ((p[3] + p[4] * X) + p[5] * Y) + cy;
+  x0 = (int)floor(xw);
+  y0 = (int)floor(yw);
+  if (x0 > W - 2) x0 = W - 2;
+  if (y0 > H - 2) y0 = H - 2;
+}
+
 // R37: a pixel of frame a votes iff unoccluded, its warp lands in [0, W-1] x [0, H-1], and no
 // pixel the bilinear sample or its gradient reads in frame b (4x4 block x0-1..x0+2, y0-1..y0+2,
 // clamped) is occluded.  Db = that 4x4 dilation of frame b's mask, precomputed (k_mask_dil).
@@ -72,13 +86,10 @@ __device__ __forceinline__ bool irls_pixel(const double* Ia, const uint8_t* Ma, 
                                            const uint8_t* Db, int W, int H, const double* p, double cx,
                                            double cy, double s, int i, int j, Pix& o) {
   if (Ma[(int64_t)j * W + i]) return false;
-  double X = ((double)i - cx) / s, Y = ((double)j - cy) / s;
-  double xw = ((p[0] + p[1] * X) + p[2] * Y) + cx;
-  double yw = ((p[3] + p[4] * X) + p[5] * Y) + cy;
+  double X, Y, xw, yw;
+  int x0, y0;
+  irls_pos(W, H, p, cx, cy, s, i, j, X, Y, xw, yw, x0, y0);
   if (!(xw >= 0.0 && xw <= (double)(W - 1) && yw >= 0.0 && yw <= (double)(H - 1))) return false;
-  int x0 = (int)floor(xw), y0 = (int)floor(yw);
-  if (x0 > W - 2) x0 = W - 2;
-  if (y0 > H - 2) y0 = H - 2;
   if (Db[(int64_t)y0 * W + x0]) return false;
   o.fx = xw - (double)x0;
   o.fy = yw - (double)y0;
@@ -152,6 +163,7 @@ struct IrlsLevel {
   int* iters;        // [npairs] running IRLS iteration count
   uint64_t* keys;    // [npairs][keys_stride] |r| keys, then the odd candidate lists
   uint64_t* cand;    // [npairs][keys_stride] the even candidate lists
+  double* rres;      // [npairs][keys_stride] pass-1 residual per pixel (NaN: not voting)
   int64_t keys_stride;
   int max_iter;
   double tol;
@@ -238,6 +250,7 @@ __global__ void __cluster_dims__(kCl, 1, 1) __launch_bounds__(kIrlsThreads, VINP
   const int64_t c0 = (int64_t)rk * rows_per * W;
   uint64_t* bufA = a.keys + (int64_t)n * a.keys_stride + c0;
   uint64_t* bufB = a.cand + (int64_t)n * a.keys_stride + c0;
+  double* rres = a.rres + (int64_t)n * a.keys_stride;
   const double cx = (double)(W - 1) * 0.5, cy = (double)(H - 1) * 0.5;
   const double s = (double)(W > H ? W : H) * 0.5;
 
@@ -274,6 +287,7 @@ __global__ void __cluster_dims__(kCl, 1, 1) __launch_bounds__(kIrlsThreads, VINP
         Pix o;
         ok = irls_pixel(Ia, Ma, Ib, Db, W, H, p, cx, cy, s, i, j, o);
         key = (unsigned long long)__double_as_longlong(fabs(o.r));
+        rres[(int64_t)j * W + i] = ok ? o.r : __longlong_as_double(0x7ff8000000000001ll);
       }
       unsigned bal = __ballot_sync(kFull, ok);
       unsigned off = 0;
@@ -346,16 +360,19 @@ __global__ void __cluster_dims__(kCl, 1, 1) __launch_bounds__(kIrlsThreads, VINP
       double w = 0.0, r = 0.0, J[6] = {0.0, 0.0, 0.0, 0.0, 0.0, 0.0};
       if (id < myN) {
         int jr = (int)(id / W), i = (int)(id - (int64_t)jr * W), j = (int)rk + kCl * jr;
-        Pix o;
-        if (irls_pixel(Ia, Ma, Ib, Db, W, H, p, cx, cy, s, i, j, o)) {
-          double u = o.r / c;
+        const double rr = rres[(int64_t)j * W + i];  // pass 1's residual (NaN: not voting)
+        if (rr == rr) {
+          double u = rr / c;
           if (fabs(u) < 1.0) {
             ok = true;
             double q = 1.0 - u * u;
             w = q * q;
-            r = o.r;
+            r = rr;
+            Pix o;
+            double xw, yw;
+            irls_pos(W, H, p, cx, cy, s, i, j, o.X, o.Y, xw, yw, o.x0, o.y0);
             int x0 = o.x0, y0 = o.y0;
-            double fx = o.fx, fy = o.fy;
+            double fx = xw - (double)x0, fy = yw - (double)y0;
             double g00 = gradx(Ib, W, x0, y0), g10 = gradx(Ib, W, x0 + 1, y0);
             double g01 = gradx(Ib, W, x0, y0 + 1), g11 = gradx(Ib, W, x0 + 1, y0 + 1);
             double gx = (1.0 - fy) * ((1.0 - fx) * g00 + fx * g10) + fy * ((1.0 - fx) * g01 + fx * g11);
@@ -601,6 +618,7 @@ struct AlignWs {
   int W[8], H[8];
   uint64_t* keys;
   uint64_t* cand;
+  double* rres;
   int64_t stride;
   double* p;
   size_t bytes;
@@ -626,6 +644,8 @@ AlignWs carve(void* base, int W, int H, int T, int L) {
   off += al((size_t)w.stride * (T > 1 ? T - 1 : 1) * sizeof(uint64_t));
   w.cand = (uint64_t*)(c ? c + off : nullptr);
   off += al((size_t)w.stride * (T > 1 ? T - 1 : 1) * sizeof(uint64_t));
+  w.rres = (double*)(c ? c + off : nullptr);
+  off += al((size_t)w.stride * (T > 1 ? T - 1 : 1) * sizeof(double));
   w.p = (double*)(c ? c + off : nullptr);
   off += al((size_t)(T > 1 ? T - 1 : 1) * 6 * sizeof(double));
   w.bytes = off;
@@ -682,7 +702,7 @@ vinp_status vinp_affine_estimate(const uint8_t* rgb, const uint8_t* mask, int W,
     }
     const int64_t fk = (int64_t)w.W[k] * w.H[k] * p0;  // first frame of the range at level k
     IrlsLevel a{w.I[k] + fk, w.M[k] + fk, w.D[k] + fk, w.W[k], w.H[k], w.p, status + p0, iters + p0, w.keys,
-                w.cand, w.stride, max_iter, tol};
+                w.cand, w.rres, w.stride, max_iter, tol};
     k_irls<<<np * kCl, kIrlsThreads, 0, s>>>(a);
     count_launch();
   }
