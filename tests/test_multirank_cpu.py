@@ -146,3 +146,42 @@ def test_aligned_two_ranks_split_pairs(tmp_path, orc):
     assert np.array_equal(np.load(out + ".theta.npy"), pairs)
     o, _ = orc.inpaint(ar, am, CFG["levels"], pm_iters=CFG["pm_iters"], max_outer=CFG["max_outer"])
     assert np.array_equal(np.load(out), orc.unwarp(o, v.numpy(), m.numpy(), fwd))
+
+
+def _run_cfg(rank, world, port, out_path, spec):
+    os.environ.update(MASTER_ADDR="127.0.0.1", MASTER_PORT=str(port))
+    dist.init_process_group("gloo", rank=rank, world_size=world)
+    try:
+        import oracle_ops
+        from gen.synth import random_holes
+        from paper_1503_05528_b200 import Config, Exchange, inpaint
+        W, H, T, seed, levels, steps, exchange = spec
+        v, _, _ = random_volume(W, H, T, seed=seed)
+        m = random_holes(W, H, T, seed, 2)
+        v[m.bool()] = 0
+        cfg = Config(levels=levels, pm_iters=2, max_outer=2, steps=steps, exchange=exchange)
+        out, stats, _ = inpaint(v, m, cfg, device="cpu", exchange=Exchange(), ops=oracle_ops)
+        if rank == 0:
+            np.save(out_path, out.numpy())
+            np.save(out_path + ".stats.npy", np.array([l["outer"] for l in stats.levels] +
+                                                      [l["patch_updates"] for l in stats.levels]))
+    finally:
+        dist.destroy_process_group()
+
+
+@pytest.mark.parametrize("world,W,H,T,seed,levels,steps", [
+    (2, 36, 28, 30, 11, 2, (8, 4, 2, 1)),
+    (3, 30, 24, 41, 12, 1, (16, 8, 4, 2, 1)),
+    (4, 28, 24, 44, 13, 2, (4, 2, 1)),
+])
+def test_halo_fuzz_equals_single_rank(tmp_path, world, W, H, T, seed, levels, steps):
+    """random hole shapes, frame counts, level counts and step schedules (max step 16 widens the
+    halo): the halo exchange at world sizes 2-4 equals the single-rank run, per-level counts too"""
+    outs = []
+    for wsz, ex in ((1, "allgather"), (world, "halo")):
+        out = str(tmp_path / f"fz_{wsz}_{ex}.npy")
+        mp.spawn(_run_cfg, args=(wsz, _free_port(), out, (W, H, T, seed, levels, steps, ex)), nprocs=wsz,
+                 join=True)
+        outs.append((np.load(out), np.load(out + ".stats.npy")))
+    assert np.array_equal(outs[0][0], outs[1][0])
+    assert np.array_equal(outs[0][1], outs[1][1])
