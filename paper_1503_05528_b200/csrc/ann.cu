@@ -2,13 +2,13 @@
 // propagation (a6), Philox random search (a7), the Alg. 1 schedule (a8), exact brute force (a13,
 // CUDA-core form), and the SSD / Philox test hooks.
 //
-// Execution model: one warp per target p.  The warp holds the target patch N_p in registers
-// (lane l owns voxels v = l + 32i, i < 4) and evaluates each candidate source patch with one
-// coalesced 8-byte gather per voxel, VABSDIFF4 + IDP.4A per colour / texture word and one
-// REDUX.SUM across the warp (common.cuh).  Candidate generation (neighbour shifts, Philox draws,
-// validity, de-duplication) is spread across lanes, so a candidate costs ~4 loads + 20 ALU ops
-// per lane.  Every pass reads NNF buffer `in` and writes `out` (double buffering): no atomics
-// on the NNF, results independent of scheduling.
+// Execution model: evaluate and propagation run thread-per-target (lane = an
+// x-adjacent target, so the coherent candidate gathers coalesce), random search runs 5-lane column
+// groups over a per-warp pair queue (incoherent candidates), onion-layer propagation runs warp per
+// target (short latency chain for small launches).  Distances are exact integers (VABSDIFF4 +
+// IDP.4A per colour / texture word); early aborts change no comparison.  Every pass reads NNF
+// buffer `in` and writes `out` (double buffering): no atomics on the NNF, results independent of
+// scheduling.
 #include <vector>
 
 #include "common.cuh"
@@ -325,6 +325,134 @@ __global__ void __launch_bounds__(256, KB ? 2 : VINP_PROP_MINB) k_propagate(Leve
   if ((threadIdx.x & 31) == 0) flush_count(counter, cnt);
 }
 
+// Onion (K-restricted) propagation pass, warp per target.  An onion layer holds a few hundred to
+// a few ten thousand targets, so the thread-per-target pass above runs as one latency chain per
+// lane (candidate generation, then per frame layer bytes -> predicated voxels, up to 15 frames):
+// ~40 us per launch whatever its size, x 880 launches per c5 step.  Here the 125 voxels of the
+// patch are spread over the warp (lane l owns k = l + 32 j), the (up to 6) candidates are
+// generated by lanes 0..nc-1 in parallel, and all candidate gathers are issued at once, so the
+// chain is ~8 round trips.  No early abort: a candidate is kept iff D < best in rank order (R25),
+// the same decision the aborting pass takes; counts one patch-update per evaluated candidate.
+// Warp-per-target patch (onion passes): lane l owns the voxels k = l + 32 j (j < 4, k < 125) of
+// N_p; a voxel outside Omega or K contributes nothing (its target word is zeroed and its source
+// gather skipped).  load() issues the gathers, mask() consumes the layer bytes.
+struct WideTarget {
+  uint64_t tv[4];
+  uint8_t lay[4];
+  int off[4];
+  bool ok[4];
+  __device__ __forceinline__ void load(const LevelArgs& a, int p, int px, int py, int pt, int lane) {
+    const unsigned long long* v = reinterpret_cast<const unsigned long long*>(a.vox);
+#pragma unroll
+    for (int j = 0; j < 4; ++j) {
+      const int k = lane + 32 * j;
+      const int dt = k / 25 - 2, dy = (k % 25) / 5 - 2, dx = k % 5 - 2;
+      off[j] = dt * a.g.HW + dy * a.g.W + dx;
+      ok[j] = k < 125 && inside(a.g, px + dx, py + dy, pt + dt);
+      lay[j] = ok[j] ? a.layer[p + off[j]] : (uint8_t)255;
+      tv[j] = ok[j] ? __ldg(v + (p + off[j])) : 0ull;
+    }
+  }
+  __device__ __forceinline__ void mask(int kb) {
+#pragma unroll
+    for (int j = 0; j < 4; ++j) {
+      ok[j] = ok[j] && (kb < 0 || (int)lay[j] < kb);
+      if (!ok[j]) tv[j] = 0ull;
+    }
+  }
+  // this lane's share of D(p, q) (Eq. 9, R24 integer form); q in D~, so every gather is in bounds
+  __device__ __forceinline__ uint32_t part(const unsigned long long* v, int q, int lambda) const {
+    uint64_t sv[4];
+#pragma unroll
+    for (int j = 0; j < 4; ++j) sv[j] = ok[j] ? __ldg(v + (q + off[j])) : 0ull;
+    uint32_t accc = 0, acct = 0;
+#pragma unroll
+    for (int j = 0; j < 4; ++j) VINP_ACC(tv[j], sv[j])
+    return 4u * accc + (uint32_t)lambda * acct;
+  }
+};
+
+#ifndef VINP_WIDE_BLOCK
+#define VINP_WIDE_BLOCK 64
+#endif
+#ifndef VINP_WIDE_MAX
+#define VINP_WIDE_MAX 0x7fffffff  // use the warp-per-target pass up to this many launch targets
+#endif
+__global__ void __launch_bounds__(VINP_WIDE_BLOCK) k_propagate_wide(
+    LevelArgs a, const uint64_t* __restrict__ ein, uint64_t* __restrict__ eout, int lambda,
+    int step, int sign, int kb, int only_layer, int32_t b, int32_t e,
+    const int32_t* __restrict__ list, unsigned long long* counter) {
+  const int lane = threadIdx.x & 31;
+  const int idx = b + (int)((blockIdx.x * (unsigned)blockDim.x + threadIdx.x) >> 5);
+  if (idx >= e) return;  // warp-uniform
+  const int s = list ? __ldg(list + idx) : idx;
+  const int p = __ldg(a.targets + s);
+  const uint64_t inc = __ldg(reinterpret_cast<const unsigned long long*>(ein) + s);
+  const bool act = only_layer < 0 || a.layer[p] == only_layer;  // used at the end: no stall here
+  const unsigned long long* v = reinterpret_cast<const unsigned long long*>(a.vox);
+  int px, py, pt;
+  decode(a.g, p, px, py, pt);
+  // the target side first (independent of the candidates, in flight during their generation)
+  WideTarget w;
+  w.load(a, p, px, py, pt, lane);
+  const int nc = sign == 0 ? 6 : 3;
+  // candidate c on lane c (neighbour shift -> its NNF entry -> q = p + (src - r) -> q in D~?)
+  int myq = -1;
+  if (lane < nc) {
+    const int c = lane;
+    const int sg = sign != 0 ? sign : (c < 3 ? -1 : 1);
+    const int ax = c % 3;
+    const int ox = ax == 0 ? sg * step : 0, oy = ax == 1 ? sg * step : 0, ot = ax == 2 ? sg * step : 0;
+    const int rx = px + ox, ry = py + oy, rt = pt + ot;
+    if (inside(a.g, rx, ry, rt)) {
+      const int rs = __ldg(a.slot + lin(a.g, rx, ry, rt));
+      if (rs >= 0) {
+        const int src = e_q(__ldg(reinterpret_cast<const unsigned long long*>(ein) + rs));
+        int sx, sy, st;
+        decode(a.g, src, sx, sy, st);
+        const int qx = sx - ox, qy = sy - oy, qt = st - ot;
+        if (is_source(a.g, a.flags, qx, qy, qt)) myq = lin(a.g, qx, qy, qt);
+      }
+    }
+  }
+  w.mask(kb);
+  // de-duplicate exactly as the thread pass: drop a candidate equal to the incumbent or to an
+  // earlier candidate
+  const int q0 = e_q(inc);
+  int q[6];
+#pragma unroll
+  for (int c = 0; c < 6; ++c) q[c] = __shfl_sync(kFull, myq, c);
+  bool keep[6];
+#pragma unroll
+  for (int c = 0; c < 6; ++c) {
+    bool dup = !act || c >= nc || q[c] < 0 || q[c] == q0;
+#pragma unroll
+    for (int c2 = 0; c2 < c; ++c2) dup |= (q[c2] == q[c]);
+    keep[c] = !dup;
+  }
+  // all candidate gathers in flight together (q in D~: its whole patch lies in the volume)
+  uint32_t part[6];
+#pragma unroll
+  for (int c = 0; c < 6; ++c) part[c] = keep[c] ? w.part(v, q[c], lambda) : 0u;
+  uint32_t bestD = e_D(inc);
+  int bestq = q0;
+  unsigned cnt = 0;
+#pragma unroll
+  for (int c = 0; c < 6; ++c) {
+    if (!keep[c]) continue;  // warp-uniform
+    const uint32_t D = __reduce_add_sync(kFull, part[c]);
+    if (D < bestD) {
+      bestD = D;
+      bestq = q[c];
+    }
+    ++cnt;
+  }
+  if (lane == 0) {
+    eout[s] = pack_e(bestD, bestq);
+    flush_count(counter, cnt);
+  }
+}
+
 // ------------------------------------------------------------------ a7: random search pass
 struct Radii {
   double R[32];
@@ -489,6 +617,78 @@ __global__ void __launch_bounds__(32 * WPB, VINP_MINB * 8 / WPB) k_random_search
   }
   if (have) eout[s] = pack_e(bestD, bestq);
   if (lane == 0) flush_count(counter, (unsigned)P);
+}
+
+// Random search for onion (K-restricted) launches, warp per target: lane i < M draws candidate
+// i + 1 of Eq. 3 (Philox, the same draw and fp64 offset arithmetic as above, so the same q), the
+// warp de-duplicates (a candidate equal to the incumbent or to an earlier valid one is dropped),
+// then evaluates the kept candidates 4 at a time with every gather of a batch in flight and
+// applies them in rank order with strict improvement (R25).
+__global__ void __launch_bounds__(VINP_WIDE_BLOCK) k_random_search_wide(
+    LevelArgs a, const uint64_t* __restrict__ ein, uint64_t* __restrict__ eout, int lambda, Radii rad,
+    uint64_t seed, uint32_t oc, int pm_iter, int kb, int only_layer, int32_t b, int32_t e,
+    const int32_t* __restrict__ list, unsigned long long* counter) {
+  const int lane = threadIdx.x & 31;
+  const int idx = b + (int)((blockIdx.x * (unsigned)blockDim.x + threadIdx.x) >> 5);
+  if (idx >= e) return;  // warp-uniform
+  const int s = list ? __ldg(list + idx) : idx;
+  const int p = __ldg(a.targets + s);
+  const uint64_t inc = __ldg(reinterpret_cast<const unsigned long long*>(ein) + s);
+  const bool act = only_layer < 0 || a.layer[p] == only_layer;
+  const unsigned long long* v = reinterpret_cast<const unsigned long long*>(a.vox);
+  int px, py, pt;
+  decode(a.g, p, px, py, pt);
+  WideTarget w;
+  w.load(a, p, px, py, pt, lane);
+  const int q0 = e_q(inc);
+  int myq = -1;
+  if (lane < rad.M) {  // candidate i + 1 = lane + 1
+    int q0x, q0y, q0t;
+    decode(a.g, q0, q0x, q0y, q0t);
+    uint4 u = draw((uint32_t)p, (uint32_t)pm_iter, a.level, kStreamRS, lane + 1, oc, seed);
+    double R = rad.R[lane];
+    int ox = (int)floor(__dmul_rn(R, __dmul_rn((double)u.x - 2147483648.0, 4.656612873077392578125e-10)));
+    int oy = (int)floor(__dmul_rn(R, __dmul_rn((double)u.y - 2147483648.0, 4.656612873077392578125e-10)));
+    int ot = (int)floor(__dmul_rn(R, __dmul_rn((double)u.z - 2147483648.0, 4.656612873077392578125e-10)));
+    int qx = q0x + ox, qy = q0y + oy, qt = q0t + ot;
+    if (is_source(a.g, a.flags, qx, qy, qt)) myq = lin(a.g, qx, qy, qt);
+  }
+  w.mask(kb);
+  // keep[i]: valid, not the incumbent, not equal to an earlier valid candidate
+  bool keep = act && myq >= 0 && myq != q0;
+  for (int i = 0; i < rad.M; ++i) {
+    const int qi = __shfl_sync(kFull, myq, i);
+    if (i < lane && qi >= 0 && qi == myq) keep = false;
+  }
+  unsigned km = __ballot_sync(kFull, keep);
+  const unsigned cnt = __popc(km);
+  uint32_t bestD = e_D(inc);
+  int bestq = q0;
+  while (km) {  // batches of 4 kept candidates, rank order
+    int qb[4];
+    uint32_t part[4];
+#pragma unroll
+    for (int c = 0; c < 4; ++c) {
+      const int i = km ? __ffs(km) - 1 : -1;
+      if (km) km &= km - 1u;
+      qb[c] = i >= 0 ? __shfl_sync(kFull, myq, i) : -1;
+    }
+#pragma unroll
+    for (int c = 0; c < 4; ++c) part[c] = qb[c] >= 0 ? w.part(v, qb[c], lambda) : 0u;
+#pragma unroll
+    for (int c = 0; c < 4; ++c) {
+      if (qb[c] < 0) break;  // warp-uniform
+      const uint32_t D = __reduce_add_sync(kFull, part[c]);
+      if (D < bestD) {
+        bestD = D;
+        bestq = qb[c];
+      }
+    }
+  }
+  if (lane == 0) {
+    eout[s] = pack_e(bestD, bestq);
+    flush_count(counter, cnt);
+  }
 }
 
 // ------------------------------------------------------------------ a13: brute force (CUDA cores)
@@ -697,7 +897,10 @@ vinp_status launch_propagate(const vinp_level* lv, const vinp_nnf* in, vinp_nnf*
   VINP_REQUIRE(step >= 1 && sign >= -1 && sign <= 1, "vinp_propagate: bad step/sign");
   VINP_REQUIRE((kb < 0 && only_layer < 0) || lv->layer, "vinp_propagate: layer map required");
   if (e > b) {
-    if (kb >= 0)
+    if (kb >= 0 && e - b <= VINP_WIDE_MAX)
+      k_propagate_wide<<<nblk((int64_t)(e - b) * 32, VINP_WIDE_BLOCK), VINP_WIDE_BLOCK, 0, S(stream)>>>(
+          args_of(lv), in->e, out->e, prm->lambda, step, sign, kb, only_layer, b, e, list, counter);
+    else if (kb >= 0)
       k_propagate<true><<<nblk(e - b, VINP_KB_BLOCK), VINP_KB_BLOCK, 0, S(stream)>>>(
           args_of(lv), in->e, out->e, prm->lambda, step, sign, kb, only_layer, b, e, list, counter);
     else
@@ -739,7 +942,12 @@ vinp_status launch_random_search(const vinp_level* lv, const vinp_nnf* in, vinp_
     set_error("vinp_random_search: more than 31 random-search radii (rho too close to 1)");
     return VINP_E_UNSUPPORTED;
   }
-  if (e > b) {
+  if (e > b && kb >= 0 && e - b <= VINP_WIDE_MAX && r.M <= 32) {
+    k_random_search_wide<<<nblk((int64_t)(e - b) * 32, VINP_WIDE_BLOCK), VINP_WIDE_BLOCK, 0, S(stream)>>>(
+        args_of(lv), in->e, out->e, prm->lambda, r, prm->seed, outer_code, pm_iter, kb, only_layer, b, e,
+        list, counter);
+    count_launch();
+  } else if (e > b) {
     cudaStream_t cs = S(stream);
     LevelArgs la = args_of(lv);
     const bool small = (e - b) < 148 * 32 * 8;
