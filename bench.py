@@ -311,13 +311,18 @@ def measure_roofline(ip, v, m, dev):
     wrap("random_search", lambda lv, *a, **k: (a[7], a[8]))
     wrap("nnf_evaluate", lambda lv, *a, **k: (a[4], a[5]))
     wrap("reconstruct", lambda lv, *a, **k: (a[5], a[6]))
+    # Alg. 3 as the step runs it (one vinp_onion_peel call, per-layer lists): timed as one entry,
+    # bytes = 625 B per patch-update of its passes
+    wrap("onion_peel", lambda lv, *a, **k: (0, 0))
     try:
         ip.native = False  # one C-ABI call per pass so that every launch is timed
+        ip.native_onion = True
         ip.load(v, m)
         ip.run(timing=False)
         torch.cuda.synchronize()
     finally:
         ip.native = True
+        ip.native_onion = False
         for k2, f in orig.items():
             setattr(V, k2, f)
     agg = {}

@@ -388,6 +388,12 @@ __global__ void __launch_bounds__(VINP_WIDE_BLOCK) k_propagate_wide(
   const int s = list ? __ldg(list + idx) : idx;
   const int p = __ldg(a.targets + s);
   const uint64_t inc = __ldg(reinterpret_cast<const unsigned long long*>(ein) + s);
+  // a filtered full-range launch (per-pass path): most warps leave here.  With a layer list
+  // (vinp_onion_peel) every target is in the layer, and the test waits until the end
+  if (!list && only_layer >= 0 && a.layer[p] != only_layer) {
+    if (lane == 0) eout[s] = inc;
+    return;
+  }
   const bool act = only_layer < 0 || a.layer[p] == only_layer;  // used at the end: no stall here
   const unsigned long long* v = reinterpret_cast<const unsigned long long*>(a.vox);
   int px, py, pt;
@@ -634,6 +640,10 @@ __global__ void __launch_bounds__(VINP_WIDE_BLOCK) k_random_search_wide(
   const int s = list ? __ldg(list + idx) : idx;
   const int p = __ldg(a.targets + s);
   const uint64_t inc = __ldg(reinterpret_cast<const unsigned long long*>(ein) + s);
+  if (!list && only_layer >= 0 && a.layer[p] != only_layer) {  // as k_propagate_wide
+    if (lane == 0) eout[s] = inc;
+    return;
+  }
   const bool act = only_layer < 0 || a.layer[p] == only_layer;
   const unsigned long long* v = reinterpret_cast<const unsigned long long*>(a.vox);
   int px, py, pt;

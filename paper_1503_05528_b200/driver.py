@@ -160,6 +160,7 @@ class Inpainter:
         self.stats = Stats()
         self.n_layers = 0
         self.native = True  # False: every pass through its own C-ABI call (per-launch timing)
+        self.native_onion = False  # True: Alg. 3 through vinp_onion_peel even when native is False
 
     # ------------------------------------------------------------------ setup (a1-a3)
     def load(self, rgb: torch.Tensor, mask: torch.Tensor):
@@ -316,7 +317,7 @@ class Inpainter:
         self.counter.zero_()
         e0 = ev(); e0.record()
         if cfg.onion:
-            self.onion_peel() if self.native else self.onion_peel_stepwise()
+            self.onion_peel() if (self.native or self.native_onion) else self.onion_peel_stepwise()
         else:
             st = self.states[-1]
             self.V.nnf_init_random(st.lv, st.a, self.prm, 0)
