@@ -160,11 +160,13 @@ __device__ __forceinline__ void recon_hole(const ReconArgs& a, const LaneVox& LV
                                                  max((valid & 4) ? hi[2] : 0u, (valid & 8) ? hi[3] : 0u)));
     uint32_t x = hmax ^ hmin;
     uint32_t ans = hmin & ~(x ? (0xffffffffu >> __clz(x)) : 0u);
+    // invalid keys are ~0, above every threshold T (valid high halves are < 2^31: D < 2^31, and
+    // a positive double has sign bit 0), so the counts need no validity test
     for (int bit = 31 - (x ? __clz(x) : 32); bit >= 0; --bit) {
       uint32_t T = ans | ((1u << bit) - 1);
       uint32_t c = 0;
 #pragma unroll
-      for (int i = 0; i < 4; ++i) c += ((valid >> i & 1) && hi[i] <= T);
+      for (int i = 0; i < 4; ++i) c += hi[i] <= T;
       c = __reduce_add_sync(kFull, c);
       if (c < r) ans |= 1u << bit;
     }
