@@ -115,7 +115,8 @@ __global__ void k_upsample(LevelArgs c, const uint64_t* __restrict__ ce, LevelAr
     accc = __dp4a(dc, dc, accc);                                              \
     acct = __dp4a(dx_, dx_, acct);                                            \
   }
-// KB = true (kernels launched for K-restricted onion passes): the non-interior path issues all
+// KB = true (the K-restricted onion evaluate; onion propagation / random search run the
+// warp-per-target kernels below): the non-interior path issues all
 // gathers of a frame together (in-Omega predicates, then the layer bytes of K, then the predicated
 // voxel loads) instead of one branch-guarded voxel at a time.
 template <bool ABORT, bool KB = false>
@@ -236,8 +237,7 @@ __global__ void __launch_bounds__(256) k_evaluate(LevelArgs a, uint64_t* __restr
 // Lane = target (thread-per-target, coherent candidates).  Candidates of rank 1..3 are evaluated
 // one rank at a time by all lanes that have one, each against the running best of its own target
 // (strict improvement in rank order, R25).
-template <bool KB>
-__global__ void __launch_bounds__(256, KB ? 2 : VINP_PROP_MINB) k_propagate(LevelArgs a, const uint64_t* __restrict__ ein,
+__global__ void __launch_bounds__(256, VINP_PROP_MINB) k_propagate(LevelArgs a, const uint64_t* __restrict__ ein,
                                                    uint64_t* __restrict__ eout, int lambda, int step,
                                                    int sign, int kb, int only_layer, int32_t b,
                                                    int32_t e, const int32_t* __restrict__ list,
@@ -311,8 +311,8 @@ __global__ void __launch_bounds__(256, KB ? 2 : VINP_PROP_MINB) k_propagate(Leve
     if (!__any_sync(kFull, mine)) break;
     if (mine) {
       bool alive = true;
-      uint32_t D = allfull ? thread_ssd<true, KB>(a, p, px, py, pt, cq[c], lambda, kb, true, bestD, alive)
-                           : thread_ssd<true, KB>(a, p, px, py, pt, cq[c], lambda, kb, full, bestD, alive);
+      uint32_t D = allfull ? thread_ssd<true>(a, p, px, py, pt, cq[c], lambda, kb, true, bestD, alive)
+                           : thread_ssd<true>(a, p, px, py, pt, cq[c], lambda, kb, full, bestD, alive);
       if (alive && D < bestD) {
         bestD = D;
         bestq = cq[c];
@@ -374,9 +374,6 @@ struct WideTarget {
 
 #ifndef VINP_WIDE_BLOCK
 #define VINP_WIDE_BLOCK 64
-#endif
-#ifndef VINP_WIDE_MAX
-#define VINP_WIDE_MAX 0x7fffffff  // use the warp-per-target pass up to this many launch targets
 #endif
 __global__ void __launch_bounds__(VINP_WIDE_BLOCK) k_propagate_wide(
     LevelArgs a, const uint64_t* __restrict__ ein, uint64_t* __restrict__ eout, int lambda,
@@ -477,12 +474,12 @@ __device__ __forceinline__ uint32_t sum5(uint32_t x, int base, int k) {
   return s2 + __shfl_sync(kFull, x, base + (k + 4) % 5);
 }
 
-template <int NC, int WPB, bool KNOWN, int TPW>
+template <int NC, int WPB, int TPW>
 __global__ void __launch_bounds__(32 * WPB, VINP_MINB * 8 / WPB) k_random_search(
     LevelArgs a, const uint64_t* __restrict__ ein, uint64_t* __restrict__ eout, int lambda, Radii rad,
-    uint64_t seed, uint32_t oc, int pm_iter, int kb, int only_layer, int32_t b, int32_t e,
+    uint64_t seed, uint32_t oc, int pm_iter, int only_layer, int32_t b, int32_t e,
     const int32_t* __restrict__ list, unsigned long long* counter) {
-  // TPW targets per warp (32; 8 for small launches, e.g. onion layers, so that more warps share
+  // TPW targets per warp (32; 8 for small launches, so that more warps share
   // the pair evaluations — the result does not depend on it)
   int lane = threadIdx.x & 31;
   int i0 = b + (blockIdx.x * WPB + (threadIdx.x >> 5)) * TPW;
@@ -579,7 +576,6 @@ __global__ void __launch_bounds__(32 * WPB, VINP_MINB * 8 / WPB) k_random_search
     for (int r = 0; r < 5; ++r) {
       ro[r] = dtc * a.g.HW + (r - 2) * a.g.W + dx;
       okr[r] = tok && (unsigned)(ty + r - 2) < (unsigned)a.g.H;
-      if (KNOWN) okr[r] = okr[r] && a.layer[pi + (okr[r] ? ro[r] : 0)] < kb;
     }
     uint64_t tv[5], sv[5];
 #pragma unroll
@@ -907,14 +903,11 @@ vinp_status launch_propagate(const vinp_level* lv, const vinp_nnf* in, vinp_nnf*
   VINP_REQUIRE(step >= 1 && sign >= -1 && sign <= 1, "vinp_propagate: bad step/sign");
   VINP_REQUIRE((kb < 0 && only_layer < 0) || lv->layer, "vinp_propagate: layer map required");
   if (e > b) {
-    if (kb >= 0 && e - b <= VINP_WIDE_MAX)
+    if (kb >= 0)  // K-restricted (onion) launch: warp per target
       k_propagate_wide<<<nblk((int64_t)(e - b) * 32, VINP_WIDE_BLOCK), VINP_WIDE_BLOCK, 0, S(stream)>>>(
           args_of(lv), in->e, out->e, prm->lambda, step, sign, kb, only_layer, b, e, list, counter);
-    else if (kb >= 0)
-      k_propagate<true><<<nblk(e - b, VINP_KB_BLOCK), VINP_KB_BLOCK, 0, S(stream)>>>(
-          args_of(lv), in->e, out->e, prm->lambda, step, sign, kb, only_layer, b, e, list, counter);
     else
-      k_propagate<false><<<nblk(e - b, VINP_PROP_BLOCK), VINP_PROP_BLOCK, 0, S(stream)>>>(
+      k_propagate<<<nblk(e - b, VINP_PROP_BLOCK), VINP_PROP_BLOCK, 0, S(stream)>>>(
           args_of(lv), in->e, out->e, prm->lambda, step, sign, kb, only_layer, b, e, list, counter);
     count_launch();
   }
@@ -952,7 +945,7 @@ vinp_status launch_random_search(const vinp_level* lv, const vinp_nnf* in, vinp_
     set_error("vinp_random_search: more than 31 random-search radii (rho too close to 1)");
     return VINP_E_UNSUPPORTED;
   }
-  if (e > b && kb >= 0 && e - b <= VINP_WIDE_MAX && r.M <= 32) {
+  if (e > b && kb >= 0) {  // K-restricted (onion) launch: warp per target (M <= 31 < 32 lanes)
     k_random_search_wide<<<nblk((int64_t)(e - b) * 32, VINP_WIDE_BLOCK), VINP_WIDE_BLOCK, 0, S(stream)>>>(
         args_of(lv), in->e, out->e, prm->lambda, r, prm->seed, outer_code, pm_iter, kb, only_layer, b, e,
         list, counter);
@@ -961,23 +954,15 @@ vinp_status launch_random_search(const vinp_level* lv, const vinp_nnf* in, vinp_
     cudaStream_t cs = S(stream);
     LevelArgs la = args_of(lv);
     const bool small = (e - b) < 148 * 32 * 8;
-#define VINP_RS2(NC, WPB, KN, TPW)                                                                 \
-  k_random_search<NC, WPB, KN, TPW><<<nblk(e - b, TPW * WPB), 32 * WPB, 0, cs>>>(                   \
-      la, in->e, out->e, prm->lambda, r, prm->seed, outer_code, pm_iter, kb, only_layer, b, e, list, \
-      counter)
-#define VINP_RS(NC, WPB)                                                                           \
-  do {                                                                                             \
-    if (kb >= 0) {                                                                                 \
-      if (small)                                                                                   \
-        VINP_RS2(NC, WPB, true, 8);                                                                \
-      else                                                                                         \
-        VINP_RS2(NC, WPB, true, 32);                                                               \
-    } else {                                                                                       \
-      if (small)                                                                                   \
-        VINP_RS2(NC, WPB, false, 8);                                                               \
-      else                                                                                         \
-        VINP_RS2(NC, WPB, false, 32);                                                              \
-    }                                                                                              \
+#define VINP_RS2(NC, WPB, TPW)                                                                       \
+  k_random_search<NC, WPB, TPW><<<nblk(e - b, TPW * WPB), 32 * WPB, 0, cs>>>(                           \
+      la, in->e, out->e, prm->lambda, r, prm->seed, outer_code, pm_iter, only_layer, b, e, list, counter)
+#define VINP_RS(NC, WPB)          \
+  do {                            \
+    if (small)                    \
+      VINP_RS2(NC, WPB, 8);       \
+    else                          \
+      VINP_RS2(NC, WPB, 32);      \
   } while (0)
     if (r.M <= 8)
       VINP_RS(8, VINP_RS_WPB);
