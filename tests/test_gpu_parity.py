@@ -186,10 +186,16 @@ def test_onion_restricted_passes_bit_exact(V, orc):
         V.nnf_evaluate(lv, a, ip.prm, kb, j)
         orc.evaluate(ol, f, lam, kb, j)
         assert len(B.nnf_equal(orc, lv, a.e, a.n, f)) == 0
-        g = f.copy()
-        V.propagate(lv, a, b, ip.prm, 2, -1, kb, j)
-        orc.propagate(ol, f, g, lam, 2, -1, kb, j)
-        assert len(B.nnf_equal(orc, lv, b.e, b.n, g)) == 0
+        # the warp-per-target onion kernels: both sign policies (3 and 6 candidates per target)
+        for step, sign in ((2, -1), (1, 0), (4, 1)):
+            g = f.copy()
+            V.propagate(lv, a, b, ip.prm, step, sign, kb, j)
+            orc.propagate(ol, f, g, lam, step, sign, kb, j)
+            assert len(B.nnf_equal(orc, lv, b.e, b.n, g)) == 0
+            a, b = b, a
+            f = g
+        a, b = b, a  # b: the last propagation result
+        g, f = f, f.copy()
         V.random_search(lv, b, a, ip.prm, oc, 1, kb, j)
         orc.random_search(ol, g, f, lam, seed, 0.5, lv.rmax, lv.level, oc, 1, kb, j)
         assert len(B.nnf_equal(orc, lv, a.e, a.n, f)) == 0
