@@ -90,9 +90,6 @@ __global__ void k_upsample(LevelArgs c, const uint64_t* __restrict__ ce, LevelAr
 #ifndef VINP_PROP_BLOCK
 #define VINP_PROP_BLOCK 128  // smaller blocks shorten the tail of every pass (measured: -2% per step vs 256)
 #endif
-#ifndef VINP_KB_BLOCK
-#define VINP_KB_BLOCK 64  // onion (K-restricted) passes: small layers, spread over more SMs
-#endif
 #ifndef VINP_MINB
 #define VINP_MINB 3
 #endif
@@ -115,11 +112,7 @@ __global__ void k_upsample(LevelArgs c, const uint64_t* __restrict__ ce, LevelAr
     accc = __dp4a(dc, dc, accc);                                              \
     acct = __dp4a(dx_, dx_, acct);                                            \
   }
-// KB = true (the K-restricted onion evaluate; onion propagation / random search run the
-// warp-per-target kernels below): the non-interior path issues all
-// gathers of a frame together (in-Omega predicates, then the layer bytes of K, then the predicated
-// voxel loads) instead of one branch-guarded voxel at a time.
-template <bool ABORT, bool KB = false>
+template <bool ABORT>
 __device__ __forceinline__ uint32_t thread_ssd(const LevelArgs& a, int p, int px, int py, int pt,
                                                int q, int lambda, int kb, bool full, uint32_t thr,
                                                bool& alive) {
@@ -145,7 +138,7 @@ __device__ __forceinline__ uint32_t thread_ssd(const LevelArgs& a, int p, int px
         accc = __dp4a(dc, dc, accc);
         acct = __dp4a(dx_, dx_, acct);
       }
-    } else if (!KB) {  // border target: one branch-guarded voxel at a time (rare)
+    } else {  // border target: one branch-guarded voxel at a time (rare)
 #pragma unroll
       for (int dy = -2; dy <= 2; ++dy) {
         int ro = dt * a.g.HW + dy * a.g.W;
@@ -160,30 +153,6 @@ __device__ __forceinline__ uint32_t thread_ssd(const LevelArgs& a, int p, int px
         }
       }
     }
-    if (KB && !full) {
-      bool ok[25];
-      const bool tin = (unsigned)(pt + dt) < (unsigned)a.g.T;
-#pragma unroll
-      for (int k = 0; k < 25; ++k)
-        ok[k] = tin && (unsigned)(py + k / 5 - 2) < (unsigned)a.g.H && (unsigned)(px + k % 5 - 2) < (unsigned)a.g.W;
-      if (kb >= 0) {
-        uint8_t lay[25];
-#pragma unroll
-        for (int k = 0; k < 25; ++k)
-          lay[k] = ok[k] ? a.layer[p + dt * a.g.HW + (k / 5 - 2) * a.g.W + (k % 5 - 2)] : (uint8_t)255;
-#pragma unroll
-        for (int k = 0; k < 25; ++k) ok[k] = ok[k] && (int)lay[k] < kb;
-      }
-      uint64_t tv[25], sv[25];
-#pragma unroll
-      for (int k = 0; k < 25; ++k) {
-        int off = dt * a.g.HW + (k / 5 - 2) * a.g.W + (k % 5 - 2);
-        tv[k] = ok[k] ? __ldg(v + (p + off)) : 0ull;
-        sv[k] = ok[k] ? __ldg(v + (q + off)) : 0ull;
-      }
-#pragma unroll
-      for (int k = 0; k < 25; ++k) VINP_ACC(tv[k], sv[k])
-    }
     if (ABORT) {
       uint32_t part = 4u * accc + (uint32_t)lambda * acct;
       if (part >= thr) alive = false;
@@ -195,7 +164,6 @@ __device__ __forceinline__ uint32_t thread_ssd(const LevelArgs& a, int p, int px
 }
 
 // ------------------------------------------------------------------ a5: evaluate
-template <bool KB>
 __global__ void __launch_bounds__(256) k_evaluate(LevelArgs a, uint64_t* __restrict__ ee,
                                                   uint8_t* __restrict__ en, int lambda, int kb,
                                                   int only_layer, int32_t b, int32_t e,
@@ -213,7 +181,7 @@ __global__ void __launch_bounds__(256) k_evaluate(LevelArgs a, uint64_t* __restr
     int q = e_q(ee[s]);
     bool full = kb < 0 && px >= 2 && px < a.g.W - 2 && py >= 2 && py < a.g.H - 2 && pt >= 2 && pt < a.g.T - 2;
     bool alive = true;
-    uint32_t D = thread_ssd<false, KB>(a, p, px, py, pt, q, lambda, kb, full, 0, alive);
+    uint32_t D = thread_ssd<false>(a, p, px, py, pt, q, lambda, kb, full, 0, alive);
     int n = 0;
     if (full) {
       n = 125;
@@ -453,6 +421,34 @@ __global__ void __launch_bounds__(VINP_WIDE_BLOCK) k_propagate_wide(
   if (lane == 0) {
     eout[s] = pack_e(bestD, bestq);
     flush_count(counter, cnt);
+  }
+}
+
+// Onion (K-restricted) evaluate, warp per target: D(p, phi(p)) over the voxels of N_p in Omega
+// and K (Alg. 3: only known voxels count) and their number n.
+__global__ void __launch_bounds__(VINP_WIDE_BLOCK) k_evaluate_wide(LevelArgs a, uint64_t* __restrict__ ee,
+                                                                   uint8_t* __restrict__ en, int lambda,
+                                                                   int kb, int only_layer, int32_t b,
+                                                                   int32_t e, const int32_t* __restrict__ list,
+                                                                   unsigned long long* counter) {
+  const int lane = threadIdx.x & 31;
+  const int idx = b + (int)((blockIdx.x * (unsigned)blockDim.x + threadIdx.x) >> 5);
+  if (idx >= e) return;  // warp-uniform
+  const int s = list ? __ldg(list + idx) : idx;
+  const int p = __ldg(a.targets + s);
+  if (only_layer >= 0 && a.layer[p] != only_layer) return;
+  int px, py, pt;
+  decode(a.g, p, px, py, pt);
+  WideTarget w;
+  w.load(a, p, px, py, pt, lane);
+  const int q = e_q(ee[s]);
+  w.mask(kb);
+  const uint32_t D = __reduce_add_sync(kFull, w.part(reinterpret_cast<const unsigned long long*>(a.vox), q, lambda));
+  const uint32_t n = __reduce_add_sync(kFull, (uint32_t)(w.ok[0] + w.ok[1] + w.ok[2] + w.ok[3]));
+  if (lane == 0) {
+    ee[s] = pack_e(D, q);
+    en[s] = (uint8_t)n;
+    flush_count(counter, 1);
   }
 }
 
@@ -883,11 +879,11 @@ vinp_status launch_evaluate(const vinp_level* lv, vinp_nnf* nnf, const vinp_para
   VINP_REQUIRE(nnf && nnf->e && nnf->n, "vinp_nnf_evaluate: null nnf");
   VINP_REQUIRE((kb < 0 && only_layer < 0) || lv->layer, "vinp_nnf_evaluate: layer map required");
   if (e > b) {
-    if (kb >= 0)
-      k_evaluate<true><<<nblk(e - b, VINP_KB_BLOCK), VINP_KB_BLOCK, 0, S(stream)>>>(
+    if (kb >= 0)  // K-restricted (onion) launch: warp per target
+      k_evaluate_wide<<<nblk((int64_t)(e - b) * 32, VINP_WIDE_BLOCK), VINP_WIDE_BLOCK, 0, S(stream)>>>(
           args_of(lv), nnf->e, nnf->n, prm->lambda, kb, only_layer, b, e, list, counter);
     else
-      k_evaluate<false><<<nblk(e - b, VINP_EVAL_BLOCK), VINP_EVAL_BLOCK, 0, S(stream)>>>(
+      k_evaluate<<<nblk(e - b, VINP_EVAL_BLOCK), VINP_EVAL_BLOCK, 0, S(stream)>>>(
           args_of(lv), nnf->e, nnf->n, prm->lambda, kb, only_layer, b, e, list, counter);
     count_launch();
   }
