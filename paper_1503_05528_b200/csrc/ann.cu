@@ -293,14 +293,6 @@ __global__ void __launch_bounds__(256, VINP_PROP_MINB) k_propagate(LevelArgs a, 
   if ((threadIdx.x & 31) == 0) flush_count(counter, cnt);
 }
 
-// Onion (K-restricted) propagation pass, warp per target.  An onion layer holds a few hundred to
-// a few ten thousand targets, so the thread-per-target pass above runs as one latency chain per
-// lane (candidate generation, then per frame layer bytes -> predicated voxels, up to 15 frames):
-// ~40 us per launch whatever its size, x 880 launches per c5 step.  Here the 125 voxels of the
-// patch are spread over the warp (lane l owns k = l + 32 j), the (up to 6) candidates are
-// generated by lanes 0..nc-1 in parallel, and all candidate gathers are issued at once, so the
-// chain is ~8 round trips.  No early abort: a candidate is kept iff D < best in rank order (R25),
-// the same decision the aborting pass takes; counts one patch-update per evaluated candidate.
 // Warp-per-target patch (onion passes): lane l owns the voxels k = l + 32 j (j < 4, k < 125) of
 // N_p; a voxel outside Omega or K contributes nothing (its target word is zeroed and its source
 // gather skipped).  load() issues the gathers, mask() consumes the layer bytes.
@@ -343,6 +335,14 @@ struct WideTarget {
 #ifndef VINP_WIDE_BLOCK
 #define VINP_WIDE_BLOCK 64
 #endif
+// Onion (K-restricted) propagation pass, warp per target.  An onion layer holds a few hundred to
+// a few ten thousand targets, so a thread-per-target pass runs as one latency chain per lane
+// (candidate generation, then per frame layer bytes -> predicated voxels, up to 15 frames): it
+// measured ~40 us per launch whatever its size, x 880 launches per c5 step.  Here the 125 voxels of the
+// patch are spread over the warp (lane l owns k = l + 32 j), the (up to 6) candidates are
+// generated by lanes 0..nc-1 in parallel, and all candidate gathers are issued at once, so the
+// chain is ~8 round trips.  No early abort: a candidate is kept iff D < best in rank order (R25),
+// the same decision the aborting pass takes; counts one patch-update per evaluated candidate.
 __global__ void __launch_bounds__(VINP_WIDE_BLOCK) k_propagate_wide(
     LevelArgs a, const uint64_t* __restrict__ ein, uint64_t* __restrict__ eout, int lambda,
     int step, int sign, int kb, int only_layer, int32_t b, int32_t e,
