@@ -96,6 +96,9 @@ __global__ void k_upsample(LevelArgs c, const uint64_t* __restrict__ ce, LevelAr
 #ifndef VINP_PROP_MINB
 #define VINP_PROP_MINB 4
 #endif
+#ifndef VINP_RS_SMALL
+#define VINP_RS_SMALL (148 * 32 * 8)  // random-search launches below this many targets: 8 per warp
+#endif
 
 // ------------------------------------------------------------------ thread-per-target SSD
 // Used where candidates are spatially coherent (evaluate, propagation): lane l of a warp owns
@@ -949,7 +952,7 @@ vinp_status launch_random_search(const vinp_level* lv, const vinp_nnf* in, vinp_
   } else if (e > b) {
     cudaStream_t cs = S(stream);
     LevelArgs la = args_of(lv);
-    const bool small = (e - b) < 148 * 32 * 8;
+    const bool small = (e - b) < VINP_RS_SMALL;
 #define VINP_RS2(NC, WPB, TPW)                                                                       \
   k_random_search<NC, WPB, TPW><<<nblk(e - b, TPW * WPB), 32 * WPB, 0, cs>>>(                           \
       la, in->e, out->e, prm->lambda, r, prm->seed, outer_code, pm_iter, only_layer, b, e, list, counter)
