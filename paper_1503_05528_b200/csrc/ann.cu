@@ -90,6 +90,12 @@ __global__ void k_upsample(LevelArgs c, const uint64_t* __restrict__ ce, LevelAr
 #ifndef VINP_PROP_BLOCK
 #define VINP_PROP_BLOCK 128  // smaller blocks shorten the tail of every pass (measured: -2% per step vs 256)
 #endif
+#ifndef VINP_PROP_BLOCK_MID
+#define VINP_PROP_BLOCK_MID 64  // launches below VINP_PROP_BIG targets (levels >= 2 of c5): -3 ms per step
+#endif
+#ifndef VINP_PROP_BIG
+#define VINP_PROP_BIG (1 << 23)
+#endif
 #ifndef VINP_MINB
 #define VINP_MINB 3
 #endif
@@ -902,11 +908,12 @@ vinp_status launch_propagate(const vinp_level* lv, const vinp_nnf* in, vinp_nnf*
   VINP_REQUIRE(step >= 1 && sign >= -1 && sign <= 1, "vinp_propagate: bad step/sign");
   VINP_REQUIRE((kb < 0 && only_layer < 0) || lv->layer, "vinp_propagate: layer map required");
   if (e > b) {
+    const int pb = e - b >= VINP_PROP_BIG ? VINP_PROP_BLOCK : VINP_PROP_BLOCK_MID;
     if (kb >= 0)  // K-restricted (onion) launch: warp per target
       k_propagate_wide<<<nblk((int64_t)(e - b) * 32, VINP_WIDE_BLOCK), VINP_WIDE_BLOCK, 0, S(stream)>>>(
           args_of(lv), in->e, out->e, prm->lambda, step, sign, kb, only_layer, b, e, list, counter);
     else
-      k_propagate<<<nblk(e - b, VINP_PROP_BLOCK), VINP_PROP_BLOCK, 0, S(stream)>>>(
+      k_propagate<<<nblk(e - b, pb), pb, 0, S(stream)>>>(
           args_of(lv), in->e, out->e, prm->lambda, step, sign, kb, only_layer, b, e, list, counter);
     count_launch();
   }
