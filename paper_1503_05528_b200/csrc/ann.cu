@@ -82,7 +82,7 @@ __global__ void k_upsample(LevelArgs c, const uint64_t* __restrict__ ce, LevelAr
 }
 
 #ifndef VINP_EVAL_BLOCK
-#define VINP_EVAL_BLOCK 256
+#define VINP_EVAL_BLOCK 64  // shorter tails (measured: level-1 evaluate 13.5 -> 12.3 ms per step vs 256)
 #endif
 #ifndef VINP_RS_WPB
 #define VINP_RS_WPB 2  // warps per block for <= 12 candidates (measured: 8 -> 2 saves 3% per step)
