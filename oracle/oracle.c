@@ -582,6 +582,27 @@ int64_t or_change_l1(const float* a, const float* b, int64_t n) {
   return s;
 }
 
+/* The literal P:988 statistic ||u_H - v_H||_2 (stop_rule 1): sum of llrint((a-b)^2 * 2^20); the
+ * difference of two floats is exact in fp64 and so is its square (2 x 24 significant bits). */
+int64_t or_change_l2(const float* a, const float* b, int64_t n) {
+  int64_t s = 0;
+  for (int64_t i = 0; i < n; ++i) {
+    double d = (double)a[i] - (double)b[i];
+    s += llrint(d * d * 1048576.0);
+  }
+  return s;
+}
+
+/* Alg. 4 P:979-988 loop condition "while e > 0.1 and k < k_max" (threshold 0.1,
+ * at most 20 iterations; R19 for the norm).  e_fixed is the statistic scaled by 2^20. */
+int or_stop(int64_t e_fixed, int64_t n_holes, int k, int max_outer, int stop_rule) {
+  if (k >= max_outer) return 1;
+  if (stop_rule == 0) /* e_fixed / 2^20 / (3|H|) <= 0.1  <=>  10 e_fixed <= 3|H| 2^20 */
+    return 10 * (__int128)e_fixed <= 3 * (__int128)n_holes * 1048576;
+  /* sqrt(e_fixed / 2^20) / (3|H|) <= 0.1  <=>  100 e_fixed <= 9 |H|^2 2^20 */
+  return 100 * (__int128)e_fixed <= 9 * (__int128)n_holes * n_holes * 1048576;
+}
+
 /* Eq. 1 P:286-289 (diagnostic): E = sum_{p in H} d^2(W_p, W_{p+phi(p)}) = sum D/(4n). */
 double or_energy(const or_level* lv, const or_nnf* nnf) {
   double E = 0.0;
@@ -752,7 +773,10 @@ int or_inpaint(const uint8_t* rgb, const uint8_t* occ, int W, int H, int T, cons
         or_reconstruct(lv, &c->a, OR_WEIGHTED, j, 0, lv->n_holes, c->cur_rgb, c->cur_tex);
         /* commit only layer j (the others are untouched in cur) */
         for (int32_t hh = 0; hh < lv->n_holes; ++hh)
-          if (lv->layer[lv->holes[hh]] == j) or_commit(lv, c->cur_rgb, c->cur_tex, hh, hh + 1);
+          if (lv->layer[lv->holes[hh]] == j) {
+            or_commit(lv, c->cur_rgb, c->cur_tex, hh, hh + 1);
+            st->onion_commits += 1;
+          }
       }
     }
   }
@@ -761,19 +785,21 @@ int or_inpaint(const uint8_t* rgb, const uint8_t* occ, int W, int H, int T, cons
     or_work* c = &w[l];
     or_level* lv = &c->lv;
     int k = 0;
+    st->n_holes[l - 1] = lv->n_holes;
     for (;;) {
       memcpy(c->prev_rgb, c->cur_rgb, 12 * (size_t)lv->n_holes);
       memcpy(c->prev_tex, c->cur_tex, 8 * (size_t)lv->n_holes);
       st->patch_updates[l - 1] += ann_search(c, prm, l, (uint32_t)k, -1, -1);
       or_reconstruct(lv, &c->a, OR_WEIGHTED, -1, 0, lv->n_holes, c->cur_rgb, c->cur_tex);
       or_commit(lv, c->cur_rgb, c->cur_tex, 0, lv->n_holes);
-      int64_t e = or_change_l1(c->cur_rgb, c->prev_rgb, 3 * (int64_t)lv->n_holes);
+      int64_t e = prm->stop_rule == 1 ? or_change_l2(c->cur_rgb, c->prev_rgb, 3 * (int64_t)lv->n_holes)
+                                       : or_change_l1(c->cur_rgb, c->prev_rgb, 3 * (int64_t)lv->n_holes);
+      if (k < 32) st->change_fixed[l - 1][k] = e;
       ++k;
       if (prm->fixed_outer > 0) {
         if (k >= prm->fixed_outer) break;
-      } else {
-        /* e = e_fixed / 2^20 / (3|H|) <= 0.1  <=>  10 e_fixed <= 3|H| 2^20 */
-        if (10 * e <= 3 * (int64_t)lv->n_holes * 1048576 || k >= prm->max_outer) break;
+      } else if (or_stop(e, lv->n_holes, k, prm->max_outer, prm->stop_rule)) {
+        break;
       }
     }
     st->outer_iters[l - 1] = k;

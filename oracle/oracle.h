@@ -78,6 +78,8 @@ void or_reconstruct(or_level* lv, const or_nnf* nnf, int mode, int layer_j, int3
                     float* out_rgb, float* out_tex);
 void or_commit(or_level* lv, const float* out_rgb, const float* out_tex, int32_t hb, int32_t he);
 int64_t or_change_l1(const float* a, const float* b, int64_t n);
+/* literal P:988 variant: sum over hole channels of llrint((a-b)^2 2^20) ((a-b)^2 is exact in fp64) */
+int64_t or_change_l2(const float* a, const float* b, int64_t n);
 double or_energy(const or_level* lv, const or_nnf* nnf);
 int64_t or_brute_force(const or_level* lv, or_nnf* out, int lambda, int32_t b, int32_t e);
 
@@ -134,12 +136,24 @@ typedef struct {
   int steps[8];
   uint64_t seed;
   double rho;
+  int stop_rule; /* 0: R19 e = ||u_H - v_H||_1 / (3|H|); 1: literal P:988 ||u_H - v_H||_2 / (3|H|) */
 } or_params;
 typedef struct {
   int outer_iters[16];
   int64_t patch_updates[16];
   int onion_layers;
+  /* diagnostics for the pins: the change statistic of every outer iteration (fixed point 2^20,
+   * or_change_l1 / or_change_l2 by stop_rule; first 32 iterations), |H| per level, and how many
+   * hole voxels the onion peel committed (each exactly once) */
+  int64_t change_fixed[16][32];
+  int64_t n_holes[16];
+  int64_t onion_commits;
 } or_stats;
+/* R19 / P:930-939 stopping decision after outer iteration k (1-based) of a level with n_holes
+ * hole voxels: 1 = stop.  stop_rule 0: e_fixed = sum llrint(|a-b| 2^20), stop iff
+ * e_fixed / 2^20 / (3 n_holes) <= 0.1; stop_rule 1: e_fixed = sum llrint((a-b)^2 2^20), stop iff
+ * sqrt(e_fixed / 2^20) / (3 n_holes) <= 0.1.  Always stop at k >= max_outer. */
+int or_stop(int64_t e_fixed, int64_t n_holes, int k, int max_outer, int stop_rule);
 int or_inpaint(const uint8_t* rgb, const uint8_t* occ, int W, int H, int T, const or_params* prm,
                uint8_t* out_rgb, or_stats* st);
 

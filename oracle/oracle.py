@@ -16,13 +16,18 @@ import numpy as np
 _HERE = os.path.dirname(os.path.abspath(__file__))
 _LIB_PATH = os.path.join(_HERE, "liboracle.so")
 _lib = None
+# tools/mutation_check.py: build a mutated copy of oracle.c (in a temp dir) instead of this one
+_SRC_OVERRIDE = os.environ.get("VINP_ORACLE_SRC")
+if _SRC_OVERRIDE:
+    _LIB_PATH = os.path.join(os.path.dirname(_SRC_OVERRIDE), "liboracle_mut.so")
 
 
 def build(force: bool = False) -> str:
-    src = os.path.join(_HERE, "oracle.c")
+    src = _SRC_OVERRIDE or os.path.join(_HERE, "oracle.c")
     if force or not os.path.exists(_LIB_PATH) or os.path.getmtime(_LIB_PATH) < max(
             os.path.getmtime(src), os.path.getmtime(os.path.join(_HERE, "oracle.h"))):
-        cmd = f"gcc -O2 -std=c11 -ffp-contract=off -fopenmp -fPIC -shared -o {_LIB_PATH} {src} -lm"
+        cmd = (f"gcc -O2 -std=c11 -ffp-contract=off -fopenmp -fPIC -shared -I {_HERE} -o {_LIB_PATH} "
+               f"{src} -lm")
         if os.system(cmd) != 0:
             raise RuntimeError("oracle build failed: " + cmd)
     return _LIB_PATH
@@ -47,12 +52,13 @@ class OrParams(C.Structure):
     _fields_ = [("levels", C.c_int), ("pm_iters", C.c_int), ("fixed_outer", C.c_int),
                 ("max_outer", C.c_int), ("lambda_", C.c_int), ("tex_half", C.c_int),
                 ("n_steps", C.c_int), ("sign_policy", C.c_int), ("steps", C.c_int * 8), ("seed", C.c_uint64),
-                ("rho", C.c_double)]
+                ("rho", C.c_double), ("stop_rule", C.c_int)]
 
 
 class OrStats(C.Structure):
     _fields_ = [("outer_iters", C.c_int * 16), ("patch_updates", C.c_int64 * 16),
-                ("onion_layers", C.c_int)]
+                ("onion_layers", C.c_int), ("change_fixed", (C.c_int64 * 32) * 16),
+                ("n_holes", C.c_int64 * 16), ("onion_commits", C.c_int64)]
 
 
 def lib():
@@ -77,6 +83,8 @@ def lib():
             "or_reconstruct": (None, [P, P, I, I, I32, I32, P, P]),
             "or_commit": (None, [P, P, P, I32, I32]),
             "or_change_l1": (I64, [P, P, I64]),
+            "or_change_l2": (I64, [P, P, I64]),
+            "or_stop": (I, [I64, I64, I, I, I]),
             "or_energy": (D, [P, P]),
             "or_brute_force": (I64, [P, P, I, I32, I32]),
             "or_inpaint": (I, [P, P, I, I, I, P, P, P]),
@@ -263,6 +271,16 @@ def change_l1(a, b):
     return lib().or_change_l1(_p(a), _p(b), a.size)
 
 
+def change_l2(a, b):
+    a = np.ascontiguousarray(a, np.float32).ravel()
+    b = np.ascontiguousarray(b, np.float32).ravel()
+    return lib().or_change_l2(_p(a), _p(b), a.size)
+
+
+def stop(e_fixed, n_holes, k, max_outer=20, stop_rule=0):
+    return bool(lib().or_stop(int(e_fixed), int(n_holes), int(k), int(max_outer), int(stop_rule)))
+
+
 def energy(lv, nnf):
     return lib().or_energy(lv.struct(), nnf.struct())
 
@@ -291,14 +309,14 @@ def ann_search(lv, a: NNF, lam, seed, level, outer_code, pm_iters, steps=(8, 4, 
 
 
 def inpaint(rgb, occ, levels, pm_iters=10, fixed_outer=0, max_outer=20, lam=50, seed=1,
-            steps=(8, 4, 2, 1), rho=0.5, tex_half=-1, sign_policy=0):
+            steps=(8, 4, 2, 1), rho=0.5, tex_half=-1, sign_policy=0, stop_rule=0):
     T, H, W, _ = rgb.shape
     prm = OrParams()
     prm.levels, prm.pm_iters, prm.fixed_outer, prm.max_outer = levels, pm_iters, fixed_outer, max_outer
     prm.lambda_, prm.tex_half, prm.n_steps, prm.sign_policy = lam, tex_half, len(steps), sign_policy
     for i, s in enumerate(steps):
         prm.steps[i] = s
-    prm.seed, prm.rho = seed, rho
+    prm.seed, prm.rho, prm.stop_rule = seed, rho, stop_rule
     st = OrStats()
     out = np.zeros_like(rgb)
     rgb, occ = np.ascontiguousarray(rgb), np.ascontiguousarray(occ)
@@ -307,7 +325,9 @@ def inpaint(rgb, occ, levels, pm_iters=10, fixed_outer=0, max_outer=20, lam=50, 
     if rc != 0:
         raise RuntimeError(f"or_inpaint failed: {rc}")
     return out, dict(outer_iters=list(st.outer_iters)[:levels],
-                     patch_updates=list(st.patch_updates)[:levels], onion_layers=st.onion_layers)
+                     patch_updates=list(st.patch_updates)[:levels], onion_layers=st.onion_layers,
+                     change_fixed=[list(st.change_fixed[l])[:min(st.outer_iters[l], 32)] for l in range(levels)],
+                     n_holes=list(st.n_holes)[:levels], onion_commits=st.onion_commits)
 
 
 def ambiguity_exact(N):
