@@ -199,16 +199,25 @@ vinp_status vinp_onion_peel(vinp_level* lv, vinp_nnf* a, vinp_nnf* b, const vinp
 /* ---- a11: stopping-rule change (Alg. 4, R19): *out (device int64) += sum_i
  * llrint(|a_i - b_i| 2^20).  e = out / 2^20 / (3|H|). */
 vinp_status vinp_change_l1(const float* a, const float* b, int64_t n, int64_t* out, void* stream);
+/* The literal P:988 statistic (Config stop_rule = 1): *out += sum_i llrint((a_i - b_i)^2 2^20) (the
+ * square of a float difference is exact in fp64); e = sqrt(out / 2^20) / (3|H|).  Same buffers and
+ * errors as vinp_change_l1. */
+vinp_status vinp_change_l2(const float* a, const float* b, int64_t n, int64_t* out, void* stream);
 
 /* ---- Eq. 1 P:286-289 (diagnostic): *out (device double) = sum_{p in H} D_p / (4 n_p). */
 vinp_status vinp_energy(const vinp_level* lv, const vinp_nnf* nnf, double* out, void* stream);
 
 /* ---- a13: exact NN (definition of Matching): argmin over q in D~ of D(p, q), K = Omega,
- * ties -> smallest q; target slots [b, e).  ws: vinp_brute_force_ws_bytes. */
+ * ties -> smallest q; target slots [b, e).  The CUDA-core form needs no workspace:
+ * vinp_brute_force_ws_bytes returns 0 and ws may be NULL.  Errors: VINP_E_INVALID (null buffers,
+ * bad range), VINP_E_UNSUPPORTED (lambda outside [0,126]), VINP_E_NO_SOURCE (D~ empty), all
+ * synchronous. */
 size_t vinp_brute_force_ws_bytes(const vinp_level* lv);
 vinp_status vinp_brute_force(const vinp_level* lv, vinp_nnf* out, const vinp_params* prm, int32_t b,
                              int32_t e, void* ws, size_t ws_bytes, void* stream);
-/* The same exact NN over an explicit list of target slots (CUDA cores). */
+/* The same exact NN over an explicit device list of n target slots (CUDA cores); every list entry
+ * must lie in [0, n_targets).  Same synchronous argument errors as vinp_brute_force (the list's
+ * contents live on the device and are not inspected). */
 vinp_status vinp_brute_force_list(const vinp_level* lv, vinp_nnf* out, const vinp_params* prm,
                                   const int32_t* list, int32_t n, void* stream);
 /* Tensor-core form (north_star: "optional exact brute-force NN mode expressed as a dense

@@ -102,6 +102,9 @@ __global__ void k_upsample(LevelArgs c, const uint64_t* __restrict__ ce, LevelAr
 #ifndef VINP_PROP_MINB
 #define VINP_PROP_MINB 4
 #endif
+#ifndef VINP_PROP_FRAME_MAJOR
+#define VINP_PROP_FRAME_MAJOR 1
+#endif
 #ifndef VINP_RS_SMALL
 #define VINP_RS_SMALL (148 * 32 * 8)  // random-search launches below this many targets: 8 per warp
 #endif
@@ -282,6 +285,65 @@ __global__ void __launch_bounds__(256, VINP_PROP_MINB) k_propagate(LevelArgs a, 
   bool full = act && kb < 0 && px >= 2 && px < a.g.W - 2 && py >= 2 && py < a.g.H - 2 && pt >= 2 &&
               pt < a.g.T - 2;
   bool allfull = __all_sync(kFull, full || !act);
+#if VINP_PROP_FRAME_MAJOR
+  if (allfull) {
+    // Row-major over the patch, all of this lane's candidates per target row: each target row (5
+    // coalesced 8-byte gathers) is loaded once and compared with the same row of every live
+    // candidate, instead of once per candidate.  A candidate is dropped after a frame once its
+    // partial sum reaches the incumbent's D (it can then never be accepted: exact, R35); the
+    // survivors are applied in rank order with strict improvement (R25).
+    const unsigned long long* v = reinterpret_cast<const unsigned long long*>(a.vox);
+    uint32_t accc[NCMAX], acct[NCMAX];
+    unsigned alive = 0;
+#pragma unroll
+    for (int c = 0; c < NCMAX; ++c) {
+      accc[c] = acct[c] = 0;
+      if (c < ncand) alive |= 1u << c;
+    }
+    cnt = ncand;
+    const uint32_t thr = bestD;
+#pragma unroll 1
+    for (int dt = -2; dt <= 2; ++dt) {
+      if (!__any_sync(kFull, alive != 0)) break;
+#pragma unroll
+      for (int dy = -2; dy <= 2; ++dy) {
+        const int ro = dt * a.g.HW + dy * a.g.W;
+        uint64_t tv[5];
+#pragma unroll
+        for (int dx = -2; dx <= 2; ++dx) tv[dx + 2] = alive ? __ldg(v + (p + ro + dx)) : 0ull;
+#pragma unroll
+        for (int c = 0; c < NCMAX; ++c) {
+          if (!((alive >> c) & 1)) continue;
+          uint64_t sv[5];
+#pragma unroll
+          for (int dx = -2; dx <= 2; ++dx) sv[dx + 2] = __ldg(v + (cq[c] + ro + dx));
+#pragma unroll
+          for (int k = 0; k < 5; ++k) {
+            uint32_t dc = __vabsdiffu4((uint32_t)tv[k], (uint32_t)sv[k]);
+            uint32_t dx_ = __vabsdiffu4((uint32_t)(tv[k] >> 32), (uint32_t)(sv[k] >> 32));
+            accc[c] = __dp4a(dc, dc, accc[c]);
+            acct[c] = __dp4a(dx_, dx_, acct[c]);
+          }
+        }
+      }
+#pragma unroll
+      for (int c = 0; c < NCMAX; ++c)
+        if (4u * accc[c] + (uint32_t)lambda * acct[c] >= thr) alive &= ~(1u << c);
+    }
+#pragma unroll
+    for (int c = 0; c < NCMAX; ++c) {
+      const uint32_t D = 4u * accc[c] + (uint32_t)lambda * acct[c];
+      if (((alive >> c) & 1) && D < bestD) {
+        bestD = D;
+        bestq = cq[c];
+      }
+    }
+    if (have) eout[s] = pack_e(bestD, bestq);
+    cnt = __reduce_add_sync(kFull, cnt);
+    if ((threadIdx.x & 31) == 0) flush_count(counter, cnt);
+    return;
+  }
+#endif
 #pragma unroll
   for (int c = 0; c < NCMAX; ++c) {
     bool mine = c < ncand;
@@ -823,7 +885,9 @@ static Radii make_radii(const vinp_level* lv, const vinp_params* prm) {
   int rmax = prm->rmax > 0 ? prm->rmax : std::max(lv->W, std::max(lv->H, lv->T));
   double R = (double)rmax;
   r.M = 0;
-  for (int i = 1; i <= 32; ++i) {
+  // the kernels hold at most 32 radii (one per lane in the warp-per-target form); a 33rd radius
+  // R_33 >= 1 is refused rather than dropped (the oracle would evaluate it)
+  for (int i = 1; i <= 33; ++i) {
     R = R * prm->rho;
     if (!(R >= 1.0)) break;
     if (r.M == 32) { r.M = -1; break; }
@@ -948,10 +1012,10 @@ vinp_status launch_random_search(const vinp_level* lv, const vinp_nnf* in, vinp_
   VINP_REQUIRE((kb < 0 && only_layer < 0) || lv->layer, "vinp_random_search: layer map required");
   Radii r = make_radii(lv, prm);
   if (r.M < 0) {
-    set_error("vinp_random_search: more than 31 random-search radii (rho too close to 1)");
+    set_error("vinp_random_search: more than 32 random-search radii R_i = rmax rho^i >= 1 (rho too close to 1)");
     return VINP_E_UNSUPPORTED;
   }
-  if (e > b && kb >= 0) {  // K-restricted (onion) launch: warp per target (M <= 31 < 32 lanes)
+  if (e > b && kb >= 0) {  // K-restricted (onion) launch: warp per target (M <= 32 lanes)
     k_random_search_wide<<<nblk((int64_t)(e - b) * 32, VINP_WIDE_BLOCK), VINP_WIDE_BLOCK, 0, S(stream)>>>(
         args_of(lv), in->e, out->e, prm->lambda, r, prm->seed, outer_code, pm_iter, kb, only_layer, b, e,
         list, counter);
@@ -1026,7 +1090,10 @@ vinp_status vinp_ann_search(const vinp_level* lv, vinp_nnf* a, vinp_nnf* b, cons
   return VINP_OK;
 }
 
-size_t vinp_brute_force_ws_bytes(const vinp_level* lv) { return lv ? 256 : 0; }
+size_t vinp_brute_force_ws_bytes(const vinp_level* lv) {
+  (void)lv;
+  return 0;  // the CUDA-core form needs no workspace
+}
 
 vinp_status vinp_brute_force(const vinp_level* lv, vinp_nnf* out, const vinp_params* prm, int32_t b,
                              int32_t e, void* ws, size_t ws_bytes, void* stream) {
@@ -1049,6 +1116,15 @@ vinp_status vinp_brute_force(const vinp_level* lv, vinp_nnf* out, const vinp_par
 
 vinp_status vinp_brute_force_list(const vinp_level* lv, vinp_nnf* out, const vinp_params* prm,
                                   const int32_t* list, int32_t n, void* stream) {
+  vinp_status st = check_nnf_args(lv, "vinp_brute_force_list", 0, 0, prm);
+  if (st) return st;
+  VINP_REQUIRE(out && out->e && out->n, "vinp_brute_force_list: null nnf");
+  VINP_REQUIRE(n >= 0 && (n == 0 || list), "vinp_brute_force_list: null list or negative count");
+  VINP_REQUIRE(n <= lv->n_targets, "vinp_brute_force_list: more list entries than targets");
+  if (lv->n_sources <= 0) {
+    set_error("vinp_brute_force_list: D~ is empty");
+    return VINP_E_NO_SOURCE;
+  }
   if (n > 0) {
     k_brute_force<<<n, 32 * kWarpsPerBlock, 0, S(stream)>>>(args_of(lv), out->e, out->n, prm->lambda, 0,
                                                              n, list);

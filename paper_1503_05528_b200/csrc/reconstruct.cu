@@ -301,12 +301,17 @@ __global__ void k_commit(Geo g, uint64_t* __restrict__ vox, const uint8_t* __res
   vox[p] = w;
 }
 
-__global__ void k_change_l1(const float* __restrict__ a, const float* __restrict__ b, int64_t n,
-                            unsigned long long* __restrict__ out) {
+// L2 = false: sum llrint(|a-b| 2^20) (R19); L2 = true: sum llrint((a-b)^2 2^20), the literal
+// P:988 norm (the difference of two floats and its square are exact in fp64)
+template <bool L2>
+__global__ void k_change(const float* __restrict__ a, const float* __restrict__ b, int64_t n,
+                         unsigned long long* __restrict__ out) {
   int64_t acc = 0;
   for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n;
-       i += (int64_t)gridDim.x * blockDim.x)
-    acc += __double2ll_rn(fabs((double)a[i] - (double)b[i]) * 1048576.0);
+       i += (int64_t)gridDim.x * blockDim.x) {
+    double d = (double)a[i] - (double)b[i];
+    acc += __double2ll_rn((L2 ? __dmul_rn(d, d) : fabs(d)) * 1048576.0);
+  }
   acc = warp_sum64(acc);
   __shared__ long long sm[32];
   int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
@@ -394,10 +399,20 @@ vinp_status vinp_change_l1(const float* a, const float* b, int64_t n, int64_t* o
   VINP_REQUIRE(out && n >= 0 && (n == 0 || (a && b)), "vinp_change_l1: bad args");
   if (n > 0) {
     int g = (int)std::min<int64_t>(nblk(n, 256), 148 * 8);
-    k_change_l1<<<g, 256, 0, S(stream)>>>(a, b, n, (unsigned long long*)out);
+    k_change<false><<<g, 256, 0, S(stream)>>>(a, b, n, (unsigned long long*)out);
     count_launch();
   }
   return check_launch("vinp_change_l1");
+}
+
+vinp_status vinp_change_l2(const float* a, const float* b, int64_t n, int64_t* out, void* stream) {
+  VINP_REQUIRE(out && n >= 0 && (n == 0 || (a && b)), "vinp_change_l2: bad args");
+  if (n > 0) {
+    int g = (int)std::min<int64_t>(nblk(n, 256), 148 * 8);
+    k_change<true><<<g, 256, 0, S(stream)>>>(a, b, n, (unsigned long long*)out);
+    count_launch();
+  }
+  return check_launch("vinp_change_l2");
 }
 
 vinp_status vinp_energy(const vinp_level* lv, const vinp_nnf* nnf, double* out, void* stream) {

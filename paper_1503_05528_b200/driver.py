@@ -42,9 +42,21 @@ class Config:
     align_iters: int = 20       # R38: IRLS iterations per level
     align_tol: float = 1e-4     # R38: update-norm stop
     exchange: str = "allgather"  # multi-GPU: "allgather" every pass, or "halo" (NEXT #4, P2P)
+    stop_rule: int = 0          # 0: R19 e = ||u_H - v_H||_1 / (3|H|); 1: literal P:988 ||.||_2 / (3|H|)
 
     def params(self) -> V.Params:
         return V.Params(lam=self.lam, tex_half=self.tex_half, seed=self.seed, rho=self.rho)
+
+
+def stop_now(e_fixed: int, n_holes: int, k: int, max_outer: int, stop_rule: int = 0) -> bool:
+    """Alg. 4 P:979-988 loop exit after outer iteration k (e <= 0.1, at most 20
+    iterations).  e_fixed = the change statistic x 2^20 (exact integer, python ints: no overflow).
+    stop_rule 0 (R19): e = e_fixed / 2^20 / (3|H|); 1 (literal P:988): e = sqrt(e_fixed / 2^20) / (3|H|)."""
+    if k >= max_outer:
+        return True
+    if stop_rule == 0:
+        return 10 * e_fixed <= 3 * n_holes * (1 << 20)
+    return 100 * e_fixed <= 9 * n_holes * n_holes * (1 << 20)
 
 
 class Exchange:
@@ -328,6 +340,7 @@ class Inpainter:
             st = self.states[l - 1]
             lv = st.lv
             k = 0
+            changes = []
             while True:
                 st.prev_rgb.copy_(st.cur_rgb)
                 st.prev_tex.copy_(st.cur_tex)
@@ -335,16 +348,20 @@ class Inpainter:
                 self.reconstruct(st, V.WEIGHTED)
                 self.change.zero_()
                 hb, he = self.ex.slab(lv.n_holes)
-                self.V.change_l1(st.cur_rgb[hb:he], st.prev_rgb[hb:he], self.change)
+                chg = self.V.change_l2 if cfg.stop_rule == 1 else self.V.change_l1
+                chg(st.cur_rgb[hb:he], st.prev_rgb[hb:he], self.change)
                 self.ex.allreduce_sum(self.change)
                 k += 1
                 if cfg.fixed_outer > 0:
+                    changes.append(self.change.clone())  # read once at the end (no sync here)
                     if k >= cfg.fixed_outer:
                         break
                 else:
                     e_fixed = int(self.change.item())  # the one host sync per outer iteration
-                    if 10 * e_fixed <= 3 * lv.n_holes * (1 << 20) or k >= cfg.max_outer:
+                    changes.append(e_fixed)
+                    if stop_now(e_fixed, lv.n_holes, k, cfg.max_outer, cfg.stop_rule):
                         break
+            self.stats.levels[l - 1]["change_fixed"] = changes
             if l == 1:
                 self.reconstruct(st, V.BEST_PATCH, full=True)  # Eq. 6; every rank gets u
             else:
@@ -381,6 +398,8 @@ class Inpainter:
             per[0] -= onion_pu[0]
         self.ex.allreduce_sum(per)
         per = per.tolist()
+        for d in self.stats.levels:  # the stopping statistic of every outer iteration (x 2^20)
+            d["change_fixed"] = [int(c) for c in d.get("change_fixed", [])]
         for i, l in enumerate(range(L, 0, -1)):
             self.stats.levels[l - 1]["patch_updates"] = int(per[i])
         self.stats.total_patch_updates = int(sum(per))

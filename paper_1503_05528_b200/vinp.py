@@ -70,6 +70,7 @@ def _load():
         "vinp_reconstruct": (I, [P, P, I, I, I32, I32, P, P, I, P]),
         "vinp_commit": (I, [P, P, P, I, I32, I32, P]),
         "vinp_change_l1": (I, [P, P, I64, P, P]),
+        "vinp_change_l2": (I, [P, P, I64, P, P]),
         "vinp_energy": (I, [P, P, P, P]),
         "vinp_brute_force_ws_bytes": (C.c_size_t, [P]),
         "vinp_brute_force": (I, [P, P, P, I32, I32, P, C.c_size_t, P]),
@@ -102,7 +103,7 @@ EXPORTED = [
     "vinp_build_lists", "vinp_layers", "vinp_nnf_init_random", "vinp_nnf_upsample",
     "vinp_nnf_evaluate", "vinp_propagate", "vinp_random_search", "vinp_ann_search",
     "vinp_onion_ws_bytes", "vinp_onion_peel",
-    "vinp_reconstruct", "vinp_commit", "vinp_change_l1", "vinp_energy",
+    "vinp_reconstruct", "vinp_commit", "vinp_change_l1", "vinp_change_l2", "vinp_energy",
     "vinp_brute_force_ws_bytes", "vinp_brute_force", "vinp_patch_ssd", "vinp_philox",
     "vinp_tc_gemm_u8", "vinp_patch_ambiguity", "vinp_brute_force_list", "vinp_brute_force_tc_ws_bytes", "vinp_brute_force_tc",
     "vinp_affine_ws_bytes", "vinp_affine_estimate", "vinp_affine_chain", "vinp_align_warp", "vinp_unwarp",
@@ -336,6 +337,10 @@ def commit(lv, out_rgb, out_tex, layer_j=-1, hb=0, he=None):
 
 def change_l1(a, b, out):
     _check(_lib.vinp_change_l1(_ptr(a), _ptr(b), a.numel(), _ptr(out), _stream()), "vinp_change_l1")
+
+
+def change_l2(a, b, out):
+    _check(_lib.vinp_change_l2(_ptr(a), _ptr(b), a.numel(), _ptr(out), _stream()), "vinp_change_l2")
 
 
 def energy(lv, nnf, out):

@@ -247,6 +247,10 @@ def change_l1(a, b, out):
     out += int(orc.change_l1(a.numpy(), b.numpy()))
 
 
+def change_l2(a, b, out):
+    out += int(orc.change_l2(a.numpy(), b.numpy()))
+
+
 # ----------------------------------------------------------------------------- realignment (NEXT #1)
 def affine_ws_bytes(W, H, T, levels=3):
     return 1

@@ -61,3 +61,34 @@ def test_no_source_is_refused_by_the_tensor_core_mode():
     st = lib.vinp_brute_force_tc(lv.struct(), out.struct(), C.byref(V.Params().struct()), 0, 1, V._ptr(ws),
                                  ws.numel(), None)
     assert st in (1, 2)
+
+
+def test_brute_force_list_checks_arguments():
+    """vinp_brute_force_list: the same synchronous argument checks as vinp_brute_force."""
+    V, lib = _lib()
+    lv = V.Level.alloc(16, 12, 6, 1, torch.device("cuda"))
+    out = V.NNF.alloc(4, "cuda")
+    n0 = V.launch_count()
+    prm = V.Params()
+    assert lib.vinp_brute_force_list(lv.struct(), out.struct(), C.byref(prm.struct()), None, 3, None) == 1
+    assert lib.vinp_brute_force_list(None, out.struct(), C.byref(prm.struct()), None, 0, None) == 1
+    assert lib.vinp_brute_force_list(lv.struct(), out.struct(), C.byref(V.Params(lam=127).struct()), None, 0,
+                                     None) in (1, 4)
+    assert V.launch_count() == n0
+    assert V._lib.vinp_brute_force_ws_bytes(lv.struct()) == 0
+
+
+def test_too_many_random_search_radii_are_refused():
+    """rmax rho^33 >= 1 (e.g. rmax = 1920, rho = 0.8): refused (VINP_E_UNSUPPORTED), not truncated."""
+    V, lib = _lib()
+    from gen.synth import generate
+    from paper_1503_05528_b200 import Config, Inpainter
+    v, m, _ = generate("c1")
+    ip = Inpainter(64, 48, 20, Config(levels=1), "cuda")
+    ip.load(v.cuda(), m.cuda())
+    st = ip.states[0]
+    ok = V.Params(rho=0.8, rmax=1500)   # R_32 = 1.19, R_33 = 0.95: 32 radii, accepted
+    bad = V.Params(rho=0.8, rmax=1920)  # R_33 = 1.22: refused
+    V.random_search(st.lv, st.a, st.b, ok, 0, 1)
+    with pytest.raises(V.VinpError, match="32 random-search radii"):
+        V.random_search(st.lv, st.a, st.b, bad, 0, 1)

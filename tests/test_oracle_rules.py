@@ -363,3 +363,19 @@ def test_random_search_counts_distinct_valid_candidates(orc):
             ref += 1
     assert dups > 10
     assert cnt == ref
+
+
+def test_driver_stop_decision_equals_oracle(orc):
+    """The driver's host-side loop exit (driver.stop_now, python integers) takes the oracle's
+    decision (or_stop, __int128) on random and boundary statistics, for both norms."""
+    from paper_1503_05528_b200.driver import stop_now
+    import random
+    rng = random.Random(1)
+    for _ in range(3000):
+        nh = rng.randint(1, 20_000_000)
+        rule = rng.randint(0, 1)
+        edge = 3 * nh * 2 ** 20 // 10 if rule == 0 else 9 * nh * nh * 2 ** 20 // 100
+        e = max(0, edge + rng.randint(-3, 3)) if rng.random() < 0.5 else rng.randint(0, 4 * edge + 2)
+        e = min(e, 2 ** 63 - 1)  # the statistic is an int64 on both sides
+        k = rng.randint(1, 21)
+        assert stop_now(e, nh, k, 20, rule) == orc.stop(e, nh, k, 20, rule), (e, nh, k, rule)
