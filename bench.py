@@ -195,6 +195,7 @@ def main():
     barrier()
     n0 = V.launch_count()
     pu = 0
+    stale = 0
     with Clocks(local) as clk:
         e0 = torch.cuda.Event(enable_timing=True)
         e1 = torch.cuda.Event(enable_timing=True)
@@ -202,6 +203,7 @@ def main():
         for _ in range(args.steps):
             st = step()
             pu += st.total_patch_updates
+            stale += st.total_stale_skipped
         e1.record()
         barrier()
     launches = V.launch_count() - n0
@@ -273,7 +275,10 @@ def main():
                            "l2": "inputs larger than L2 (level-1 volume 1.66 GB)",
                            "parallelism": f"target slabs x{world}",
                            "exchange": args.exchange if world > 1 else None},
-                "patch_updates_per_step": pu // args.steps, "sec_per_level": levels,
+                "patch_updates_per_step": pu // args.steps,
+                # R41: stale propagation candidates proven unable to win, skipped (not patch-updates)
+                "stale_skipped_per_step": stale // args.steps, "sec_per_step": ms / args.steps / 1000.0,
+                "sec_per_level": levels,
                 "roofline": roof, "cpu_baseline": cpu, "e2e": e2e, "gpu_launches": launches,
                 "clocks": clk.summary()}
         print(json.dumps(line), flush=True)
@@ -329,7 +334,7 @@ def measure_roofline(ip, v, m, dev):
     per_level = {}
     for name, s0, s1, c0, c1, (b, e), lvl in rec:
         ms = s0.elapsed_time(s1)
-        pu = int(c1.item() - c0.item())
+        pu = int(c1[0].item() - c0[0].item())
         slots = e - b
         if name == "reconstruct":
             by = B_HOLE * slots

@@ -99,9 +99,12 @@ int main(int argc, char** argv) {
   a.n = (uint8_t*)dalloc((size_t)nt);
   b.e = (uint64_t*)dalloc(8 * (size_t)nt);
   b.n = a.n; /* n is shared by the ping-pong pair */
+  a.stamp = (uint8_t*)dalloc((size_t)nt); /* R41 change stamps: one array per buffer */
+  b.stamp = (uint8_t*)dalloc((size_t)nt);
   float* cur_rgb = (float*)dalloc(12 * (size_t)nh);
   float* cur_tex = (float*)dalloc(8 * (size_t)nh);
-  unsigned long long* counter = (unsigned long long*)dalloc(8);
+  /* [0] patch-updates (evaluated candidates), [1] stale candidates skipped (R41) */
+  unsigned long long* counter = (unsigned long long*)dalloc(16);
   const int32_t steps[4] = {8, 4, 2, 1};
 
   /* Alg. 4 at the coarsest (= only) level: random phi, onion peel (Alg. 3) */
@@ -116,8 +119,8 @@ int main(int argc, char** argv) {
   CK(vinp_reconstruct(&lv, &a, VINP_BEST_PATCH, -1, 0, nh, cur_rgb, cur_tex, 1, NULL));
   uint8_t* out_d = (uint8_t*)dalloc(3 * N);
   CK(vinp_output_rgb(&lv, out_d, NULL));
-  unsigned long long pu = 0;
-  cudaMemcpy(&pu, counter, 8, cudaMemcpyDeviceToHost);
+  unsigned long long pu[2] = {0, 0};
+  cudaMemcpy(pu, counter, 16, cudaMemcpyDeviceToHost);
   cudaMemcpy(rgb, out_d, 3 * N, cudaMemcpyDeviceToHost);
   if (cudaDeviceSynchronize() != cudaSuccess) {
     fprintf(stderr, "CUDA error: %s\n", cudaGetErrorString(cudaGetLastError()));
@@ -129,7 +132,7 @@ int main(int argc, char** argv) {
     return 1;
   }
   fclose(f);
-  printf("targets %d holes %d layers %d patch-updates %llu launches %llu\n", nt, nh, n_layers, pu,
-         (unsigned long long)vinp_launch_count());
+  printf("targets %d holes %d layers %d patch-updates %llu stale-skipped %llu launches %llu\n", nt, nh,
+         n_layers, pu[0], pu[1], (unsigned long long)vinp_launch_count());
   return 0;
 }

@@ -71,8 +71,11 @@ typedef struct {
 } vinp_level;
 
 typedef struct {
-  uint64_t* e;  /* [n_targets] (D << 32) | source index */
-  uint8_t* n;   /* [n_targets] patch voxel count; may be shared by ping-pong buffers */
+  uint64_t* e;      /* [n_targets] (D << 32) | source index */
+  uint8_t* n;       /* [n_targets] patch voxel count; may be shared by ping-pong buffers */
+  uint8_t* stamp;   /* [n_targets] or NULL: index of the pass of the current ANN search that last
+                       changed e[s] (0 = unchanged since its evaluate); one array per ping-pong
+                       buffer.  Enables the exact stale-candidate skip of vinp_propagate (R41). */
 } vinp_nnf;
 
 typedef struct {
@@ -138,6 +141,8 @@ vinp_status vinp_nnf_init_random(const vinp_level* lv, vinp_nnf* nnf, const vinp
 vinp_status vinp_nnf_upsample(const vinp_level* coarse, const vinp_nnf* cn, const vinp_level* fine,
                               vinp_nnf* fn, const vinp_params* prm, int32_t b, int32_t e,
                               void* stream);
+/* Evaluate also sets stamp[s] = 0 for every slot of [b, e) (filtered-out slots included) when
+ * nnf->stamp is given: it starts the pass numbering of an ANN search. */
 vinp_status vinp_nnf_evaluate(const vinp_level* lv, vinp_nnf* nnf, const vinp_params* prm, int kb,
                               int only_layer, int32_t b, int32_t e, unsigned long long* counter,
                               void* stream);
@@ -146,24 +151,36 @@ vinp_status vinp_nnf_evaluate(const vinp_level* lv, vinp_nnf* nnf, const vinp_pa
  * Candidates in rank order: 0 = in(p); 1..3 = in(p + sign*step*e_x / e_y / e_t) for neighbours in
  * Omega and H~ (sign = 0: 1..6 = the -step then the +step neighbours).  A candidate is evaluated iff q = p + v is in Omega and D~ and v differs from the
  * incumbent and from every earlier valid candidate; strict improvement wins.  Reads `in`, writes
- * `out` for slots [b, e).  counter (device, may be NULL) += evaluated candidates. */
+ * `out` for slots [b, e).  counter (device, may be NULL) += evaluated candidates.
+ * Stale skip (R41; only if in->stamp and out->stamp are both given, else both must be NULL):
+ * `pass` in [1, 255] is this pass's index in the current ANN search (evaluate = 0) and `since`
+ * the index of the previous pass with the same (step, sign) in that search (0 = none).  A
+ * candidate whose neighbour r has in->stamp[r] < since proposes the shift it proposed at pass
+ * `since`; it was then tested against this target (or equalled its incumbent), whose D has not
+ * grown since, so it cannot win (strict improvement) and is not evaluated: the NNF is identical
+ * to the unskipped pass.  Such candidates are counted in counter[1] (counter then points to two
+ * u64), not in counter[0].  out->stamp[s] = pass if e[s] changed, else in->stamp[s]. */
 vinp_status vinp_propagate(const vinp_level* lv, const vinp_nnf* in, vinp_nnf* out,
                            const vinp_params* prm, int step, int sign, int kb, int only_layer,
-                           int32_t b, int32_t e, unsigned long long* counter, void* stream);
+                           int32_t b, int32_t e, int pass, int since, unsigned long long* counter,
+                           void* stream);
 
 /* ---- a7: random search (Eq. 3, Alg. 1; R1, R3, R7) ----
  * v0 = in(p); for i = 1, 2, ...: R_i = rmax * rho^i (repeated fp64 multiplication) while
  * R_i >= 1; delta_c = (U_c - 2^31) 2^-31 from Philox(p, pm_iter, (level<<24)|(2<<16)|i,
- * outer_code); q_i = p + v0 + floor(R_i delta).  Same validity / duplicate / strict rules. */
+ * outer_code); q_i = p + v0 + floor(R_i delta).  Same validity / duplicate / strict rules.
+ * With stamps (as vinp_propagate), out->stamp[s] = pass if e[s] changed, else in->stamp[s]. */
 vinp_status vinp_random_search(const vinp_level* lv, const vinp_nnf* in, vinp_nnf* out,
                                const vinp_params* prm, uint32_t outer_code, int pm_iter, int kb,
-                               int only_layer, int32_t b, int32_t e, unsigned long long* counter,
-                               void* stream);
+                               int only_layer, int32_t b, int32_t e, int pass,
+                               unsigned long long* counter, void* stream);
 
 /* ---- a8: ANN search (Alg. 1), single GPU: evaluate, then for k = 1..K: for each step
  * s in steps: propagate(s, sign); random_search(k).  sign_policy 0: sign = +1 for odd k, -1 for
  * even k (Alg. 1's alternation, R5); 1: sign = 0 (both directions) on every pass (R6).  Uses `b`
- * as the ping-pong buffer; the result is in `a`. */
+ * as the ping-pong buffer; the result is in `a`.  With stamps on both buffers, passes are numbered
+ * 1, 2, ... in schedule order and the R41 stale skip is applied (counter[1], see vinp_propagate);
+ * if K * (n_steps + 1) > 255 the search runs without it. */
 vinp_status vinp_ann_search(const vinp_level* lv, vinp_nnf* a, vinp_nnf* b, const vinp_params* prm,
                             uint32_t outer_code, int K, const int32_t* steps, int n_steps,
                             int sign_policy, int kb, int only_layer, unsigned long long* counter,

@@ -374,9 +374,10 @@ static void copy_entry(const or_nnf* in, or_nnf* out, int32_t s) {
  * best if its distance is strictly smaller (R25).  Returns the number of evaluated candidates.
  * ---------------------------------------------------------------------------------------- */
 int64_t or_propagate(const or_level* lv, const or_nnf* in, or_nnf* out, int lambda, int step,
-                     int sign, int kb, int only_layer, int32_t b, int32_t e) {
-  int64_t cnt = 0;
-#pragma omp parallel for reduction(+ : cnt) schedule(dynamic, 256)
+                     int sign, int kb, int only_layer, int32_t b, int32_t e, const or_nnf* prev,
+                     int64_t* stale) {
+  int64_t cnt = 0, nst = 0;
+#pragma omp parallel for reduction(+ : cnt, nst) schedule(dynamic, 256)
   for (int32_t s = b; s < e; ++s) {
     int32_t p = lv->targets[s];
     copy_entry(in, out, s);
@@ -406,6 +407,9 @@ int64_t or_propagate(const or_level* lv, const or_nnf* in, or_nnf* out, int lamb
         if (seen[k][0] == vx && seen[k][1] == vy && seen[k][2] == vt) dup = 1;
       if (dup) continue;
       seen[nseen][0] = vx; seen[nseen][1] = vy; seen[nseen][2] = vt; ++nseen;
+      /* R41 (count only): the neighbour proposes the shift it proposed in the previous pass with
+       * this (step, sign) of the same ANN search, `prev` = that pass's input */
+      if (prev && prev->dx[rs] == vx && prev->dy[rs] == vy && prev->dt[rs] == vt) nst += 1;
       uint32_t D, n;
       or_patch_ssd(lv, p, (int32_t)lin(lv, px + vx, py + vy, pt + vt), lambda, kb, &D, &n);
       cnt += 1;
@@ -415,6 +419,7 @@ int64_t or_propagate(const or_level* lv, const or_nnf* in, or_nnf* out, int lamb
       }
     }
   }
+  if (stale) *stale = nst;
   return cnt;
 }
 
@@ -688,22 +693,47 @@ static void copy_nnf(const or_nnf* a, or_nnf* b, int32_t n) {
 /* ANN search, Alg. 1 with R3/R5/R6: evaluate; for k = 1..K: for s in steps: propagate(s, sigma_k)
  * with sigma_k = +1 for odd k and -1 for even k (sign_policy 0) or 0 = both directions
  * (sign_policy 1); random_search(k).  Result in w->a. */
-static int64_t ann_search(or_work* w, const or_params* prm, int level, uint32_t oc, int kb, int ol) {
+static int64_t ann_search(or_work* w, const or_params* prm, int level, uint32_t oc, int kb, int ol,
+                          int64_t* stale) {
   or_level* lv = &w->lv;
   int32_t n = lv->n_targets;
   int rmax = lv->W > lv->H ? lv->W : lv->H;
   if (lv->T > rmax) rmax = lv->T;
   int64_t cnt = or_nnf_evaluate(lv, &w->a, prm->lambda, kb, ol, 0, n);
+  /* R41 (count only): snap[i][sign+1] = the input of the last propagation pass of this search
+   * with step steps[i] and this sign (i = the first index holding that step) */
+  or_nnf snap[8][3];
+  int have[8][3];
+  memset(have, 0, sizeof(have));
   for (int k = 1; k <= prm->pm_iters; ++k) {
     int sign = prm->sign_policy ? 0 : ((k % 2 == 1) ? 1 : -1);
     for (int i = 0; i < prm->n_steps; ++i) {
-      cnt += or_propagate(lv, &w->a, &w->b, prm->lambda, prm->steps[i], sign, kb, ol, 0, n);
+      int i0 = 0;
+      while (prm->steps[i0] != prm->steps[i]) ++i0;
+      int h = have[i0][sign + 1];
+      or_nnf* sp = &snap[i0][sign + 1];
+      int64_t st = 0;
+      cnt += or_propagate(lv, &w->a, &w->b, prm->lambda, prm->steps[i], sign, kb, ol, 0, n,
+                          h ? sp : NULL, &st);
+      if (stale) *stale += st;
+      if (!h) {
+        sp->dx = (int32_t*)malloc(4 * (size_t)(n ? n : 1));
+        sp->dy = (int32_t*)malloc(4 * (size_t)(n ? n : 1));
+        sp->dt = (int32_t*)malloc(4 * (size_t)(n ? n : 1));
+        have[i0][sign + 1] = 1;
+      }
+      memcpy(sp->dx, w->a.dx, 4 * (size_t)n);
+      memcpy(sp->dy, w->a.dy, 4 * (size_t)n);
+      memcpy(sp->dt, w->a.dt, 4 * (size_t)n);
       copy_nnf(&w->b, &w->a, n);
     }
     cnt += or_random_search(lv, &w->a, &w->b, prm->lambda, prm->seed, prm->rho, rmax, level, oc, k,
                             kb, ol, 0, n);
     copy_nnf(&w->b, &w->a, n);
   }
+  for (int i = 0; i < 8; ++i)
+    for (int g = 0; g < 3; ++g)
+      if (have[i][g]) { free(snap[i][g].dx); free(snap[i][g].dy); free(snap[i][g].dt); }
   return cnt;
 }
 
@@ -768,7 +798,8 @@ int or_inpaint(const uint8_t* rgb, const uint8_t* occ, int W, int H, int T, cons
     or_nnf_init_random(lv, &c->a, prm->seed, L, 0, 0, lv->n_targets);
     for (int j = 0; j <= nl; ++j) {
       int kb = j < 1 ? 1 : j;
-      st->patch_updates[L - 1] += ann_search(c, prm, L, 0x80000000u | (uint32_t)j, kb, j);
+      st->patch_updates[L - 1] += ann_search(c, prm, L, 0x80000000u | (uint32_t)j, kb, j,
+                                             &st->stale[L - 1]);
       if (j >= 1) {
         or_reconstruct(lv, &c->a, OR_WEIGHTED, j, 0, lv->n_holes, c->cur_rgb, c->cur_tex);
         /* commit only layer j (the others are untouched in cur) */
@@ -789,7 +820,7 @@ int or_inpaint(const uint8_t* rgb, const uint8_t* occ, int W, int H, int T, cons
     for (;;) {
       memcpy(c->prev_rgb, c->cur_rgb, 12 * (size_t)lv->n_holes);
       memcpy(c->prev_tex, c->cur_tex, 8 * (size_t)lv->n_holes);
-      st->patch_updates[l - 1] += ann_search(c, prm, l, (uint32_t)k, -1, -1);
+      st->patch_updates[l - 1] += ann_search(c, prm, l, (uint32_t)k, -1, -1, &st->stale[l - 1]);
       or_reconstruct(lv, &c->a, OR_WEIGHTED, -1, 0, lv->n_holes, c->cur_rgb, c->cur_tex);
       or_commit(lv, c->cur_rgb, c->cur_tex, 0, lv->n_holes);
       int64_t e = prm->stop_rule == 1 ? or_change_l2(c->cur_rgb, c->prev_rgb, 3 * (int64_t)lv->n_holes)

@@ -69,8 +69,12 @@ void or_nnf_upsample(const or_level* coarse, const or_nnf* cn, const or_level* f
                      uint64_t seed, int level, int32_t b, int32_t e);
 int64_t or_nnf_evaluate(const or_level* lv, or_nnf* nnf, int lambda, int kb, int only_layer,
                         int32_t b, int32_t e);
+/* prev (may be NULL): the input NNF of the previous pass with the same (step, sign) in the same
+ * ANN search; *stale (may be NULL) receives how many of the evaluated candidates equal the shift
+ * their neighbour held in prev (R41: a count only, the pass itself is unchanged) */
 int64_t or_propagate(const or_level* lv, const or_nnf* in, or_nnf* out, int lambda, int step,
-                     int sign, int kb, int only_layer, int32_t b, int32_t e);
+                     int sign, int kb, int only_layer, int32_t b, int32_t e, const or_nnf* prev,
+                     int64_t* stale);
 int64_t or_random_search(const or_level* lv, const or_nnf* in, or_nnf* out, int lambda,
                          uint64_t seed, double rho, int rmax, int level, uint32_t outer_code,
                          int pm_iter, int kb, int only_layer, int32_t b, int32_t e);
@@ -148,6 +152,8 @@ typedef struct {
   int64_t change_fixed[16][32];
   int64_t n_holes[16];
   int64_t onion_commits;
+  /* per level: evaluated propagation candidates that were stale (R41), included in patch_updates */
+  int64_t stale[16];
 } or_stats;
 /* R19 / P:930-939 stopping decision after outer iteration k (1-based) of a level with n_holes
  * hole voxels: 1 = stop.  stop_rule 0: e_fixed = sum llrint(|a-b| 2^20), stop iff

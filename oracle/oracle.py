@@ -58,7 +58,7 @@ class OrParams(C.Structure):
 class OrStats(C.Structure):
     _fields_ = [("outer_iters", C.c_int * 16), ("patch_updates", C.c_int64 * 16),
                 ("onion_layers", C.c_int), ("change_fixed", (C.c_int64 * 32) * 16),
-                ("n_holes", C.c_int64 * 16), ("onion_commits", C.c_int64)]
+                ("n_holes", C.c_int64 * 16), ("onion_commits", C.c_int64), ("stale", C.c_int64 * 16)]
 
 
 def lib():
@@ -78,7 +78,7 @@ def lib():
             "or_nnf_init_random": (I64, [P, P, U64, I, C.c_uint32, I32, I32]),
             "or_nnf_upsample": (None, [P, P, P, P, U64, I, I32, I32]),
             "or_nnf_evaluate": (I64, [P, P, I, I, I, I32, I32]),
-            "or_propagate": (I64, [P, P, P, I, I, I, I, I, I32, I32]),
+            "or_propagate": (I64, [P, P, P, I, I, I, I, I, I32, I32, P, P]),
             "or_random_search": (I64, [P, P, P, I, U64, D, I, I, C.c_uint32, I, I, I, I32, I32]),
             "or_reconstruct": (None, [P, P, I, I, I32, I32, P, P]),
             "or_commit": (None, [P, P, P, I32, I32]),
@@ -239,9 +239,14 @@ def evaluate(lv, nnf, lam, kb=-1, ol=-1, b=0, e=None):
     return lib().or_nnf_evaluate(lv.struct(), nnf.struct(), lam, kb, ol, b, e)
 
 
-def propagate(lv, nin, nout, lam, step, sign, kb=-1, ol=-1, b=0, e=None):
+def propagate(lv, nin, nout, lam, step, sign, kb=-1, ol=-1, b=0, e=None, prev=None, stale=None):
+    """prev: the input NNF of the previous pass with this (step, sign) in the same ANN search;
+    stale: a 1-element int64 array that receives the R41 stale count (evaluated candidates whose
+    neighbour held the same shift in prev)."""
     e = len(lv.targets) if e is None else e
-    return lib().or_propagate(lv.struct(), nin.struct(), nout.struct(), lam, step, sign, kb, ol, b, e)
+    st = np.zeros(1, np.int64) if stale is None else stale
+    return lib().or_propagate(lv.struct(), nin.struct(), nout.struct(), lam, step, sign, kb, ol, b, e,
+                              prev.struct() if prev is not None else None, _p(st))
 
 
 def random_search(lv, nin, nout, lam, seed, rho, rmax, level, outer_code, pm_iter, kb=-1, ol=-1,
@@ -294,18 +299,25 @@ WEIGHTED, UNWEIGHTED, BEST_PATCH = 0, 1, 2
 
 
 def ann_search(lv, a: NNF, lam, seed, level, outer_code, pm_iters, steps=(8, 4, 2, 1), rho=0.5,
-               kb=-1, ol=-1, sign_policy=0):
-    """Alg. 1 schedule (R3/R5/R6), same as or_inpaint's internal ann_search; result in ``a``."""
+               kb=-1, ol=-1, sign_policy=0, with_stale=False):
+    """Alg. 1 schedule (R3/R5/R6), same as or_inpaint's internal ann_search; result in ``a``.
+    Returns (a, count) or, with_stale, (a, count, stale) with stale the R41 count (included in
+    count)."""
     b = a.copy()
     cnt = evaluate(lv, a, lam, kb, ol)
+    snaps = {}  # (step, sign) -> input of the last such pass (R41 stale count)
+    stale = np.zeros(1, np.int64)
+    n_stale = 0
     for k in range(1, pm_iters + 1):
         sign = 0 if sign_policy else (1 if k % 2 == 1 else -1)
         for s in steps:
-            cnt += propagate(lv, a, b, lam, s, sign, kb, ol)
+            cnt += propagate(lv, a, b, lam, s, sign, kb, ol, prev=snaps.get((s, sign)), stale=stale)
+            n_stale += int(stale[0])
+            snaps[(s, sign)] = a.copy()
             a, b = b, a
         cnt += random_search(lv, a, b, lam, seed, rho, lv.rmax, level, outer_code, k, kb, ol)
         a, b = b, a
-    return a, cnt
+    return (a, cnt, n_stale) if with_stale else (a, cnt)
 
 
 def inpaint(rgb, occ, levels, pm_iters=10, fixed_outer=0, max_outer=20, lam=50, seed=1,
@@ -327,7 +339,8 @@ def inpaint(rgb, occ, levels, pm_iters=10, fixed_outer=0, max_outer=20, lam=50, 
     return out, dict(outer_iters=list(st.outer_iters)[:levels],
                      patch_updates=list(st.patch_updates)[:levels], onion_layers=st.onion_layers,
                      change_fixed=[list(st.change_fixed[l])[:min(st.outer_iters[l], 32)] for l in range(levels)],
-                     n_holes=list(st.n_holes)[:levels], onion_commits=st.onion_commits)
+                     n_holes=list(st.n_holes)[:levels], onion_commits=st.onion_commits,
+                     stale=list(st.stale)[:levels])
 
 
 def ambiguity_exact(N):

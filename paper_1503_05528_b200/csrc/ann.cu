@@ -177,13 +177,14 @@ __device__ __forceinline__ uint32_t thread_ssd(const LevelArgs& a, int p, int px
 
 // ------------------------------------------------------------------ a5: evaluate
 __global__ void __launch_bounds__(256) k_evaluate(LevelArgs a, uint64_t* __restrict__ ee,
-                                                  uint8_t* __restrict__ en, int lambda, int kb,
-                                                  int only_layer, int32_t b, int32_t e,
-                                                  const int32_t* __restrict__ list,
+                                                  uint8_t* __restrict__ en, uint8_t* __restrict__ es,
+                                                  int lambda, int kb, int only_layer, int32_t b,
+                                                  int32_t e, const int32_t* __restrict__ list,
                                                   unsigned long long* counter) {
   int idx = b + blockIdx.x * blockDim.x + threadIdx.x;
   bool act = idx < e;
   int s = act ? (list ? __ldg(list + idx) : idx) : 0;
+  if (act && es) es[s] = 0;  // pass 0 of the ANN search (R41)
   int p = act ? __ldg(a.targets + s) : 0;
   act = act && (only_layer < 0 || a.layer[p] == only_layer);
   unsigned cnt = 0;
@@ -218,9 +219,12 @@ __global__ void __launch_bounds__(256) k_evaluate(LevelArgs a, uint64_t* __restr
 // one rank at a time by all lanes that have one, each against the running best of its own target
 // (strict improvement in rank order, R25).
 __global__ void __launch_bounds__(256, VINP_PROP_MINB) k_propagate(LevelArgs a, const uint64_t* __restrict__ ein,
-                                                   uint64_t* __restrict__ eout, int lambda, int step,
+                                                   uint64_t* __restrict__ eout,
+                                                   const uint8_t* __restrict__ sin,
+                                                   uint8_t* __restrict__ sout, int lambda, int step,
                                                    int sign, int kb, int only_layer, int32_t b,
-                                                   int32_t e, const int32_t* __restrict__ list,
+                                                   int32_t e, int pass, int since,
+                                                   const int32_t* __restrict__ list,
                                                    unsigned long long* counter) {
   int idx = b + blockIdx.x * blockDim.x + threadIdx.x;
   bool have = idx < e;
@@ -233,8 +237,10 @@ __global__ void __launch_bounds__(256, VINP_PROP_MINB) k_propagate(LevelArgs a, 
   constexpr int NCMAX = 6;
   const int nc = sign == 0 ? 6 : 3;
   int q[NCMAX] = {-1, -1, -1, -1, -1, -1};
+  bool stl[NCMAX] = {false, false, false, false, false, false};
   int px = 0, py = 0, pt = 0;
   int q0 = e_q(inc);
+  unsigned nstale = 0;
   if (act) {
     decode(a.g, p, px, py, pt);
 #pragma unroll
@@ -248,6 +254,7 @@ __global__ void __launch_bounds__(256, VINP_PROP_MINB) k_propagate(LevelArgs a, 
         int rs = __ldg(a.slot + lin(a.g, rx, ry, rt));
         if (rs >= 0) {
           int src = e_q(__ldg(reinterpret_cast<const unsigned long long*>(ein) + rs));
+          if (since > 0) stl[c] = __ldg(sin + rs) < since;  // R41: unchanged since pass `since`
           int sx, sy, st;
           decode(a.g, src, sx, sy, st);
           int qx = sx - ox, qy = sy - oy, qt = st - ot;  // q = p + (src - r)
@@ -263,6 +270,13 @@ __global__ void __launch_bounds__(256, VINP_PROP_MINB) k_propagate(LevelArgs a, 
       for (int c2 = 0; c2 < c; ++c2) dup |= (q[c2] == q[c]);
       if (dup) q[c] = -1;
     }
+    // then drop the stale survivors (R41): they cannot beat the incumbent
+#pragma unroll
+    for (int c = 0; c < NCMAX; ++c)
+      if (q[c] >= 0 && stl[c]) {
+        q[c] = -1;
+        ++nstale;
+      }
   }
   // compact this lane's candidates to the front (rank order kept), so that the warp runs the
   // SSD loop once per candidate *slot* rather than once per neighbour rank any lane has
@@ -338,9 +352,16 @@ __global__ void __launch_bounds__(256, VINP_PROP_MINB) k_propagate(LevelArgs a, 
         bestq = cq[c];
       }
     }
-    if (have) eout[s] = pack_e(bestD, bestq);
+    if (have) {
+      eout[s] = pack_e(bestD, bestq);
+      if (sout) sout[s] = bestq != q0 ? (uint8_t)pass : __ldg(sin + s);
+    }
     cnt = __reduce_add_sync(kFull, cnt);
-    if ((threadIdx.x & 31) == 0) flush_count(counter, cnt);
+    nstale = __reduce_add_sync(kFull, nstale);
+    if ((threadIdx.x & 31) == 0) {
+      flush_count(counter, cnt);
+      if (counter && nstale) flush_count(counter + 1, nstale);
+    }
     return;
   }
 #endif
@@ -359,9 +380,16 @@ __global__ void __launch_bounds__(256, VINP_PROP_MINB) k_propagate(LevelArgs a, 
       ++cnt;
     }
   }
-  if (have) eout[s] = pack_e(bestD, bestq);
+  if (have) {
+    eout[s] = pack_e(bestD, bestq);
+    if (sout) sout[s] = bestq != q0 ? (uint8_t)pass : __ldg(sin + s);
+  }
   cnt = __reduce_add_sync(kFull, cnt);
-  if ((threadIdx.x & 31) == 0) flush_count(counter, cnt);
+  nstale = __reduce_add_sync(kFull, nstale);
+  if ((threadIdx.x & 31) == 0) {
+    flush_count(counter, cnt);
+    if (counter && nstale) flush_count(counter + 1, nstale);
+  }
 }
 
 // Warp-per-target patch (onion passes): lane l owns the voxels k = l + 32 j (j < 4, k < 125) of
@@ -415,8 +443,9 @@ struct WideTarget {
 // chain is ~8 round trips.  No early abort: a candidate is kept iff D < best in rank order (R25),
 // the same decision the aborting pass takes; counts one patch-update per evaluated candidate.
 __global__ void __launch_bounds__(VINP_WIDE_BLOCK) k_propagate_wide(
-    LevelArgs a, const uint64_t* __restrict__ ein, uint64_t* __restrict__ eout, int lambda,
-    int step, int sign, int kb, int only_layer, int32_t b, int32_t e,
+    LevelArgs a, const uint64_t* __restrict__ ein, uint64_t* __restrict__ eout,
+    const uint8_t* __restrict__ sin, uint8_t* __restrict__ sout, int lambda, int step, int sign,
+    int kb, int only_layer, int32_t b, int32_t e, int pass, int since,
     const int32_t* __restrict__ list, unsigned long long* counter) {
   const int lane = threadIdx.x & 31;
   const int idx = b + (int)((blockIdx.x * (unsigned)blockDim.x + threadIdx.x) >> 5);
@@ -427,7 +456,10 @@ __global__ void __launch_bounds__(VINP_WIDE_BLOCK) k_propagate_wide(
   // a filtered full-range launch (per-pass path): most warps leave here.  With a layer list
   // (vinp_onion_peel) every target is in the layer, and the test waits until the end
   if (!list && only_layer >= 0 && a.layer[p] != only_layer) {
-    if (lane == 0) eout[s] = inc;
+    if (lane == 0) {
+      eout[s] = inc;
+      if (sout) sout[s] = sin[s];
+    }
     return;
   }
   const bool act = only_layer < 0 || a.layer[p] == only_layer;  // used at the end: no stall here
@@ -440,6 +472,7 @@ __global__ void __launch_bounds__(VINP_WIDE_BLOCK) k_propagate_wide(
   const int nc = sign == 0 ? 6 : 3;
   // candidate c on lane c (neighbour shift -> its NNF entry -> q = p + (src - r) -> q in D~?)
   int myq = -1;
+  bool mystl = false;
   if (lane < nc) {
     const int c = lane;
     const int sg = sign != 0 ? sign : (c < 3 ? -1 : 1);
@@ -450,6 +483,7 @@ __global__ void __launch_bounds__(VINP_WIDE_BLOCK) k_propagate_wide(
       const int rs = __ldg(a.slot + lin(a.g, rx, ry, rt));
       if (rs >= 0) {
         const int src = e_q(__ldg(reinterpret_cast<const unsigned long long*>(ein) + rs));
+        if (since > 0) mystl = __ldg(sin + rs) < since;  // R41
         int sx, sy, st;
         decode(a.g, src, sx, sy, st);
         const int qx = sx - ox, qy = sy - oy, qt = st - ot;
@@ -464,13 +498,19 @@ __global__ void __launch_bounds__(VINP_WIDE_BLOCK) k_propagate_wide(
   int q[6];
 #pragma unroll
   for (int c = 0; c < 6; ++c) q[c] = __shfl_sync(kFull, myq, c);
+  const unsigned stlm = __ballot_sync(kFull, mystl);
   bool keep[6];
+  unsigned nstale = 0;
 #pragma unroll
   for (int c = 0; c < 6; ++c) {
     bool dup = !act || c >= nc || q[c] < 0 || q[c] == q0;
 #pragma unroll
     for (int c2 = 0; c2 < c; ++c2) dup |= (q[c2] == q[c]);
     keep[c] = !dup;
+    if (keep[c] && ((stlm >> c) & 1)) {  // R41: stale, cannot win
+      keep[c] = false;
+      ++nstale;
+    }
   }
   // all candidate gathers in flight together (q in D~: its whole patch lies in the volume)
   uint32_t part[6];
@@ -491,14 +531,17 @@ __global__ void __launch_bounds__(VINP_WIDE_BLOCK) k_propagate_wide(
   }
   if (lane == 0) {
     eout[s] = pack_e(bestD, bestq);
+    if (sout) sout[s] = bestq != q0 ? (uint8_t)pass : sin[s];
     flush_count(counter, cnt);
+    if (counter && nstale) flush_count(counter + 1, nstale);
   }
 }
 
 // Onion (K-restricted) evaluate, warp per target: D(p, phi(p)) over the voxels of N_p in Omega
 // and K (Alg. 3: only known voxels count) and their number n.
 __global__ void __launch_bounds__(VINP_WIDE_BLOCK) k_evaluate_wide(LevelArgs a, uint64_t* __restrict__ ee,
-                                                                   uint8_t* __restrict__ en, int lambda,
+                                                                   uint8_t* __restrict__ en,
+                                                                   uint8_t* __restrict__ es, int lambda,
                                                                    int kb, int only_layer, int32_t b,
                                                                    int32_t e, const int32_t* __restrict__ list,
                                                                    unsigned long long* counter) {
@@ -506,6 +549,7 @@ __global__ void __launch_bounds__(VINP_WIDE_BLOCK) k_evaluate_wide(LevelArgs a, 
   const int idx = b + (int)((blockIdx.x * (unsigned)blockDim.x + threadIdx.x) >> 5);
   if (idx >= e) return;  // warp-uniform
   const int s = list ? __ldg(list + idx) : idx;
+  if (es && lane == 0) es[s] = 0;  // pass 0 of the ANN search (R41)
   const int p = __ldg(a.targets + s);
   if (only_layer >= 0 && a.layer[p] != only_layer) return;
   int px, py, pt;
@@ -543,8 +587,9 @@ __device__ __forceinline__ uint32_t sum5(uint32_t x, int base, int k) {
 
 template <int NC, int WPB, int TPW>
 __global__ void __launch_bounds__(32 * WPB, VINP_MINB * 8 / WPB) k_random_search(
-    LevelArgs a, const uint64_t* __restrict__ ein, uint64_t* __restrict__ eout, int lambda, Radii rad,
-    uint64_t seed, uint32_t oc, int pm_iter, int only_layer, int32_t b, int32_t e,
+    LevelArgs a, const uint64_t* __restrict__ ein, uint64_t* __restrict__ eout,
+    const uint8_t* __restrict__ sin, uint8_t* __restrict__ sout, int lambda, Radii rad,
+    uint64_t seed, uint32_t oc, int pm_iter, int only_layer, int32_t b, int32_t e, int pass,
     const int32_t* __restrict__ list, unsigned long long* counter) {
   // TPW targets per warp (32; 8 for small launches, so that more warps share
   // the pair evaluations — the result does not depend on it)
@@ -684,7 +729,10 @@ __global__ void __launch_bounds__(32 * WPB, VINP_MINB * 8 / WPB) k_random_search
         ++dtc;
     }
   }
-  if (have) eout[s] = pack_e(bestD, bestq);
+  if (have) {
+    eout[s] = pack_e(bestD, bestq);
+    if (sout) sout[s] = bestq != e_q(inc) ? (uint8_t)pass : __ldg(sin + s);
+  }
   if (lane == 0) flush_count(counter, (unsigned)P);
 }
 
@@ -694,8 +742,9 @@ __global__ void __launch_bounds__(32 * WPB, VINP_MINB * 8 / WPB) k_random_search
 // then evaluates the kept candidates 4 at a time with every gather of a batch in flight and
 // applies them in rank order with strict improvement (R25).
 __global__ void __launch_bounds__(VINP_WIDE_BLOCK) k_random_search_wide(
-    LevelArgs a, const uint64_t* __restrict__ ein, uint64_t* __restrict__ eout, int lambda, Radii rad,
-    uint64_t seed, uint32_t oc, int pm_iter, int kb, int only_layer, int32_t b, int32_t e,
+    LevelArgs a, const uint64_t* __restrict__ ein, uint64_t* __restrict__ eout,
+    const uint8_t* __restrict__ sin, uint8_t* __restrict__ sout, int lambda, Radii rad,
+    uint64_t seed, uint32_t oc, int pm_iter, int kb, int only_layer, int32_t b, int32_t e, int pass,
     const int32_t* __restrict__ list, unsigned long long* counter) {
   const int lane = threadIdx.x & 31;
   const int idx = b + (int)((blockIdx.x * (unsigned)blockDim.x + threadIdx.x) >> 5);
@@ -704,7 +753,10 @@ __global__ void __launch_bounds__(VINP_WIDE_BLOCK) k_random_search_wide(
   const int p = __ldg(a.targets + s);
   const uint64_t inc = __ldg(reinterpret_cast<const unsigned long long*>(ein) + s);
   if (!list && only_layer >= 0 && a.layer[p] != only_layer) {  // as k_propagate_wide
-    if (lane == 0) eout[s] = inc;
+    if (lane == 0) {
+      eout[s] = inc;
+      if (sout) sout[s] = sin[s];
+    }
     return;
   }
   const bool act = only_layer < 0 || a.layer[p] == only_layer;
@@ -760,6 +812,7 @@ __global__ void __launch_bounds__(VINP_WIDE_BLOCK) k_random_search_wide(
   }
   if (lane == 0) {
     eout[s] = pack_e(bestD, bestq);
+    if (sout) sout[s] = bestq != q0 ? (uint8_t)pass : sin[s];
     flush_count(counter, cnt);
   }
 }
@@ -954,31 +1007,46 @@ vinp_status launch_evaluate(const vinp_level* lv, vinp_nnf* nnf, const vinp_para
   if (e > b) {
     if (kb >= 0)  // K-restricted (onion) launch: warp per target
       k_evaluate_wide<<<nblk((int64_t)(e - b) * 32, VINP_WIDE_BLOCK), VINP_WIDE_BLOCK, 0, S(stream)>>>(
-          args_of(lv), nnf->e, nnf->n, prm->lambda, kb, only_layer, b, e, list, counter);
+          args_of(lv), nnf->e, nnf->n, nnf->stamp, prm->lambda, kb, only_layer, b, e, list, counter);
     else
       k_evaluate<<<nblk(e - b, VINP_EVAL_BLOCK), VINP_EVAL_BLOCK, 0, S(stream)>>>(
-          args_of(lv), nnf->e, nnf->n, prm->lambda, kb, only_layer, b, e, list, counter);
+          args_of(lv), nnf->e, nnf->n, nnf->stamp, prm->lambda, kb, only_layer, b, e, list, counter);
     count_launch();
   }
   return check_launch("vinp_nnf_evaluate");
 }
+// R41 stamps: both buffers or neither; pass in [1, 255]; since in [0, pass)
+static vinp_status check_stamps(const vinp_nnf* in, const vinp_nnf* out, int pass, int since,
+                                const char* who) {
+  VINP_REQUIRE(!in->stamp == !out->stamp, "%s: stamps must be given on both buffers or neither", who);
+  VINP_REQUIRE(!in->stamp || in->stamp != out->stamp, "%s: the two buffers share a stamp array", who);
+  VINP_REQUIRE(!in->stamp || (pass >= 1 && pass <= 255 && since >= 0 && since < pass),
+               "%s: need 1 <= pass <= 255 and 0 <= since < pass (got %d, %d)", who, pass, since);
+  return VINP_OK;
+}
+
 vinp_status launch_propagate(const vinp_level* lv, const vinp_nnf* in, vinp_nnf* out,
                              const vinp_params* prm, int step, int sign, int kb, int only_layer,
-                             int32_t b, int32_t e, const int32_t* list, unsigned long long* counter,
-                             void* stream) {
+                             int32_t b, int32_t e, int pass, int since, const int32_t* list,
+                             unsigned long long* counter, void* stream) {
   vinp_status st = check_nnf_args(lv, "vinp_propagate", list ? 0 : b, list ? 0 : e, prm);
   if (st) return st;
   VINP_REQUIRE(in && in->e && out && out->e && in->e != out->e, "vinp_propagate: need two buffers");
+  st = check_stamps(in, out, pass, since, "vinp_propagate");
+  if (st) return st;
+  if (!in->stamp) since = 0;
   VINP_REQUIRE(step >= 1 && sign >= -1 && sign <= 1, "vinp_propagate: bad step/sign");
   VINP_REQUIRE((kb < 0 && only_layer < 0) || lv->layer, "vinp_propagate: layer map required");
   if (e > b) {
     const int pb = e - b >= VINP_PROP_BIG ? VINP_PROP_BLOCK : VINP_PROP_BLOCK_MID;
     if (kb >= 0)  // K-restricted (onion) launch: warp per target
       k_propagate_wide<<<nblk((int64_t)(e - b) * 32, VINP_WIDE_BLOCK), VINP_WIDE_BLOCK, 0, S(stream)>>>(
-          args_of(lv), in->e, out->e, prm->lambda, step, sign, kb, only_layer, b, e, list, counter);
+          args_of(lv), in->e, out->e, in->stamp, out->stamp, prm->lambda, step, sign, kb, only_layer, b, e,
+          pass, since, list, counter);
     else
       k_propagate<<<nblk(e - b, pb), pb, 0, S(stream)>>>(
-          args_of(lv), in->e, out->e, prm->lambda, step, sign, kb, only_layer, b, e, list, counter);
+          args_of(lv), in->e, out->e, in->stamp, out->stamp, prm->lambda, step, sign, kb, only_layer, b, e,
+          pass, since, list, counter);
     count_launch();
   }
   return check_launch("vinp_propagate");
@@ -994,8 +1062,10 @@ vinp_status vinp_nnf_evaluate(const vinp_level* lv, vinp_nnf* nnf, const vinp_pa
 
 vinp_status vinp_propagate(const vinp_level* lv, const vinp_nnf* in, vinp_nnf* out,
                            const vinp_params* prm, int step, int sign, int kb, int only_layer,
-                           int32_t b, int32_t e, unsigned long long* counter, void* stream) {
-  return launch_propagate(lv, in, out, prm, step, sign, kb, only_layer, b, e, nullptr, counter, stream);
+                           int32_t b, int32_t e, int pass, int since, unsigned long long* counter,
+                           void* stream) {
+  return launch_propagate(lv, in, out, prm, step, sign, kb, only_layer, b, e, pass, since, nullptr,
+                          counter, stream);
 }
 
 }  // extern "C"
@@ -1003,11 +1073,13 @@ vinp_status vinp_propagate(const vinp_level* lv, const vinp_nnf* in, vinp_nnf* o
 namespace vinp {
 vinp_status launch_random_search(const vinp_level* lv, const vinp_nnf* in, vinp_nnf* out,
                                  const vinp_params* prm, uint32_t outer_code, int pm_iter, int kb,
-                                 int only_layer, int32_t b, int32_t e, const int32_t* list,
+                                 int only_layer, int32_t b, int32_t e, int pass, const int32_t* list,
                                  unsigned long long* counter, void* stream) {
   vinp_status st = check_nnf_args(lv, "vinp_random_search", list ? 0 : b, list ? 0 : e, prm);
   if (st) return st;
   VINP_REQUIRE(in && in->e && out && out->e && in->e != out->e, "vinp_random_search: need two buffers");
+  st = check_stamps(in, out, pass, 0, "vinp_random_search");
+  if (st) return st;
   VINP_REQUIRE(prm->rho > 0 && prm->rho < 1, "vinp_random_search: rho must lie in (0,1)");
   VINP_REQUIRE((kb < 0 && only_layer < 0) || lv->layer, "vinp_random_search: layer map required");
   Radii r = make_radii(lv, prm);
@@ -1017,8 +1089,8 @@ vinp_status launch_random_search(const vinp_level* lv, const vinp_nnf* in, vinp_
   }
   if (e > b && kb >= 0) {  // K-restricted (onion) launch: warp per target (M <= 32 lanes)
     k_random_search_wide<<<nblk((int64_t)(e - b) * 32, VINP_WIDE_BLOCK), VINP_WIDE_BLOCK, 0, S(stream)>>>(
-        args_of(lv), in->e, out->e, prm->lambda, r, prm->seed, outer_code, pm_iter, kb, only_layer, b, e,
-        list, counter);
+        args_of(lv), in->e, out->e, in->stamp, out->stamp, prm->lambda, r, prm->seed, outer_code, pm_iter, kb,
+        only_layer, b, e, pass, list, counter);
     count_launch();
   } else if (e > b) {
     cudaStream_t cs = S(stream);
@@ -1026,7 +1098,8 @@ vinp_status launch_random_search(const vinp_level* lv, const vinp_nnf* in, vinp_
     const bool small = (e - b) < VINP_RS_SMALL;
 #define VINP_RS2(NC, WPB, TPW)                                                                       \
   k_random_search<NC, WPB, TPW><<<nblk(e - b, TPW * WPB), 32 * WPB, 0, cs>>>(                           \
-      la, in->e, out->e, prm->lambda, r, prm->seed, outer_code, pm_iter, only_layer, b, e, list, counter)
+      la, in->e, out->e, in->stamp, out->stamp, prm->lambda, r, prm->seed, outer_code, pm_iter, only_layer, b, e, \
+      pass, list, counter)
 #define VINP_RS(NC, WPB)          \
   do {                            \
     if (small)                    \
@@ -1053,9 +1126,9 @@ vinp_status launch_random_search(const vinp_level* lv, const vinp_nnf* in, vinp_
 extern "C" {
 vinp_status vinp_random_search(const vinp_level* lv, const vinp_nnf* in, vinp_nnf* out,
                                const vinp_params* prm, uint32_t outer_code, int pm_iter, int kb,
-                               int only_layer, int32_t b, int32_t e, unsigned long long* counter,
-                               void* stream) {
-  return launch_random_search(lv, in, out, prm, outer_code, pm_iter, kb, only_layer, b, e, nullptr,
+                               int only_layer, int32_t b, int32_t e, int pass,
+                               unsigned long long* counter, void* stream) {
+  return launch_random_search(lv, in, out, prm, outer_code, pm_iter, kb, only_layer, b, e, pass, nullptr,
                               counter, stream);
 }
 
@@ -1065,23 +1138,30 @@ vinp_status vinp_ann_search(const vinp_level* lv, vinp_nnf* a, vinp_nnf* b, cons
                             void* stream) {
   VINP_REQUIRE(sign_policy == 0 || sign_policy == 1, "vinp_ann_search: bad sign_policy");
   VINP_REQUIRE(a && b && steps && n_steps >= 0 && n_steps <= 16 && K >= 0, "vinp_ann_search: bad args");
-  vinp_status st = vinp_nnf_evaluate(lv, a, prm, kb, only_layer, 0, lv->n_targets, counter, stream);
+  vinp_nnf ua = *a, ub = *b;
+  if ((int64_t)K * (n_steps + 1) > 255) ua.stamp = ub.stamp = nullptr;  // pass index would overflow u8
+  vinp_status st = vinp_nnf_evaluate(lv, &ua, prm, kb, only_layer, 0, lv->n_targets, counter, stream);
   if (st) return st;
-  vinp_nnf* cur = a;
-  vinp_nnf* nxt = b;
+  vinp_nnf* cur = &ua;
+  vinp_nnf* nxt = &ub;
+  PassClock clk;
   for (int k = 1; k <= K; ++k) {
     int sign = sign_policy ? 0 : ((k % 2 == 1) ? 1 : -1);
     for (int i = 0; i < n_steps; ++i) {
-      st = vinp_propagate(lv, cur, nxt, prm, steps[i], sign, kb, only_layer, 0, lv->n_targets,
-                          counter, stream);
+      int since = clk.since(steps[i], sign);
+      st = vinp_propagate(lv, cur, nxt, prm, steps[i], sign, kb, only_layer, 0, lv->n_targets, clk.pass,
+                          since, counter, stream);
       if (st) return st;
+      clk.tick(steps[i], sign);
       std::swap(cur, nxt);
     }
-    st = vinp_random_search(lv, cur, nxt, prm, outer_code, k, kb, only_layer, 0, lv->n_targets,
+    st = vinp_random_search(lv, cur, nxt, prm, outer_code, k, kb, only_layer, 0, lv->n_targets, clk.pass,
                             counter, stream);
     if (st) return st;
+    clk.tick(0, 2);
     std::swap(cur, nxt);
   }
+  cur = cur == &ua ? a : b;
   if (cur != a && lv->n_targets > 0) {
     if (cudaMemcpyAsync(a->e, cur->e, sizeof(uint64_t) * lv->n_targets, cudaMemcpyDeviceToDevice,
                         S(stream)) != cudaSuccess)

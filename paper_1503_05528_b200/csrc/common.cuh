@@ -47,12 +47,39 @@ vinp_status launch_evaluate(const vinp_level* lv, vinp_nnf* nnf, const vinp_para
                             unsigned long long* counter, void* stream);
 vinp_status launch_propagate(const vinp_level* lv, const vinp_nnf* in, vinp_nnf* out,
                              const vinp_params* prm, int step, int sign, int kb, int only_layer,
-                             int32_t b, int32_t e, const int32_t* list, unsigned long long* counter,
-                             void* stream);
+                             int32_t b, int32_t e, int pass, int since, const int32_t* list,
+                             unsigned long long* counter, void* stream);
 vinp_status launch_random_search(const vinp_level* lv, const vinp_nnf* in, vinp_nnf* out,
                                  const vinp_params* prm, uint32_t outer_code, int pm_iter, int kb,
-                                 int only_layer, int32_t b, int32_t e, const int32_t* list,
+                                 int only_layer, int32_t b, int32_t e, int pass, const int32_t* list,
                                  unsigned long long* counter, void* stream);
+
+// Pass numbering of one ANN search for the R41 stale skip (host side): evaluate = pass 0, then
+// 1, 2, ... in schedule order; since(step, sign) = the index of the last earlier propagation pass
+// with that (step, sign), 0 if none.
+struct PassClock {
+  int pass = 1;
+  int n = 0;
+  int key_step[64], key_sign[64], last[64];
+  int since(int step, int sign) const {
+    for (int i = 0; i < n; ++i)
+      if (key_step[i] == step && key_sign[i] == sign) return last[i];
+    return 0;
+  }
+  void tick(int step, int sign) {  // sign 2 = a random-search pass
+    if (sign != 2) {
+      int i = 0;
+      while (i < n && !(key_step[i] == step && key_sign[i] == sign)) ++i;
+      if (i == n && n < 64) {
+        key_step[n] = step;
+        key_sign[n] = sign;
+        ++n;
+      }
+      if (i < 64) last[i] = pass;
+    }
+    ++pass;
+  }
+};
 vinp_status launch_reconstruct(vinp_level* lv, const vinp_nnf* nnf, int mode, int layer_j, int32_t hb,
                                int32_t he, const int32_t* list, float* out_rgb, float* out_tex,
                                int commit, void* stream);

@@ -168,6 +168,11 @@ vinp_status vinp_onion_peel(vinp_level* lv, vinp_nnf* a, vinp_nnf* b, const vinp
   int* bc = (int*)w;
   int nkeys = n_layers + 1;
   int mx = std::max(nt, nh);
+  VINP_REQUIRE(!a->stamp == !b->stamp && (!a->stamp || a->stamp != b->stamp),
+               "vinp_onion_peel: stamps must be given on both buffers (distinct) or neither");
+  vinp_nnf ua = *a, ub = *b;
+  const bool use = a->stamp && (int64_t)K * (n_steps + 1) <= 255;
+  if (!use) ua.stamp = ub.stamp = nullptr;
   if (mx > 0) {
     k_iota<<<nblk(mx, 256), 256, 0, s>>>(iota, mx);
     count_launch();
@@ -193,23 +198,31 @@ vinp_status vinp_onion_peel(vinp_level* lv, vinp_nnf* a, vinp_nnf* b, const vinp
     // both buffers agree outside layer j for the whole layer (Jacobi passes touch layer j only)
     if (nt > 0 && cudaMemcpyAsync(b->e, a->e, 8 * (size_t)nt, cudaMemcpyDeviceToDevice, s) != cudaSuccess)
       return check_launch("vinp_onion_peel(copy)");
-    vinp_nnf* cur = a;
-    vinp_nnf* nxt = b;
+    // R41 stamps: every entry is unchanged since the start of layer j's search (pass 0)
+    if (use && nt > 0 && (cudaMemsetAsync(a->stamp, 0, (size_t)nt, s) != cudaSuccess ||
+                          cudaMemsetAsync(b->stamp, 0, (size_t)nt, s) != cudaSuccess))
+      return check_launch("vinp_onion_peel(stamps)");
+    vinp_nnf* cur = &ua;
+    vinp_nnf* nxt = &ub;
     if (te > tb) {
       st = launch_evaluate(lv, cur, prm, kb, j, tb, te, tlist, counter, stream);
       if (st) return st;
+      PassClock clk;
       for (int k = 1; k <= K; ++k) {
         int sign = sign_policy ? 0 : ((k % 2 == 1) ? 1 : -1);
         for (int i = 0; i < n_steps; ++i) {
-          st = launch_propagate(lv, cur, nxt, prm, steps[i], sign, kb, j, tb, te, tlist, counter, stream);
+          st = launch_propagate(lv, cur, nxt, prm, steps[i], sign, kb, j, tb, te, clk.pass,
+                                clk.since(steps[i], sign), tlist, counter, stream);
           if (st) return st;
+          clk.tick(steps[i], sign);
           std::swap(cur, nxt);
         }
-        st = launch_random_search(lv, cur, nxt, prm, oc, k, kb, j, tb, te, tlist, counter, stream);
+        st = launch_random_search(lv, cur, nxt, prm, oc, k, kb, j, tb, te, clk.pass, tlist, counter, stream);
         if (st) return st;
+        clk.tick(0, 2);
         std::swap(cur, nxt);
       }
-      if (cur != a && cudaMemcpyAsync(a->e, cur->e, 8 * (size_t)nt, cudaMemcpyDeviceToDevice, s) != cudaSuccess)
+      if (cur != &ua && cudaMemcpyAsync(a->e, cur->e, 8 * (size_t)nt, cudaMemcpyDeviceToDevice, s) != cudaSuccess)
         return check_launch("vinp_onion_peel(copy)");
     }
     if (j >= 1 && hoff[j + 1] > hoff[j]) {

@@ -43,6 +43,7 @@ class Config:
     align_tol: float = 1e-4     # R38: update-norm stop
     exchange: str = "allgather"  # multi-GPU: "allgather" every pass, or "halo" (NEXT #4, P2P)
     stop_rule: int = 0          # 0: R19 e = ||u_H - v_H||_1 / (3|H|); 1: literal P:988 ||.||_2 / (3|H|)
+    skip_stale: bool = True     # R41: exact skip of stale propagation candidates (NNF unchanged)
 
     def params(self) -> V.Params:
         return V.Params(lam=self.lam, tex_half=self.tex_half, seed=self.seed, rho=self.rho)
@@ -141,7 +142,8 @@ class Stats:
     total_ms: float = 0.0
     onion_ms: float = 0.0
 
-    total_patch_updates: int = 0
+    total_patch_updates: int = 0   # evaluated candidates (patch-updates)
+    total_stale_skipped: int = 0   # R41 stale propagation candidates skipped (not patch-updates)
 
     @property
     def patch_updates(self):
@@ -166,7 +168,8 @@ class Inpainter:
         n1 = W * H * T
         self.ws = torch.empty(max(self.V.texture_ws_bytes(self.levels[0]), self.V.sets_ws_bytes(self.levels[0])) + 256,
                               dtype=torch.uint8, device=self.device)
-        self.counter = torch.zeros(1, dtype=torch.int64, device=self.device)
+        # [0] patch-updates (evaluated candidates), [1] stale candidates skipped (R41)
+        self.counter = torch.zeros(2, dtype=torch.int64, device=self.device)
         self.change = torch.zeros(1, dtype=torch.int64, device=self.device)
         self.states: List[LevelState] = []
         self.stats = Stats()
@@ -201,8 +204,8 @@ class Inpainter:
                 continue
             # every NNF entry / hole value is written (init, upsample, evaluate, reconstruct)
             # before it is read, so no zero fill is needed
-            a = V.NNF.alloc(npad, self.device, zero=False)
-            b = V.NNF.alloc(npad, self.device, n=a.n, zero=False)
+            a = V.NNF.alloc(npad, self.device, zero=False, stamp=self.cfg.skip_stale)
+            b = V.NNF.alloc(npad, self.device, n=a.n, zero=False, stamp=self.cfg.skip_stale)
             z = lambda k: torch.empty((hpad, k), dtype=torch.float32, device=self.device)
             self.states.append(LevelState(lv, a, b, z(3), z(2), z(3), z(2)))
         self.halo = self.cfg.exchange == "halo" and self.ex.world > 1
@@ -257,23 +260,38 @@ class Inpainter:
             return
         b, e = self.ex.slab(n)
         if replicated:
-            gather = lambda t: None  # noqa: E731
+            gather1 = lambda t: None  # noqa: E731
         elif self.halo:
-            gather = lambda t: self.ex.halo(t, n, st.halo_nnf)  # noqa: E731
+            gather1 = lambda t: self.ex.halo(t, n, st.halo_nnf)  # noqa: E731
         else:
-            gather = lambda t: self.ex.gather(t, n)  # noqa: E731
-        self.V.nnf_evaluate(lv, st.a, prm, kb, only_layer, b, e, self.counter)
-        gather(st.a.e)
-        gather(st.a.n)
+            gather1 = lambda t: self.ex.gather(t, n)  # noqa: E731
+
+        def gather(f):  # an NNF buffer: entries, and the R41 stamps the next pass reads
+            gather1(f.e)
+            if f.stamp is not None:
+                gather1(f.stamp)
+
+        use = st.a.stamp is not None and cfg.pm_iters * (len(cfg.steps) + 1) <= 255
+        a_nnf, b_nnf = (st.a, st.b) if use else (V.NNF(st.a.e, st.a.n), V.NNF(st.b.e, st.b.n))
+        self.V.nnf_evaluate(lv, a_nnf, prm, kb, only_layer, b, e, self.counter)
+        gather(a_nnf)
+        gather1(a_nnf.n)
+        clk = V.PassClock()
         for k in range(1, cfg.pm_iters + 1):
             sign = 0 if cfg.sign_policy else (1 if k % 2 == 1 else -1)
             for s in cfg.steps:
-                self.V.propagate(lv, st.a, st.b, prm, s, sign, kb, only_layer, b, e, self.counter)
+                self.V.propagate(lv, a_nnf, b_nnf, prm, s, sign, kb, only_layer, b, e, self.counter,
+                                 pass_id=clk.pass_id, since=clk.since(s, sign))
+                clk.tick(s, sign)
+                a_nnf, b_nnf = b_nnf, a_nnf
                 st.a, st.b = st.b, st.a
-                gather(st.a.e)
-            self.V.random_search(lv, st.a, st.b, prm, outer_code, k, kb, only_layer, b, e, self.counter)
+                gather(a_nnf)
+            self.V.random_search(lv, a_nnf, b_nnf, prm, outer_code, k, kb, only_layer, b, e, self.counter,
+                                 pass_id=clk.pass_id)
+            clk.tick()
+            a_nnf, b_nnf = b_nnf, a_nnf
             st.a, st.b = st.b, st.a
-            gather(st.a.e)
+            gather(a_nnf)
 
     def reconstruct(self, st: LevelState, mode: int, layer_j=-1, replicated=False, full=False):
         lv = st.lv
@@ -393,16 +411,18 @@ class Inpainter:
         for l in range(L, 0, -1):
             per.append(snaps[l] - prev)
             prev = snaps[l]
-        per = torch.cat(per)
+        per = torch.stack(per)  # [level (coarsest first), (evaluated, stale)]
         if self.ex.rank != 0:
-            per[0] -= onion_pu[0]
+            per[0] -= onion_pu
         self.ex.allreduce_sum(per)
         per = per.tolist()
         for d in self.stats.levels:  # the stopping statistic of every outer iteration (x 2^20)
             d["change_fixed"] = [int(c) for c in d.get("change_fixed", [])]
         for i, l in enumerate(range(L, 0, -1)):
-            self.stats.levels[l - 1]["patch_updates"] = int(per[i])
-        self.stats.total_patch_updates = int(sum(per))
+            self.stats.levels[l - 1]["patch_updates"] = int(per[i][0])
+            self.stats.levels[l - 1]["stale_skipped"] = int(per[i][1])
+        self.stats.total_patch_updates = int(sum(x[0] for x in per))
+        self.stats.total_stale_skipped = int(sum(x[1] for x in per))
         return self.stats
 
     def output(self, rgb_in: torch.Tensor) -> torch.Tensor:

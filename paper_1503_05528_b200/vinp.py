@@ -34,7 +34,7 @@ class _Level(C.Structure):
 
 
 class _NNF(C.Structure):
-    _fields_ = [("e", C.c_void_p), ("n", C.c_void_p)]
+    _fields_ = [("e", C.c_void_p), ("n", C.c_void_p), ("stamp", C.c_void_p)]
 
 
 class _Params(C.Structure):
@@ -62,8 +62,8 @@ def _load():
         "vinp_nnf_init_random": (I, [P, P, P, U32, I32, I32, P]),
         "vinp_nnf_upsample": (I, [P, P, P, P, P, I32, I32, P]),
         "vinp_nnf_evaluate": (I, [P, P, P, I, I, I32, I32, P, P]),
-        "vinp_propagate": (I, [P, P, P, P, I, I, I, I, I32, I32, P, P]),
-        "vinp_random_search": (I, [P, P, P, P, U32, I, I, I, I32, I32, P, P]),
+        "vinp_propagate": (I, [P, P, P, P, I, I, I, I, I32, I32, I, I, P, P]),
+        "vinp_random_search": (I, [P, P, P, P, U32, I, I, I, I32, I32, I, P, P]),
         "vinp_ann_search": (I, [P, P, P, P, U32, I, P, I, I, I, I, P, P]),
         "vinp_onion_ws_bytes": (C.c_size_t, [P]),
         "vinp_onion_peel": (I, [P, P, P, P, I, P, I, I, I, P, P, P, P, C.c_size_t, P]),
@@ -200,18 +200,20 @@ class Level:
 class NNF:
     e: torch.Tensor
     n: torch.Tensor
+    stamp: Optional[torch.Tensor] = None  # R41 change stamps (one per ping-pong buffer) or None
     _s: object = field(default=None, repr=False)
 
     @classmethod
-    def alloc(cls, n_slots, device, n=None, zero=True):
+    def alloc(cls, n_slots, device, n=None, zero=True, stamp=False):
         mk = torch.zeros if zero else torch.empty
         e = mk(max(n_slots, 1), dtype=torch.int64, device=device)
         if n is None:
             n = mk(max(n_slots, 1), dtype=torch.uint8, device=device)
-        return cls(e, n)
+        st = torch.zeros(max(n_slots, 1), dtype=torch.uint8, device=device) if stamp else None
+        return cls(e, n, st)
 
     def struct(self):
-        self._s = _NNF(_ptr(self.e), _ptr(self.n))
+        self._s = _NNF(_ptr(self.e), _ptr(self.n), _ptr(self.stamp))
         return C.byref(self._s)
 
 
@@ -289,18 +291,39 @@ def nnf_evaluate(lv, nnf, prm, kb=-1, only_layer=-1, b=0, e=None, counter=None):
                                   b, e, _ptr(counter), _stream()), "vinp_nnf_evaluate")
 
 
-def propagate(lv, nin, nout, prm, step, sign, kb=-1, only_layer=-1, b=0, e=None, counter=None):
+class PassClock:
+    """Pass numbering of one ANN search for the R41 stale skip (host logic, as csrc/common.cuh):
+    evaluate = pass 0, then 1, 2, ... in schedule order; since(step, sign) = the index of the last
+    earlier propagation pass with that (step, sign) in the search, 0 if none."""
+
+    def __init__(self):
+        self.pass_id = 1
+        self.last = {}
+
+    def since(self, step, sign):
+        return self.last.get((step, sign), 0)
+
+    def tick(self, step=None, sign=None):  # step None: a random-search pass
+        if step is not None:
+            self.last[(step, sign)] = self.pass_id
+        self.pass_id += 1
+
+
+def propagate(lv, nin, nout, prm, step, sign, kb=-1, only_layer=-1, b=0, e=None, counter=None,
+              pass_id=1, since=0):
+    """pass_id / since: the R41 pass numbering (used only when both buffers carry stamps; counter
+    must then hold 2 int64: [0] evaluated, [1] skipped stale candidates)."""
     e = lv.n_targets if e is None else e
     _check(_lib.vinp_propagate(lv.struct(), nin.struct(), nout.struct(), C.byref(prm.struct()), step,
-                               sign, kb, only_layer, b, e, _ptr(counter), _stream()),
+                               sign, kb, only_layer, b, e, pass_id, since, _ptr(counter), _stream()),
            "vinp_propagate")
 
 
 def random_search(lv, nin, nout, prm, outer_code, pm_iter, kb=-1, only_layer=-1, b=0, e=None,
-                  counter=None):
+                  counter=None, pass_id=1):
     e = lv.n_targets if e is None else e
     _check(_lib.vinp_random_search(lv.struct(), nin.struct(), nout.struct(), C.byref(prm.struct()),
-                                   outer_code, pm_iter, kb, only_layer, b, e, _ptr(counter),
+                                   outer_code, pm_iter, kb, only_layer, b, e, pass_id, _ptr(counter),
                                    _stream()), "vinp_random_search")
 
 

@@ -80,7 +80,16 @@ def _from_orc(lv, f, nnf):
 
 def _count(counter, c):
     if counter is not None:
-        counter += int(c)
+        counter[0] += int(c)
+
+
+def _stamp(lv, nin, nout, b, e, pass_id):
+    """R41 stamps as the kernels write them (the oracle evaluates every candidate, so nothing is
+    skipped here: the stamps only travel through the driver's exchanges)."""
+    if nin.stamp is None:
+        return
+    ch = (nout.e[b:e] & 0xFFFFFFFF) != (nin.e[b:e] & 0xFFFFFFFF)
+    nout.stamp[b:e] = torch.where(ch, torch.full_like(nin.stamp[b:e], pass_id), nin.stamp[b:e])
 
 
 # ----------------------------------------------------------------------------- setup
@@ -172,18 +181,22 @@ def nnf_evaluate(lv, nnf, prm, kb=-1, only_layer=-1, b=0, e=None, counter=None):
     f = _to_orc(lv, nnf)
     _count(counter, orc.evaluate(ol, f, prm.lam, kb, only_layer, b, e))
     _from_orc(lv, f, nnf)
+    if nnf.stamp is not None:
+        nnf.stamp[b:e] = 0
 
 
-def propagate(lv, nin, nout, prm, step, sign, kb=-1, only_layer=-1, b=0, e=None, counter=None):
+def propagate(lv, nin, nout, prm, step, sign, kb=-1, only_layer=-1, b=0, e=None, counter=None,
+              pass_id=1, since=0):
     e = lv.n_targets if e is None else e
     ol = _OLevel(lv)
     fi, fo = _to_orc(lv, nin), _to_orc(lv, nout)
     _count(counter, orc.propagate(ol, fi, fo, prm.lam, step, sign, kb, only_layer, b, e))
     _from_orc(lv, fo, nout)
+    _stamp(lv, nin, nout, b, e, pass_id)
 
 
 def random_search(lv, nin, nout, prm, outer_code, pm_iter, kb=-1, only_layer=-1, b=0, e=None,
-                  counter=None):
+                  counter=None, pass_id=1):
     e = lv.n_targets if e is None else e
     ol = _OLevel(lv)
     fi, fo = _to_orc(lv, nin), _to_orc(lv, nout)
@@ -191,6 +204,7 @@ def random_search(lv, nin, nout, prm, outer_code, pm_iter, kb=-1, only_layer=-1,
     _count(counter, orc.random_search(ol, fi, fo, prm.lam, prm.seed, prm.rho, rmax, lv.level, outer_code,
                                       pm_iter, kb, only_layer, b, e))
     _from_orc(lv, fo, nout)
+    _stamp(lv, nin, nout, b, e, pass_id)
 
 
 def ann_search(lv, a, b, prm, outer_code, K, steps=(8, 4, 2, 1), kb=-1, only_layer=-1, counter=None,

@@ -46,4 +46,6 @@ def test_c_program_equals_oracle(tmp_path, orc):
     ref, st = orc.inpaint(v, m, 1, pm_iters=4, fixed_outer=3)
     assert np.array_equal(out, ref)
     pu = int(r.stdout.split("patch-updates")[1].split()[0])
-    assert pu == sum(st["patch_updates"])
+    stale = int(r.stdout.split("stale-skipped")[1].split()[0])
+    assert stale == sum(st["stale"])  # R41
+    assert pu + stale == sum(st["patch_updates"])

@@ -28,7 +28,7 @@ def test_invalid_arguments_are_reported_synchronously():
     assert st in (1, 4) and lib.vinp_last_error()
     # propagate needs two distinct NNF buffers
     st = lib.vinp_propagate(lv.struct(), nnf.struct(), nnf.struct(), C.byref(V.Params().struct()), 8, 1, -1,
-                            -1, 0, 0, None, None)
+                            -1, 0, 0, 1, 0, None, None)
     assert st == 1 and lib.vinp_last_error()
     # realignment: frames must be at least 2 x 2
     assert lib.vinp_affine_estimate(None, None, 1, 1, 3, 3, 20, 1e-4, 0, -1, None, None, None, None, 0, None) == 1

@@ -131,6 +131,7 @@ def test_aligned_inpainting_end_to_end(orc):
     ref = orc.unwarp(o_out, v, m, fwd)
     assert np.array_equal(out.cpu().numpy(), ref)
     assert [l["outer"] for l in stats.levels] == o_st["outer_iters"]
-    assert stats.total_patch_updates == sum(o_st["patch_updates"])
+    assert stats.total_patch_updates + stats.total_stale_skipped == sum(o_st["patch_updates"])
+    assert stats.total_stale_skipped == sum(o_st["stale"])
     # outside the occlusion the result is the input, bit for bit
     assert np.array_equal(out.cpu().numpy()[m == 0], v[m == 0])

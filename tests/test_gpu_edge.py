@@ -20,7 +20,8 @@ def _both(orc, v, m, levels, **kw):
     g = out.cpu().numpy()
     assert np.array_equal(g, ref)
     assert [l["outer"] for l in stats.levels] == st["outer_iters"]
-    assert stats.total_patch_updates == sum(st["patch_updates"])
+    assert stats.total_patch_updates + stats.total_stale_skipped == sum(st["patch_updates"])
+    assert stats.total_stale_skipped == sum(st["stale"])
     assert np.array_equal(g[m == 0], v[m == 0])
     return g, stats
 

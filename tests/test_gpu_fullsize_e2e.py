@@ -40,12 +40,15 @@ def test_whole_pipeline_full_size(orc, name):
                           max_outer=c.max_outer, lam=c.lam, seed=c.seed)
     report = dict(outer_gpu=[l["outer"] for l in stats.levels], outer_orc=st["outer_iters"],
                   pu_gpu=[l["patch_updates"] for l in stats.levels], pu_orc=st["patch_updates"],
+                  stale_gpu=[l["stale_skipped"] for l in stats.levels], stale_orc=st["stale"],
                   diff_voxels=int((g != ref).any(-1).sum()))
     print(name, report)
     for l in range(c.levels):
         assert stats.levels[l]["change_fixed"] == st["change_fixed"][l], ("stopping statistic", l + 1)
     assert report["outer_gpu"] == report["outer_orc"]
-    assert report["pu_gpu"] == report["pu_orc"]
+    # R41: evaluated + skipped stale = the oracle's count, and the skipped sets agree
+    assert report["stale_gpu"] == report["stale_orc"]
+    assert [a + b for a, b in zip(report["pu_gpu"], report["stale_gpu"])] == report["pu_orc"]
     assert report["diff_voxels"] == 0
 
 
@@ -89,7 +92,8 @@ def test_c5_level1_one_outer_iteration_every_slot(orc):
         setattr(host, name, getattr(lv, name).cpu())
     host.n_targets, host.n_holes, host.n_sources = nt, nh, lv.n_sources
     ol = OO._OLevel(host)
-    cnt = torch.zeros(1, dtype=torch.int64, device="cuda")
+    cnt = torch.zeros(2, dtype=torch.int64, device="cuda")  # evaluated, stale skipped (R41)
+    assert st.a.stamp is not None and st.b.stamp is not None
 
     def gpu(x):
         return OO._to_orc(host, V.NNF(x.e.cpu(), x.n.cpu()))
@@ -108,29 +112,39 @@ def test_c5_level1_one_outer_iteration_every_slot(orc):
     f_ref = f_in.copy()
     c_ref = orc.evaluate(ol, f_ref, prm.lam)
     equal(gpu(st.a), f_ref, "evaluate")
-    assert int(cnt) == c_ref
+    assert int(cnt[0]) == c_ref
     passes = 1
     total = c_ref
+    skipped = 0
+    clk = V.PassClock()
+    snaps = {}
     for k in range(1, ip.cfg.pm_iters + 1):
         sign = 1 if k % 2 == 1 else -1
         for s in ip.cfg.steps:
             f_in = gpu(st.a)
             cnt.zero_()
-            V.propagate(lv, st.a, st.b, prm, s, sign, counter=cnt)
+            V.propagate(lv, st.a, st.b, prm, s, sign, counter=cnt, pass_id=clk.pass_id,
+                        since=clk.since(s, sign))
+            clk.tick(s, sign)
             f_ref = f_in.copy()
-            c_ref = orc.propagate(ol, f_in, f_ref, prm.lam, s, sign)
+            stale = np.zeros(1, np.int64)
+            c_ref = orc.propagate(ol, f_in, f_ref, prm.lam, s, sign, prev=snaps.get((s, sign)), stale=stale)
+            snaps[(s, sign)] = f_in
             equal(gpu(st.b), f_ref, f"propagate k={k} s={s}")
-            assert int(cnt) == c_ref, ("propagate count", k, s)
+            assert int(cnt[1]) == int(stale[0]), ("stale count", k, s)
+            assert int(cnt[0]) + int(cnt[1]) == c_ref, ("propagate count", k, s)
             st.a, st.b = st.b, st.a
             passes += 1
             total += c_ref
+            skipped += int(stale[0])
         f_in = gpu(st.a)
         cnt.zero_()
-        V.random_search(lv, st.a, st.b, prm, 0, k, counter=cnt)
+        V.random_search(lv, st.a, st.b, prm, 0, k, counter=cnt, pass_id=clk.pass_id)
+        clk.tick()
         f_ref = f_in.copy()
         c_ref = orc.random_search(ol, f_in, f_ref, prm.lam, prm.seed, prm.rho, ol.rmax, 1, 0, k)
         equal(gpu(st.b), f_ref, f"random search k={k}")
-        assert int(cnt) == c_ref, ("random search count", k)
+        assert int(cnt[0]) == c_ref, ("random search count", k)
         st.a, st.b = st.b, st.a
         passes += 1
         total += c_ref
@@ -145,7 +159,9 @@ def test_c5_level1_one_outer_iteration_every_slot(orc):
     orc.reconstruct(ol, f_a, orc.WEIGHTED, -1, 0, nh, o_rgb, o_tex)
     err = max(np.abs(o_rgb - g_rgb).max(), np.abs(o_tex - g_tex).max())
     exact = float(np.mean(o_rgb == g_rgb))
-    print(f"c5 l1 outer iteration: {total} patch-updates, reconstruct max |err| {err:.2e}, exact {exact:.6f}")
+    print(f"c5 l1 outer iteration: {total} candidates ({skipped} stale, skipped on the GPU), "
+          f"reconstruct max |err| {err:.2e}, exact {exact:.6f}")
+    assert skipped > 0
     assert err <= 1e-3
     orc.commit(ol, o_rgb, o_tex, 0, nh)
     vb = lv.vox.view(torch.uint8).view(lv.N, 8).cpu().numpy()

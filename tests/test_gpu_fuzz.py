@@ -49,7 +49,8 @@ def test_pipeline_fuzz(orc, i):
     out, stats, _ = inpaint(v, m, cfg, device="cuda")
     assert np.array_equal(out.cpu().numpy(), ref), c
     assert [l["outer"] for l in stats.levels] == st["outer_iters"], c
-    assert stats.total_patch_updates == sum(st["patch_updates"]), c
+    assert stats.total_patch_updates + stats.total_stale_skipped == sum(st["patch_updates"]), c
+    assert stats.total_stale_skipped == sum(st["stale"]), c
 
 
 @pytest.mark.parametrize("i", range(6))

@@ -379,3 +379,72 @@ def test_driver_stop_decision_equals_oracle(orc):
         e = min(e, 2 ** 63 - 1)  # the statistic is an int64 on both sides
         k = rng.randint(1, 21)
         assert stop_now(e, nh, k, 20, rule) == orc.stop(e, nh, k, 20, rule), (e, nh, k, rule)
+
+
+# ------------------------------------------------------------------------- R41 stale candidates
+def _candidates(lv, f, s, step, sign):
+    """The propagation candidates of target slot s that are evaluated (Alg. 1 P:418-434 with R2,
+    R6): neighbour r = p + sg*step*e_axis in H~, shift v = phi(r) valid at p, v different from the
+    incumbent and every earlier candidate.  Returns [(rank, neighbour slot, v)]."""
+    p = int(lv.targets[s])
+    x, y, t = _xyz(lv, p)
+    seen = [_shift(f, s)]
+    out = []
+    order = [(sign, a) for a in range(3)] if sign else [(-1, a) for a in range(3)] + [(1, a) for a in range(3)]
+    for rank, (sg, ax) in enumerate(order, start=1):
+        r = [x, y, t]
+        r[ax] += sg * step
+        if not (0 <= r[0] < lv.W and 0 <= r[1] < lv.H and 0 <= r[2] < lv.T):
+            continue
+        rs = int(lv.slot[_lin(lv, *r)])
+        if rs < 0:
+            continue
+        v = _shift(f, rs)
+        if not _valid_shift(lv, p, v) or v in seen:
+            continue
+        seen.append(v)
+        out.append((rank, rs, v))
+    return out
+
+
+@pytest.mark.parametrize("sign_policy", [0, 1])
+def test_stale_candidates_brute_force(orc, sign_policy):
+    """R41 by brute force on a tiny level: a candidate whose neighbour holds the same shift as at
+    the previous pass with the same (step, sign) of the search is (i) counted exactly as the
+    oracle's stale count and (ii) never strictly better than the target's incumbent, which is
+    why the GPU may skip it without changing the NNF (strict improvement, R25)."""
+    from gen.synth import random_volume
+    v, m, _ = random_volume(22, 18, 9, seed=3, hole_frac=0.08)
+    rgb, occ = v.numpy(), m.numpy()
+    lv = _level(orc, rgb, occ, tex=orc.texture(rgb, occ, 1))
+    lam = 50
+    nt = len(lv.targets)
+    f = orc.NNF.empty(nt)
+    orc.init_random(lv, f, 1, 1, 0)
+    orc.evaluate(lv, f, lam)
+    snaps = {}
+    n_stale_total = 0
+    for k in range(1, 7):
+        sign = 0 if sign_policy else (1 if k % 2 else -1)
+        for step in (4, 2, 1):
+            prev = snaps.get((step, sign))
+            want = 0
+            for s in range(nt):
+                for rank, rs, cand in _candidates(lv, f, s, step, sign):
+                    if prev is not None and _shift(prev, rs) == cand:
+                        want += 1
+                        x, y, t = _xyz(lv, lv.targets[s])
+                        q = _lin(lv, x + cand[0], y + cand[1], t + cand[2])
+                        D, _ = orc.patch_ssd(lv, int(lv.targets[s]), q, lam)
+                        assert D >= int(f.D[s]), (k, step, s, rank)
+            g = f.copy()
+            st = np.zeros(1, np.int64)
+            orc.propagate(lv, f, g, lam, step, sign, prev=prev, stale=st)
+            assert int(st[0]) == want, (k, step)
+            n_stale_total += want
+            snaps[(step, sign)] = f
+            f = g
+        g = f.copy()
+        orc.random_search(lv, f, g, lam, 1, 0.5, lv.rmax, 1, 0, k)
+        f = g
+    assert n_stale_total > 0
