@@ -105,9 +105,125 @@ __global__ void k_upsample(LevelArgs c, const uint64_t* __restrict__ ce, LevelAr
 #ifndef VINP_PROP_FRAME_MAJOR
 #define VINP_PROP_FRAME_MAJOR 1
 #endif
+#ifndef VINP_PROP_SPARSE
+#define VINP_PROP_SPARSE 12  // warps with at most this many live propagation candidates: group path
+#endif
 #ifndef VINP_RS_SMALL
 #define VINP_RS_SMALL (148 * 32 * 8)  // random-search launches below this many targets: 8 per warp
 #endif
+
+// ------------------------------------------------------------------ pair evaluation by column groups
+// Random search and sparse propagation warps, evaluation by 5-lane column groups: lanes 5g..5g+4 (g < 6) evaluate one
+// (target, candidate) pair, lane k owning patch column dx = k - 2, so every row of a patch is one
+// 40-byte gather per group.  Pairs come from the warp's flattened candidate list (owner lane =
+// target, rank order); each group takes the next unassigned pair as soon as its own aborts or
+// completes.  Exact partial-distance elimination after every frame dt (25 voxels): the group sum
+// is all-reduced over its 5 lanes (3 shuffles) and checked against the owner's current minimum.
+__device__ __forceinline__ uint32_t sum5(uint32_t x, int base, int k) {
+  uint32_t s1 = x + __shfl_sync(kFull, x, base + (k + 1) % 5);
+  uint32_t s2 = s1 + __shfl_sync(kFull, s1, base + (k + 2) % 5);
+  return s2 + __shfl_sync(kFull, x, base + (k + 4) % 5);
+}
+
+// Evaluation of a warp's (candidate q, owner lane) pair list by 5-lane column groups: lanes
+// 5g..5g+4 (g < 6) evaluate one pair, lane k owning patch column dx = k - 2, so every row of a
+// patch is one 40-byte gather per group.  The owner lane holds its target (p, px, py, pt) and its
+// running best (bestD, bestq), initially the incumbent; pairs of one owner are in rank order.
+// Out-of-volume voxels of a border target contribute nothing (K = Omega).
+__device__ __forceinline__ void group_eval(const LevelArgs& a, const int2* pairs, const int P,
+                                           const int lane, const int p, const int px, const int py,
+                                           const int pt, const int lambda, uint32_t& bestD,
+                                           int& bestq) {
+  const int g = lane / 5, k = lane - 5 * (lane / 5), gbase = 5 * g, dx = k - 2;
+  const unsigned long long* v = reinterpret_cast<const unsigned long long*>(a.vox);
+  // Each 5-lane group g < 6 walks the warp's pair list on its own: one frame of its current pair
+  // per loop iteration, and as soon as the pair aborts or completes the group takes the next
+  // unassigned pair, so a surviving pair never holds other groups idle.  Sequential application
+  // in rank order with strict improvement (R25) equals the lexicographic minimum of (D, pair index)
+  // over {incumbent (D_inc, -1)} + candidates; a pair is dropped once its partial sum proves it
+  // cannot reach that minimum (partial > best D, or == best D with a later index): exact (R35).
+  int bestJ = -1;
+  int j = -1, dtc = -2, t = 0, pi = 0, ty = 0, tt = 0, sq = 0;
+  bool colok = false;
+  uint32_t accc = 0, acct = 0;
+  int next = 0;
+  const int gsrc = gbase < 30 ? gbase : 0;
+  for (;;) {
+    // hand out pairs to the groups that need one (in group order)
+    bool need = g < 6 && j < 0 && next < P;
+    unsigned nb = __ballot_sync(kFull, need && k == 0);
+    if (nb) {
+      int jj = next + __popc(nb & ((1u << gbase) - 1u));
+      bool take = need && jj < P;
+      int2 pr = take ? pairs[jj] : make_int2(0, lane);
+      int src = take ? pr.y : lane;
+      int npi = __shfl_sync(kFull, p, src), ntx = __shfl_sync(kFull, px, src);
+      int nty = __shfl_sync(kFull, py, src), ntt = __shfl_sync(kFull, pt, src);
+      if (take) {
+        j = jj;
+        t = pr.y;
+        sq = pr.x;
+        pi = npi;
+        ty = nty;
+        tt = ntt;
+        colok = (unsigned)(ntx + dx) < (unsigned)a.g.W;
+        dtc = -2;
+        accc = acct = 0;
+      }
+      next = min(P, next + __popc(nb));
+    }
+    bool active = j >= 0;
+    if (!__any_sync(kFull, active)) break;
+    // one frame of the current pair: all 10 gathers first, then the arithmetic
+    bool tok = active && colok && (unsigned)(tt + dtc) < (unsigned)a.g.T;
+    int ro[5];
+    bool okr[5];
+#pragma unroll
+    for (int r = 0; r < 5; ++r) {
+      ro[r] = dtc * a.g.HW + (r - 2) * a.g.W + dx;
+      okr[r] = tok && (unsigned)(ty + r - 2) < (unsigned)a.g.H;
+    }
+    uint64_t tv[5], sv[5];
+#pragma unroll
+    for (int r = 0; r < 5; ++r) {
+      tv[r] = __ldg(v + pi + (okr[r] ? ro[r] : 0));
+      sv[r] = __ldg(v + sq + (okr[r] ? ro[r] : 0));
+    }
+    uint32_t tD = __shfl_sync(kFull, bestD, active ? t : lane);
+    int tJ = __shfl_sync(kFull, bestJ, active ? t : lane);
+#pragma unroll
+    for (int r = 0; r < 5; ++r) {
+      uint64_t tw = okr[r] ? tv[r] : 0ull, sw = okr[r] ? sv[r] : 0ull;
+      uint32_t dc = __vabsdiffu4((uint32_t)tw, (uint32_t)sw);
+      uint32_t dtx = __vabsdiffu4((uint32_t)(tw >> 32), (uint32_t)(sw >> 32));
+      accc = __dp4a(dc, dc, accc);
+      acct = __dp4a(dtx, dtx, acct);
+    }
+    uint32_t tot = sum5(4u * accc + (uint32_t)lambda * acct, gsrc, k);
+    bool dead = active && (tot > tD || (tot == tD && j > tJ));
+    bool win = active && !dead && dtc == 2;
+    unsigned wb = __ballot_sync(kFull, win && k == 0);
+    while (wb) {  // apply this iteration's completed pairs (several may share an owner)
+      int src = __ffs(wb) - 1;
+      wb &= wb - 1u;
+      uint32_t D = __shfl_sync(kFull, tot, src);
+      int jw = __shfl_sync(kFull, j, src);
+      int qw = __shfl_sync(kFull, sq, src);
+      int own = __shfl_sync(kFull, t, src);
+      if (lane == own && (D < bestD || (D == bestD && jw < bestJ))) {
+        bestD = D;
+        bestJ = jw;
+        bestq = qw;
+      }
+    }
+    if (active) {
+      if (dead || dtc == 2)
+        j = -1;
+      else
+        ++dtc;
+    }
+  }
+}
 
 // ------------------------------------------------------------------ thread-per-target SSD
 // Used where candidates are spatially coherent (evaluate, propagation): lane l of a warp owns
@@ -296,6 +412,40 @@ __global__ void __launch_bounds__(256, VINP_PROP_MINB) k_propagate(LevelArgs a, 
   uint32_t bestD = e_D(inc);
   int bestq = q0;
   unsigned cnt = 0;
+#if VINP_PROP_SPARSE > 0
+  {
+    // Sparse warp (few live candidates, typical once the R41 skip has removed the stale ones):
+    // the warp's (candidate, owner) pairs are evaluated by 5-lane column groups, six at a time,
+    // instead of by their owner lanes with the other lanes idle.  Same rank order, same exact
+    // early abort, same result.
+    int incl = ncand;
+#pragma unroll
+    for (int d = 1; d < 32; d <<= 1) {
+      int y = __shfl_up_sync(kFull, incl, d);
+      if ((threadIdx.x & 31) >= d) incl += y;
+    }
+    const int P = __shfl_sync(kFull, incl, 31);
+    if (P <= VINP_PROP_SPARSE) {  // warp-uniform
+      __shared__ int2 s_pairs[256 / 32][VINP_PROP_SPARSE];
+      int2* pairs = s_pairs[threadIdx.x >> 5];
+#pragma unroll
+      for (int c = 0; c < NCMAX; ++c)
+        if (c < ncand) pairs[incl - ncand + c] = make_int2(cq[c], threadIdx.x & 31);
+      __syncwarp();
+      group_eval(a, pairs, P, threadIdx.x & 31, p, px, py, pt, lambda, bestD, bestq);
+      if (have) {
+        eout[s] = pack_e(bestD, bestq);
+        if (sout) sout[s] = bestq != q0 ? (uint8_t)pass : __ldg(sin + s);
+      }
+      nstale = __reduce_add_sync(kFull, nstale);
+      if ((threadIdx.x & 31) == 0) {
+        flush_count(counter, (unsigned)P);
+        if (counter && nstale) flush_count(counter + 1, nstale);
+      }
+      return;
+    }
+  }
+#endif
   bool full = act && kb < 0 && px >= 2 && px < a.g.W - 2 && py >= 2 && py < a.g.H - 2 && pt >= 2 &&
               pt < a.g.T - 2;
   bool allfull = __all_sync(kFull, full || !act);
@@ -573,18 +723,6 @@ struct Radii {
   int M;
 };
 
-// Random search, evaluation by 5-lane column groups: lanes 5g..5g+4 (g < 6) evaluate one
-// (target, candidate) pair, lane k owning patch column dx = k - 2, so every row of a patch is one
-// 40-byte gather per group.  Pairs come from the warp's flattened candidate list (owner lane =
-// target, rank order); each group takes the next unassigned pair as soon as its own aborts or
-// completes.  Exact partial-distance elimination after every frame dt (25 voxels): the group sum
-// is all-reduced over its 5 lanes (3 shuffles) and checked against the owner's current minimum.
-__device__ __forceinline__ uint32_t sum5(uint32_t x, int base, int k) {
-  uint32_t s1 = x + __shfl_sync(kFull, x, base + (k + 1) % 5);
-  uint32_t s2 = s1 + __shfl_sync(kFull, s1, base + (k + 2) % 5);
-  return s2 + __shfl_sync(kFull, x, base + (k + 4) % 5);
-}
-
 template <int NC, int WPB, int TPW>
 __global__ void __launch_bounds__(32 * WPB, VINP_MINB * 8 / WPB) k_random_search(
     LevelArgs a, const uint64_t* __restrict__ ein, uint64_t* __restrict__ eout,
@@ -640,95 +778,7 @@ __global__ void __launch_bounds__(32 * WPB, VINP_MINB * 8 / WPB) k_random_search
   __syncwarp();
   uint32_t bestD = e_D(inc);
   int bestq = e_q(inc);
-  const int g = lane / 5, k = lane - 5 * (lane / 5), gbase = 5 * g, dx = k - 2;
-  const unsigned long long* v = reinterpret_cast<const unsigned long long*>(a.vox);
-  // Each 5-lane group g < 6 walks the warp's pair list on its own: one frame of its current pair
-  // per loop iteration, and as soon as the pair aborts or completes the group takes the next
-  // unassigned pair, so a surviving pair never holds other groups idle.  Sequential application
-  // in rank order with strict improvement (R25) equals the lexicographic minimum of (D, pair index)
-  // over {incumbent (D_inc, -1)} + candidates; a pair is dropped once its partial sum proves it
-  // cannot reach that minimum (partial > best D, or == best D with a later index): exact (R35).
-  int bestJ = -1;
-  int j = -1, dtc = -2, t = 0, pi = 0, ty = 0, tt = 0, sq = 0;
-  bool colok = false;
-  uint32_t accc = 0, acct = 0;
-  int next = 0;
-  const int gsrc = gbase < 30 ? gbase : 0;
-  for (;;) {
-    // hand out pairs to the groups that need one (in group order)
-    bool need = g < 6 && j < 0 && next < P;
-    unsigned nb = __ballot_sync(kFull, need && k == 0);
-    if (nb) {
-      int jj = next + __popc(nb & ((1u << gbase) - 1u));
-      bool take = need && jj < P;
-      int2 pr = take ? pairs[jj] : make_int2(0, lane);
-      int src = take ? pr.y : lane;
-      int npi = __shfl_sync(kFull, p, src), ntx = __shfl_sync(kFull, px, src);
-      int nty = __shfl_sync(kFull, py, src), ntt = __shfl_sync(kFull, pt, src);
-      if (take) {
-        j = jj;
-        t = pr.y;
-        sq = pr.x;
-        pi = npi;
-        ty = nty;
-        tt = ntt;
-        colok = (unsigned)(ntx + dx) < (unsigned)a.g.W;
-        dtc = -2;
-        accc = acct = 0;
-      }
-      next = min(P, next + __popc(nb));
-    }
-    bool active = j >= 0;
-    if (!__any_sync(kFull, active)) break;
-    // one frame of the current pair: all 10 gathers first, then the arithmetic
-    bool tok = active && colok && (unsigned)(tt + dtc) < (unsigned)a.g.T;
-    int ro[5];
-    bool okr[5];
-#pragma unroll
-    for (int r = 0; r < 5; ++r) {
-      ro[r] = dtc * a.g.HW + (r - 2) * a.g.W + dx;
-      okr[r] = tok && (unsigned)(ty + r - 2) < (unsigned)a.g.H;
-    }
-    uint64_t tv[5], sv[5];
-#pragma unroll
-    for (int r = 0; r < 5; ++r) {
-      tv[r] = __ldg(v + pi + (okr[r] ? ro[r] : 0));
-      sv[r] = __ldg(v + sq + (okr[r] ? ro[r] : 0));
-    }
-    uint32_t tD = __shfl_sync(kFull, bestD, active ? t : lane);
-    int tJ = __shfl_sync(kFull, bestJ, active ? t : lane);
-#pragma unroll
-    for (int r = 0; r < 5; ++r) {
-      uint64_t tw = okr[r] ? tv[r] : 0ull, sw = okr[r] ? sv[r] : 0ull;
-      uint32_t dc = __vabsdiffu4((uint32_t)tw, (uint32_t)sw);
-      uint32_t dtx = __vabsdiffu4((uint32_t)(tw >> 32), (uint32_t)(sw >> 32));
-      accc = __dp4a(dc, dc, accc);
-      acct = __dp4a(dtx, dtx, acct);
-    }
-    uint32_t tot = sum5(4u * accc + (uint32_t)lambda * acct, gsrc, k);
-    bool dead = active && (tot > tD || (tot == tD && j > tJ));
-    bool win = active && !dead && dtc == 2;
-    unsigned wb = __ballot_sync(kFull, win && k == 0);
-    while (wb) {  // apply this iteration's completed pairs (several may share an owner)
-      int src = __ffs(wb) - 1;
-      wb &= wb - 1u;
-      uint32_t D = __shfl_sync(kFull, tot, src);
-      int jw = __shfl_sync(kFull, j, src);
-      int qw = __shfl_sync(kFull, sq, src);
-      int own = __shfl_sync(kFull, t, src);
-      if (lane == own && (D < bestD || (D == bestD && jw < bestJ))) {
-        bestD = D;
-        bestJ = jw;
-        bestq = qw;
-      }
-    }
-    if (active) {
-      if (dead || dtc == 2)
-        j = -1;
-      else
-        ++dtc;
-    }
-  }
+  group_eval(a, pairs, P, lane, p, px, py, pt, lambda, bestD, bestq);
   if (have) {
     eout[s] = pack_e(bestD, bestq);
     if (sout) sout[s] = bestq != e_q(inc) ? (uint8_t)pass : __ldg(sin + s);
