@@ -80,8 +80,11 @@ __device__ __forceinline__ void recon_hole(const ReconArgs& a, const LaneVox& LV
   bool n125 = true;
   const int* off = LV.off;
   bool cand[4];
+  // interior hole (the usual case): every voxel of N_p is in the volume, no per-voxel test
+  const bool interior = px >= 2 && px < a.g.W - 2 && py >= 2 && py < a.g.H - 2 && pt >= 2 && pt < a.g.T - 2;
 #pragma unroll
-  for (int i = 0; i < 4; ++i) cand[i] = LV.real[i] && inside(a.g, px + LV.dx[i], py + LV.dy[i], pt + LV.dt[i]);
+  for (int i = 0; i < 4; ++i)
+    cand[i] = LV.real[i] && (interior || inside(a.g, px + LV.dx[i], py + LV.dy[i], pt + LV.dt[i]));
   if (layer_j >= 0) {
 #pragma unroll
     for (int i = 0; i < 4; ++i) cand[i] = cand[i] && a.layer[p + (cand[i] ? off[i] : 0)] < layer_j;
@@ -230,22 +233,29 @@ __device__ __forceinline__ void recon_hole(const ReconArgs& a, const LaneVox& LV
       }
     }
   }
-  // exact sums: per-lane partials (< 2^46) split into two 23-bit halves, each summed by REDUX
-  int64_t S = 0, N[5] = {0, 0, 0, 0, 0};
+  // exact sums: w <= 2^36 is split as w = wh 2^32 + wl (wh <= 16); per channel the low part
+  // accumulates in 64 bits (one wide multiply-add per contributor) and the high part in 32 bits;
+  // the per-lane partials (< 2^46) are then summed over the warp as two 23-bit halves by REDUX
+  uint64_t Sl = 0, Nl[5] = {0, 0, 0, 0, 0};
+  uint32_t Sh = 0, Nh[5] = {0, 0, 0, 0, 0};
 #pragma unroll
   for (int i = 0; i < 4; ++i) {
-    if (!w[i]) continue;
-    uint64_t x = val[i];
-    S += w[i];
-    N[0] += w[i] * (int64_t)(x & 255);
-    N[1] += w[i] * (int64_t)((x >> 8) & 255);
-    N[2] += w[i] * (int64_t)((x >> 16) & 255);
-    N[3] += w[i] * (int64_t)((x >> 32) & 255);
-    N[4] += w[i] * (int64_t)((x >> 40) & 255);
-  }
-  S = warp_sum46(S);
+    const uint32_t wl = (uint32_t)w[i], wh = (uint32_t)((uint64_t)w[i] >> 32);
+    const uint64_t x = val[i];
+    const uint32_t c0 = (uint32_t)x, c1 = (uint32_t)(x >> 32);
+    const uint32_t v[5] = {c0 & 255, (c0 >> 8) & 255, (c0 >> 16) & 255, c1 & 255, (c1 >> 8) & 255};
+    Sl += wl;
+    Sh += wh;
 #pragma unroll
-  for (int c = 0; c < 5; ++c) N[c] = warp_sum46(N[c]);
+    for (int c = 0; c < 5; ++c) {
+      Nl[c] += (uint64_t)wl * v[c];
+      Nh[c] += wh * v[c];
+    }
+  }
+  int64_t S = warp_sum46((int64_t)(Sl + ((uint64_t)Sh << 32)));
+  int64_t N[5];
+#pragma unroll
+  for (int c = 0; c < 5; ++c) N[c] = warp_sum46((int64_t)(Nl[c] + ((uint64_t)Nh[c] << 32)));
   if (lane < 5) {
     int64_t Nc = lane == 0 ? N[0] : lane == 1 ? N[1] : lane == 2 ? N[2] : lane == 3 ? N[3] : N[4];
     float o = (float)__ddiv_rn((double)Nc, (double)S);
