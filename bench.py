@@ -27,6 +27,8 @@ sys.path.insert(0, ROOT)
 B_PU, B_TP, B_HOLE = 625, 29, 662  # algorithmic bytes: per patch-update / target-pass / hole
 CPU_SAMPLE = (24, 38, 4)  # oracle cpu_baseline sample: frames, first frame, PM iterations (~10-30 s)
 REF_SAMPLE = (12, 44, 2)  # --impl reference step: a smaller sample so W+K steps finish in minutes
+ONE_CORE_SAMPLE = (8, 46, 1)  # the oracle on one host core (OMP_NUM_THREADS=1): ~10 s
+CPU_FULL = os.path.join(ROOT, "profiles", "r02_cpu_full_outer.json")  # written by `bench.py --cpu-full`
 
 
 def _peaks():
@@ -158,9 +160,20 @@ def main():
     ap.add_argument("--no-cpu", action="store_true")
     ap.add_argument("--no-extra", action="store_true",
                     help="only the timed steps (no per-level / roofline / e2e / cpu runs): for ncu launch lists")
+    ap.add_argument("--cpu-full", action="store_true",
+                    help="time the oracle on one whole level-1 outer iteration of the config (all host "
+                         "cores; several minutes) and write profiles/r02_cpu_full_outer.json")
+    ap.add_argument("--one-core-sample", action="store_true", help=argparse.SUPPRESS)
     args = ap.parse_args()
     if args.impl == "reference":
         return run_reference(args)
+    if args.one_core_sample:  # child of the cpu_baseline leg, run with OMP_NUM_THREADS=1
+        frames, t0, iters = ONE_CORE_SAMPLE
+        pu_c, s_c, thr = oracle_sample(args.config, frames, t0, iters)
+        print(json.dumps({"pu": pu_c, "s": s_c, "threads": thr}))
+        return 0
+    if args.cpu_full:
+        return cpu_full(args.config)
 
     import torch
     import torch.distributed as dist
@@ -264,6 +277,22 @@ def main():
         cpu = {"value": pu_c / s_c, "unit": "patch-updates/s", "cores": thr, "kind": "oracle",
                "sample": f"{args.config} frames [{t0},{t0 + frames}) level 1: evaluate + {iters} PM iterations "
                          f"from random init ({pu_c} patch-updates in {s_c:.1f} s)"}
+        try:  # the same oracle on one host core, on a smaller sample
+            env = dict(os.environ, OMP_NUM_THREADS="1")
+            r = subprocess.run([sys.executable, os.path.abspath(__file__), "--one-core-sample", "--config",
+                                args.config], capture_output=True, text=True, env=env, timeout=600)
+            o = json.loads(r.stdout.strip().splitlines()[-1])
+            f1, t1, i1 = ONE_CORE_SAMPLE
+            cpu["one_core"] = {"value": o["pu"] / o["s"], "cores": o["threads"],
+                               "sample": f"{args.config} frames [{t1},{t1 + f1}) level 1: evaluate + {i1} PM "
+                                         f"iteration from random init ({o['pu']} patch-updates in {o['s']:.1f} s)"}
+        except Exception as ex_:  # reported, never fatal
+            cpu["one_core"] = {"error": str(ex_)[:200]}
+        try:  # recorded by `bench.py --cpu-full` on a GPU box's host (not re-measured here)
+            with open(CPU_FULL) as f:
+                cpu["full_outer_iteration_recorded"] = json.load(f)
+        except Exception:
+            pass
 
     if rank == 0:
         line = {"metric": "PatchMatch patch-updates/sec", "value": value, "unit": "patch-updates/s",
@@ -360,14 +389,83 @@ def measure_roofline(ip, v, m, dev):
             traffic = json.load(f).get(dom)
     except Exception:
         pass
+    # DRAM fraction: the ncu-measured DRAM bytes of one launch (cold caches: an upper bound on the
+    # steady state) over this run's average launch time; the model `frac` charges 625 B to every
+    # patch-update wherever it is served from (L1/L2 reuse can push it above 1)
+    dram_frac = None if not traffic else round(traffic / (a["ms"] / a["launches"] / 1000.0) / 1e9 / peak, 4)
     return {"kernel": f"vinp_{dom}", "bound": "hbm", "achieved": round(achieved, 1), "peak": peak,
-            "peak_kind": kind, "unit": "GB/s", "frac": round(achieved / peak, 4),
+            "peak_kind": kind, "unit": "GB/s", "frac": round(achieved / peak, 4), "dram_frac": dram_frac,
             "traffic": traffic, "bytes_per_launch": a["bytes"] / a["launches"],
             "avg_launch_ms": a["ms"] / a["launches"], "share_of_step": round(a["ms"] / tot, 4),
             "kernels": kernels, "_step_bytes": int(sum(x["bytes"] for x in agg.values())),
             "by_level": {k: {"ms": round(x["ms"], 2), "GB/s": round(x["bytes"] / (x["ms"] / 1000) / 1e9, 1),
                              "launches": x["launches"], "patch_updates": x["pu"]}
                          for k, x in sorted(per_level.items())}}
+
+
+def cpu_full(name):
+    """The oracle (all host cores) on one whole level-1 outer iteration of config `name`, from the
+    state Alg. 4 reaches there (GPU pipeline down to level 1, then the oracle takes over): evaluate,
+    K PatchMatch iterations (every candidate evaluated: the oracle has no R41 skip) and the weighted
+    reconstruction.  Writes CPU_FULL and prints it."""
+    import numpy as np
+    import torch
+    import oracle.oracle as orc
+    from gen.synth import generate, CONFIGS
+    from paper_1503_05528_b200 import Inpainter, vinp as V
+    from paper_1503_05528_b200.driver import stop_now
+    c = CONFIGS[name]
+    v, m, _ = generate(name, device="cuda")
+    ip = Inpainter(c.W, c.H, c.T, _cfg(name), "cuda")
+    ip.load(v, m)
+    ip.onion_peel()
+    for l in range(c.levels, 1, -1):  # Alg. 4 down to the first outer iteration of level 1
+        s_, f_ = ip.states[l - 1], ip.states[l - 2]
+        k = 0
+        while True:
+            s_.prev_rgb.copy_(s_.cur_rgb)
+            ip.ann_search(s_, k)
+            ip.reconstruct(s_, V.WEIGHTED)
+            ip.change.zero_()
+            V.change_l1(s_.cur_rgb[:s_.lv.n_holes], s_.prev_rgb[:s_.lv.n_holes], ip.change)
+            k += 1
+            if stop_now(int(ip.change.item()), s_.lv.n_holes, k, c.max_outer):
+                break
+        V.nnf_upsample(s_.lv, s_.a, f_.lv, f_.a, ip.prm)
+        ip.reconstruct(f_, V.UNWEIGHTED)
+    st = ip.states[0]
+    lv = st.lv
+    nt = lv.n_targets
+    vb = lv.vox.view(torch.uint8).view(c.T, c.H, c.W, 8).cpu().numpy()
+    occ = (lv.flags.view(c.T, c.H, c.W) & 1).cpu().numpy()
+    olv = orc.Level(np.ascontiguousarray(vb[..., :3]), np.ascontiguousarray(vb[..., 4:6]), occ)
+    assert len(olv.targets) == nt
+    e = st.a.e[:nt].cpu().numpy().view(np.uint64)
+    q = (e & np.uint64(0xFFFFFFFF)).astype(np.int64)
+    p = olv.targets.astype(np.int64)
+    f = orc.NNF.empty(nt)
+    f.dx[:nt] = q % c.W - p % c.W
+    f.dy[:nt] = (q // c.W) % c.H - (p // c.W) % c.H
+    f.dt[:nt] = q // (c.W * c.H) - p // (c.W * c.H)
+    del ip, v, m
+    torch.cuda.empty_cache()
+    t = time.perf_counter()
+    f, cnt = orc.ann_search(olv, f, c.lam, c.seed, 1, 0, c.pm_iters)
+    t_pm = time.perf_counter() - t
+    t = time.perf_counter()
+    orc.reconstruct(olv, f, orc.WEIGHTED)
+    t_rec = time.perf_counter() - t
+    threads = int(os.environ.get("OMP_NUM_THREADS", os.cpu_count() or 1))
+    res = {"config": name, "level": 1, "what": f"evaluate + {c.pm_iters} PatchMatch iterations + weighted "
+                                             "reconstruction, first level-1 outer iteration of Alg. 4",
+           "patch_updates": int(cnt), "s_patchmatch": round(t_pm, 2), "s_reconstruct": round(t_rec, 2),
+           "value": int(cnt) / t_pm, "unit": "patch-updates/s", "cores": threads, "kind": "oracle",
+           "host": os.uname().nodename}
+    os.makedirs(os.path.dirname(CPU_FULL), exist_ok=True)
+    with open(CPU_FULL, "w") as fh:
+        json.dump(res, fh, indent=1)
+    print(json.dumps(res), flush=True)
+    return 0
 
 
 if __name__ == "__main__":
