@@ -87,7 +87,7 @@ class Clocks:
                 "reasons": sorted(reasons), "samples": len(self.rows)}
 
 
-def _cfg(name, exchange="allgather"):
+def _cfg(name, exchange="halo"):
     from gen.synth import CONFIGS
     from paper_1503_05528_b200 import Config
     c = CONFIGS[name]
@@ -154,8 +154,9 @@ def main():
     ap.add_argument("--warmup", type=int, default=3)
     ap.add_argument("--impl", default="vinp", choices=["vinp", "reference"])
     ap.add_argument("--config", default="c5")
-    ap.add_argument("--exchange", default="allgather", choices=["allgather", "halo"],
-                    help="multi-GPU NNF / hole-value exchange (halo = NEXT #4 point-to-point, N > 1 only)")
+    ap.add_argument("--exchange", default="halo", choices=["allgather", "halo"],
+                    help="multi-GPU NNF / hole-value exchange (halo = NEXT #4 point-to-point of the rows each "
+                         "rank reads; levels below Config.replicate_below targets run replicated), N > 1 only")
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--no-cpu", action="store_true")
     ap.add_argument("--no-extra", action="store_true",

@@ -3,15 +3,17 @@ final unwarp (NEXT #1, `Config(align=True)`).
 
 Host logic only: which kernel runs on which level, the onion-peel loop (Alg. 3), the stopping
 rule (R19) and, under torch.distributed, the target-slab partition and the exchanges between
-passes (all-gather by default, halo point-to-point with `exchange="halo"`).  Every
-arithmetic step runs in libvinp's kernels.
+passes.  Every arithmetic step runs in libvinp's kernels.
 
 Multi-GPU: every rank holds the full pyramid; the sorted target list (and hole list) of a level is
-cut into W contiguous equal-count slabs; after every pass that a later pass reads, the NNF slabs
-are all-gathered; after reconstruction the fp32 hole values are all-gathered and committed on
-every rank; the change e is an exact int64 all-reduce.  Because every pass is a Jacobi pass whose
-candidates are drawn from counter-based Philox streams keyed on the voxel, the result is
-bit-identical for any number of ranks.  The onion peel (coarsest level only) runs replicated.
+cut into W contiguous equal-count slabs.  After every pass that a later pass reads, each rank
+receives the NNF rows (entries and R41 stamps) its next pass reads: by default only those rows,
+point to point (`exchange="halo"`, NEXT #4 first stage), or every slab (`exchange="allgather"`).
+After reconstruction the fp32 hole values are exchanged the same way and committed; the change e
+is an exact int64 all-reduce.  Levels with fewer than `replicate_below` targets (the coarse ones)
+and the onion peel run replicated on every rank, with no exchange, and are counted once.  Because
+every pass is a Jacobi pass whose candidates are drawn from counter-based Philox streams keyed on
+the voxel, the result is bit-identical for any number of ranks.
 """
 from __future__ import annotations
 
@@ -41,7 +43,10 @@ class Config:
     align_levels: int = 3       # R36: estimation pyramid levels
     align_iters: int = 20       # R38: IRLS iterations per level
     align_tol: float = 1e-4     # R38: update-norm stop
-    exchange: str = "allgather"  # multi-GPU: "allgather" every pass, or "halo" (NEXT #4, P2P)
+    exchange: str = "halo"      # multi-GPU: "halo" (NEXT #4: the rows a rank reads, P2P) or "allgather"
+    # multi-GPU: a level with fewer targets than this runs replicated on every rank (no exchange;
+    # its work counted once): a coarse level split W ways is launch- and exchange-bound
+    replicate_below: int = 1 << 21
     stop_rule: int = 0          # 0: R19 e = ||u_H - v_H||_1 / (3|H|); 1: literal P:988 ||.||_2 / (3|H|)
     skip_stale: bool = True     # R41: exact skip of stale propagation candidates (NNF unchanged)
 
@@ -311,6 +316,10 @@ class Inpainter:
                 self.ex.gather(st.cur_tex, n)
                 self.V.commit(lv, st.cur_rgb, st.cur_tex, layer_j, 0, n)
 
+    def replicated(self, l: int) -> bool:
+        """Level l runs replicated on every rank (multi-GPU only): fewer than replicate_below targets."""
+        return self.ex.world > 1 and self.states[l - 1].lv.n_targets < self.cfg.replicate_below
+
     # ------------------------------------------------------------------ Alg. 3 onion peel
     def onion_peel(self):
         """Alg. 3, replicated on every rank: one native call (per-layer index lists, all passes)."""
@@ -354,21 +363,24 @@ class Inpainter:
         e_on = ev(); e_on.record()
         onion_pu = self.counter.clone()  # replicated work: counted once (rank 0) in the job total
         snaps = {}  # counter after each level (device tensors: no extra host syncs)
+        repl = {l: self.replicated(l) for l in range(1, L + 1)}
         for l in range(L, 0, -1):
             st = self.states[l - 1]
             lv = st.lv
+            rp = repl[l]
             k = 0
             changes = []
             while True:
                 st.prev_rgb.copy_(st.cur_rgb)
                 st.prev_tex.copy_(st.cur_tex)
-                self.ann_search(st, k)
-                self.reconstruct(st, V.WEIGHTED)
+                self.ann_search(st, k, replicated=rp)
+                self.reconstruct(st, V.WEIGHTED, replicated=rp)
                 self.change.zero_()
-                hb, he = self.ex.slab(lv.n_holes)
+                hb, he = (0, lv.n_holes) if rp else self.ex.slab(lv.n_holes)
                 chg = self.V.change_l2 if cfg.stop_rule == 1 else self.V.change_l1
                 chg(st.cur_rgb[hb:he], st.prev_rgb[hb:he], self.change)
-                self.ex.allreduce_sum(self.change)
+                if not rp:
+                    self.ex.allreduce_sum(self.change)
                 k += 1
                 if cfg.fixed_outer > 0:
                     changes.append(self.change.clone())  # read once at the end (no sync here)
@@ -381,17 +393,19 @@ class Inpainter:
                         break
             self.stats.levels[l - 1]["change_fixed"] = changes
             if l == 1:
-                self.reconstruct(st, V.BEST_PATCH, full=True)  # Eq. 6; every rank gets u
+                self.reconstruct(st, V.BEST_PATCH, full=True, replicated=rp)  # Eq. 6; every rank gets u
             else:
-                if self.halo:  # upsampling reads the coarse NNF of any frame of the fine slab
+                if self.halo and not rp:  # upsampling reads the coarse NNF of any frame of the fine slab
                     self.ex.gather(st.a.e, lv.n_targets)
                     self.ex.gather(st.a.n, lv.n_targets)
                 f = self.states[l - 2]
-                fb, fe = self.ex.slab(f.lv.n_targets)
+                frp = repl[l - 1]
+                fb, fe = (0, f.lv.n_targets) if frp else self.ex.slab(f.lv.n_targets)
                 self.V.nnf_upsample(lv, st.a, f.lv, f.a, self.prm, fb, fe)
-                self.ex.gather(f.a.e, f.lv.n_targets)
-                self.ex.gather(f.a.n, f.lv.n_targets)
-                self.reconstruct(f, V.UNWEIGHTED)  # R20
+                if not frp:
+                    self.ex.gather(f.a.e, f.lv.n_targets)
+                    self.ex.gather(f.a.n, f.lv.n_targets)
+                self.reconstruct(f, V.UNWEIGHTED, replicated=frp)  # R20
             e1 = ev(); e1.record()
             marks[l] = (e0, e1)
             snaps[l] = self.counter.clone()
@@ -400,7 +414,7 @@ class Inpainter:
         t_all1 = ev(); t_all1.record()
         if timing:
             torch.cuda.synchronize()
-            for l, (a, b) in marks.items():
+            for l, (a, b) in marks.items():  # noqa: B007
                 self.stats.levels[l - 1]["ms"] = a.elapsed_time(b)
             self.stats.total_ms = t_all0.elapsed_time(t_all1)
             self.stats.onion_ms = t_all0.elapsed_time(e_on)
@@ -412,8 +426,11 @@ class Inpainter:
             per.append(snaps[l] - prev)
             prev = snaps[l]
         per = torch.stack(per)  # [level (coarsest first), (evaluated, stale)]
-        if self.ex.rank != 0:
+        if self.ex.rank != 0:  # replicated work (onion peel, replicated levels) counted by rank 0 only
             per[0] -= onion_pu
+            for i, l in enumerate(range(L, 0, -1)):
+                if repl[l]:
+                    per[i] = 0
         self.ex.allreduce_sum(per)
         per = per.tolist()
         for d in self.stats.levels:  # the stopping statistic of every outer iteration (x 2^20)

@@ -309,10 +309,17 @@ class PassClock:
         self.pass_id += 1
 
 
+def _counter2(counter, nnf):
+    """With R41 stamps the library adds skipped stale candidates to counter[1]."""
+    if counter is not None and nnf.stamp is not None and counter.numel() < 2:
+        raise VinpError("stamped NNF buffers need a 2-element counter (evaluated, stale)")
+
+
 def propagate(lv, nin, nout, prm, step, sign, kb=-1, only_layer=-1, b=0, e=None, counter=None,
               pass_id=1, since=0):
     """pass_id / since: the R41 pass numbering (used only when both buffers carry stamps; counter
     must then hold 2 int64: [0] evaluated, [1] skipped stale candidates)."""
+    _counter2(counter, nin)
     e = lv.n_targets if e is None else e
     _check(_lib.vinp_propagate(lv.struct(), nin.struct(), nout.struct(), C.byref(prm.struct()), step,
                                sign, kb, only_layer, b, e, pass_id, since, _ptr(counter), _stream()),
@@ -329,6 +336,7 @@ def random_search(lv, nin, nout, prm, outer_code, pm_iter, kb=-1, only_layer=-1,
 
 def ann_search(lv, a, b, prm, outer_code, K, steps=(8, 4, 2, 1), kb=-1, only_layer=-1, counter=None,
                sign_policy=0):
+    _counter2(counter, a)
     st = (C.c_int32 * len(steps))(*steps)
     _check(_lib.vinp_ann_search(lv.struct(), a.struct(), b.struct(), C.byref(prm.struct()), outer_code,
                                 K, st, len(steps), sign_policy, kb, only_layer, _ptr(counter), _stream()),
@@ -340,6 +348,7 @@ def onion_peel(lv, a, b, prm, K, n_layers, out_rgb, out_tex, steps=(8, 4, 2, 1),
     nbytes = int(_lib.vinp_onion_ws_bytes(lv.struct()))
     if ws is None or ws.numel() < nbytes:
         ws = torch.empty(nbytes, dtype=torch.uint8, device=lv.device)
+    _counter2(counter, a)
     st = (C.c_int32 * len(steps))(*steps)
     _check(_lib.vinp_onion_peel(lv.struct(), a.struct(), b.struct(), C.byref(prm.struct()), K, st,
                                 len(steps), sign_policy, n_layers, _ptr(out_rgb), _ptr(out_tex), _ptr(counter),

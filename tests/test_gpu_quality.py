@@ -33,7 +33,7 @@ def _quality(name, max_targets=None, steps=(8, 4, 2, 1), sign_policy=0):
     st = ip.states[0]
     lv = st.lv
     n = lv.n_targets if max_targets is None else min(lv.n_targets, max_targets)
-    cnt = torch.zeros(1, dtype=torch.int64, device="cuda")
+    cnt = torch.zeros(2, dtype=torch.int64, device="cuda")  # stamped buffers: evaluated, stale (R41)
     V.ann_search(lv, st.a, st.b, ip.prm, 0, c.pm_iters, tuple(steps), counter=cnt, sign_policy=sign_policy)
     bf = V.NNF.alloc(lv.n_targets, "cuda")
     V.brute_force_tc(lv, bf, ip.prm, 0, n)  # exact; bit-identical to the CUDA-core form (tests)
@@ -47,7 +47,7 @@ def _quality(name, max_targets=None, steps=(8, 4, 2, 1), sign_policy=0):
     d_pm = (Dp / (4 * npm)).mean().item()
     d_bf = (Db / (4 * nbf)).mean().item()
     same = (st.a.e[:n] == bf.e[:n]).double().mean().item()
-    return dict(config=name, steps=list(steps), sign_policy=sign_policy, patch_updates=int(cnt.item()),
+    return dict(config=name, steps=list(steps), sign_policy=sign_policy, patch_updates=int(cnt[0]), stale_skipped=int(cnt[1]),
                 targets=n, mean_d2_patchmatch=d_pm, mean_d2_bruteforce=d_bf,
                 ratio_minus_1=d_pm / d_bf - 1 if d_bf > 0 else 0.0, frac_exact=same)
 

@@ -224,7 +224,7 @@ def test_emulated_ranks_bit_identical_to_one(case, exchange, world):
     from paper_1503_05528_b200 import Config
     v, m = CASES[case]()
     L = 2 if case == "c2" else 3
-    cfg1 = Config(levels=L, exchange=exchange)
+    cfg1 = Config(levels=L, exchange=exchange, replicate_below=0)  # every level in slabs
     ref = _run_world(v, m, cfg1, 1)[0]
     got = _run_world(v, m, cfg1, world)
     for rank, (out, lev, pu, ng, nh) in enumerate(got):
@@ -233,3 +233,17 @@ def test_emulated_ranks_bit_identical_to_one(case, exchange, world):
         assert [d["patch_updates"] for d in lev] == [d["patch_updates"] for d in ref[1]], rank
         assert pu == ref[2]
         assert (nh > 0) if exchange == "halo" else (ng > 0)
+
+
+@pytest.mark.parametrize("world", [2, 4])
+def test_emulated_ranks_replicated_coarse_level(world):
+    """c2 with the coarse level (63,900 targets) replicated and level 1 (212,700) in slabs"""
+    from paper_1503_05528_b200 import Config
+    v, m = CASES["c2"]()
+    cfg = Config(levels=2, exchange="halo", replicate_below=100_000)
+    ref = _run_world(v, m, Config(levels=2), 1)[0]
+    for rank, (out, lev, pu, ng, nh) in enumerate(_run_world(v, m, cfg, world)):
+        assert torch.equal(out, ref[0]), (rank, "output video")
+        assert [d["outer"] for d in lev] == [d["outer"] for d in ref[1]], rank
+        assert [d["patch_updates"] for d in lev] == [d["patch_updates"] for d in ref[1]], rank
+        assert pu == ref[2] and nh > 0

@@ -14,7 +14,9 @@ import torch.multiprocessing as mp
 
 from gen.synth import random_volume
 
-CFG = dict(levels=2, pm_iters=2, max_outer=3)
+# replicate_below=0: every level split into slabs (these volumes are far below the default
+# threshold, which would run them replicated)
+CFG = dict(levels=2, pm_iters=2, max_outer=3, replicate_below=0)
 
 
 def _free_port():
@@ -155,11 +157,12 @@ def _run_cfg(rank, world, port, out_path, spec):
         import oracle_ops
         from gen.synth import random_holes
         from paper_1503_05528_b200 import Config, Exchange, inpaint
-        W, H, T, seed, levels, steps, exchange = spec
+        W, H, T, seed, levels, steps, exchange = spec[:7]
+        rb = spec[7] if len(spec) > 7 else 0
         v, _, _ = random_volume(W, H, T, seed=seed)
         m = random_holes(W, H, T, seed, 2)
         v[m.bool()] = 0
-        cfg = Config(levels=levels, pm_iters=2, max_outer=2, steps=steps, exchange=exchange)
+        cfg = Config(levels=levels, pm_iters=2, max_outer=2, steps=steps, exchange=exchange, replicate_below=rb)
         out, stats, _ = inpaint(v, m, cfg, device="cpu", exchange=Exchange(), ops=oracle_ops)
         if rank == 0:
             np.save(out_path, out.numpy())
@@ -182,6 +185,26 @@ def test_halo_fuzz_equals_single_rank(tmp_path, world, W, H, T, seed, levels, st
         out = str(tmp_path / f"fz_{wsz}_{ex}.npy")
         mp.spawn(_run_cfg, args=(wsz, _free_port(), out, (W, H, T, seed, levels, steps, ex)), nprocs=wsz,
                  join=True)
+        outs.append((np.load(out), np.load(out + ".stats.npy")))
+    assert np.array_equal(outs[0][0], outs[1][0])
+    assert np.array_equal(outs[0][1], outs[1][1])
+
+
+@pytest.mark.parametrize("exchange", ["halo", "allgather"])
+def test_replicated_coarse_levels_equal_single_rank(tmp_path, exchange):
+    """levels below the target-count threshold run replicated (no exchange, counted once), the
+    finer ones in slabs: world 3 equals world 1 (video, outer counts, per-level patch-updates)"""
+    W, H, T, seed, levels, steps = 44, 36, 30, 21, 3, (8, 4, 2, 1)
+    from gen.synth import random_holes
+    from oracle.oracle import sets
+    m = random_holes(W, H, T, seed, 2)
+    # threshold = the level-1 target count: level 1 is not below it (slabs), levels 2-3 are (replicated)
+    rb = int(sets(np.ascontiguousarray(m.numpy()))[1].sum())
+    outs = []
+    for wsz in (1, 3):
+        out = str(tmp_path / f"rp_{wsz}_{exchange}.npy")
+        mp.spawn(_run_cfg, args=(wsz, _free_port(), out, (W, H, T, seed, levels, steps, exchange, rb)),
+                 nprocs=wsz, join=True)
         outs.append((np.load(out), np.load(out + ".stats.npy")))
     assert np.array_equal(outs[0][0], outs[1][0])
     assert np.array_equal(outs[0][1], outs[1][1])
