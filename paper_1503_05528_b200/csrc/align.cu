@@ -667,6 +667,7 @@ size_t vinp_affine_ws_bytes(int W, int H, int T, int levels) {
 vinp_status vinp_affine_estimate(const uint8_t* rgb, const uint8_t* mask, int W, int H, int T, int levels,
                                  int max_iter, double tol, int32_t pair_b, int32_t pair_e, double* theta,
                                  int32_t* status, int32_t* iters, void* ws, size_t ws_bytes, void* stream) {
+  VINP_NVTX();
   VINP_REQUIRE(rgb && mask && theta && status && iters && ws, "vinp_affine_estimate: null argument");
   VINP_REQUIRE(W >= 2 && H >= 2 && T >= 1 && levels >= 1 && levels <= 8 && max_iter >= 0,
                "vinp_affine_estimate: bad sizes");
@@ -713,6 +714,7 @@ vinp_status vinp_affine_estimate(const uint8_t* rgb, const uint8_t* mask, int W,
 
 vinp_status vinp_affine_chain(const double* pairs, int T, double* fwd, double* inv, int32_t* err,
                               void* stream) {
+  VINP_NVTX();
   VINP_REQUIRE(fwd && inv && err && T >= 1 && (pairs || T == 1), "vinp_affine_chain: bad arguments");
   k_affine_chain<<<1, 1, 0, S(stream)>>>(pairs, T, fwd, inv, err);
   count_launch();
@@ -721,6 +723,7 @@ vinp_status vinp_affine_chain(const double* pairs, int T, double* fwd, double* i
 
 vinp_status vinp_align_warp(const uint8_t* rgb, const uint8_t* mask, int W, int H, int T, const double* inv,
                             uint8_t* rgb_out, uint8_t* mask_out, void* stream) {
+  VINP_NVTX();
   VINP_REQUIRE(rgb && mask && inv && rgb_out && mask_out, "vinp_align_warp: null argument");
   VINP_REQUIRE(W >= 2 && H >= 2 && T >= 1 && H <= 65535 && T <= 65535, "vinp_align_warp: bad sizes");
   dim3 g((W + 127) / 128, H, T);
@@ -731,6 +734,7 @@ vinp_status vinp_align_warp(const uint8_t* rgb, const uint8_t* mask, int W, int 
 
 vinp_status vinp_unwarp(const uint8_t* rgb_aligned, const uint8_t* rgb_orig, const uint8_t* mask_orig, int W,
                         int H, int T, const double* fwd, uint8_t* out, void* stream) {
+  VINP_NVTX();
   VINP_REQUIRE(rgb_aligned && rgb_orig && mask_orig && fwd && out, "vinp_unwarp: null argument");
   VINP_REQUIRE(W >= 2 && H >= 2 && T >= 1 && H <= 65535 && T <= 65535, "vinp_unwarp: bad sizes");
   dim3 g((W + 127) / 128, H, T);

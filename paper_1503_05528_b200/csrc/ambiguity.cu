@@ -54,6 +54,7 @@ extern "C" {
 
 vinp_status vinp_patch_ambiguity(int N, double sigma, uint64_t seed, uint64_t trial0, uint64_t n_trials,
                                  unsigned long long* hits, void* stream) {
+  VINP_NVTX();
   VINP_REQUIRE(N >= 1 && N <= 4096 && sigma > 0 && hits, "vinp_patch_ambiguity: bad arguments");
   if (n_trials == 0) return VINP_OK;
   uint64_t blocks = std::min<uint64_t>((n_trials + 255) / 256, 148ull * 16);

@@ -1036,6 +1036,7 @@ extern "C" {
 
 vinp_status vinp_nnf_init_random(const vinp_level* lv, vinp_nnf* nnf, const vinp_params* prm,
                                  uint32_t outer_code, int32_t b, int32_t e, void* stream) {
+  VINP_NVTX();
   vinp_status st = check_nnf_args(lv, "vinp_nnf_init_random", b, e, prm);
   if (st) return st;
   VINP_REQUIRE(nnf && nnf->e && nnf->n, "vinp_nnf_init_random: null nnf");
@@ -1054,6 +1055,7 @@ vinp_status vinp_nnf_init_random(const vinp_level* lv, vinp_nnf* nnf, const vinp
 vinp_status vinp_nnf_upsample(const vinp_level* coarse, const vinp_nnf* cn, const vinp_level* fine,
                               vinp_nnf* fn, const vinp_params* prm, int32_t b, int32_t e,
                               void* stream) {
+  VINP_NVTX();
   vinp_status st = check_nnf_args(fine, "vinp_nnf_upsample", b, e, prm);
   if (st) return st;
   st = check_level(coarse, "vinp_nnf_upsample(coarse)");
@@ -1140,6 +1142,7 @@ extern "C" {
 vinp_status vinp_nnf_evaluate(const vinp_level* lv, vinp_nnf* nnf, const vinp_params* prm, int kb,
                               int only_layer, int32_t b, int32_t e, unsigned long long* counter,
                               void* stream) {
+  VINP_NVTX();
   return launch_evaluate(lv, nnf, prm, kb, only_layer, b, e, nullptr, counter, stream);
 }
 
@@ -1147,6 +1150,7 @@ vinp_status vinp_propagate(const vinp_level* lv, const vinp_nnf* in, vinp_nnf* o
                            const vinp_params* prm, int step, int sign, int kb, int only_layer,
                            int32_t b, int32_t e, int pass, int since, unsigned long long* counter,
                            void* stream) {
+  VINP_NVTX();
   return launch_propagate(lv, in, out, prm, step, sign, kb, only_layer, b, e, pass, since, nullptr,
                           counter, stream);
 }
@@ -1211,6 +1215,7 @@ vinp_status vinp_random_search(const vinp_level* lv, const vinp_nnf* in, vinp_nn
                                const vinp_params* prm, uint32_t outer_code, int pm_iter, int kb,
                                int only_layer, int32_t b, int32_t e, int pass,
                                unsigned long long* counter, void* stream) {
+  VINP_NVTX();
   return launch_random_search(lv, in, out, prm, outer_code, pm_iter, kb, only_layer, b, e, pass, nullptr,
                               counter, stream);
 }
@@ -1219,6 +1224,7 @@ vinp_status vinp_ann_search(const vinp_level* lv, vinp_nnf* a, vinp_nnf* b, cons
                             uint32_t outer_code, int K, const int32_t* steps, int n_steps,
                             int sign_policy, int kb, int only_layer, unsigned long long* counter,
                             void* stream) {
+  VINP_NVTX();
   VINP_REQUIRE(sign_policy == 0 || sign_policy == 1, "vinp_ann_search: bad sign_policy");
   VINP_REQUIRE(a && b && steps && n_steps >= 0 && n_steps <= 16 && K >= 0, "vinp_ann_search: bad args");
   vinp_nnf ua = *a, ub = *b;
@@ -1260,6 +1266,7 @@ size_t vinp_brute_force_ws_bytes(const vinp_level* lv) {
 
 vinp_status vinp_brute_force(const vinp_level* lv, vinp_nnf* out, const vinp_params* prm, int32_t b,
                              int32_t e, void* ws, size_t ws_bytes, void* stream) {
+  VINP_NVTX();
   vinp_status st = check_nnf_args(lv, "vinp_brute_force", b, e, prm);
   if (st) return st;
   VINP_REQUIRE(out && out->e && out->n, "vinp_brute_force: null nnf");
@@ -1279,6 +1286,7 @@ vinp_status vinp_brute_force(const vinp_level* lv, vinp_nnf* out, const vinp_par
 
 vinp_status vinp_brute_force_list(const vinp_level* lv, vinp_nnf* out, const vinp_params* prm,
                                   const int32_t* list, int32_t n, void* stream) {
+  VINP_NVTX();
   vinp_status st = check_nnf_args(lv, "vinp_brute_force_list", 0, 0, prm);
   if (st) return st;
   VINP_REQUIRE(out && out->e && out->n, "vinp_brute_force_list: null nnf");
@@ -1298,6 +1306,7 @@ vinp_status vinp_brute_force_list(const vinp_level* lv, vinp_nnf* out, const vin
 
 vinp_status vinp_patch_ssd(const vinp_level* lv, const int32_t* p, const int32_t* q, int64_t n,
                            const vinp_params* prm, int kb, uint32_t* D, uint8_t* cnt, void* stream) {
+  VINP_NVTX();
   vinp_status st = check_level(lv, "vinp_patch_ssd");
   if (st) return st;
   VINP_REQUIRE(p && q && D && cnt && prm && n >= 0, "vinp_patch_ssd: bad args");
@@ -1311,6 +1320,7 @@ vinp_status vinp_patch_ssd(const vinp_level* lv, const int32_t* p, const int32_t
 }
 
 vinp_status vinp_philox(const uint32_t* ctr, int64_t n, uint64_t seed, uint32_t* out, void* stream) {
+  VINP_NVTX();
   VINP_REQUIRE(ctr && out && n >= 0, "vinp_philox: bad args");
   if (n > 0) {
     k_philox<<<nblk(n, 256), 256, 0, S(stream)>>>((const uint4*)ctr, n, seed, (uint4*)out);

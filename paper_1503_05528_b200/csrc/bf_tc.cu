@@ -383,6 +383,7 @@ vinp_status vinp_brute_force_list(const vinp_level* lv, vinp_nnf* out, const vin
 
 vinp_status vinp_brute_force_tc(const vinp_level* lv, vinp_nnf* out, const vinp_params* prm, int32_t b,
                                 int32_t e, void* ws, size_t ws_bytes, void* stream) {
+  VINP_NVTX();
   vinp_status st = check_level(lv, "vinp_brute_force_tc");
   if (st) return st;
   VINP_REQUIRE(out && out->e && out->n && prm && ws && lv->targets && lv->sources, "vinp_brute_force_tc: bad args");
@@ -452,6 +453,7 @@ vinp_status vinp_brute_force_tc(const vinp_level* lv, vinp_nnf* out, const vinp_
 }
 
 vinp_status vinp_tc_gemm_u8(const uint8_t* A, const uint8_t* B, int K, int32_t* C, void* stream) {
+  VINP_NVTX();
   VINP_REQUIRE(A && B && C && K > 0 && K % 32 == 0 && K <= 512, "vinp_tc_gemm_u8: bad arguments");
   size_t smem = 2 * 128 * (size_t)K;
   cudaFuncSetAttribute(k_tc_gemm_probe, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);

@@ -6,9 +6,20 @@
 #include <cstdarg>
 #include <cstdio>
 
+#include <nvtx3/nvToolsExt.h>
+
 #include "vinp.h"
 
 namespace vinp {
+
+// One NVTX range per C-ABI call (header-only NVTX v3: without an attached tool the push / pop are
+// a null-pointer test each), so nsys / ncu --nvtx can attribute kernels to the call that launched
+// them.
+struct NvtxRange {
+  explicit NvtxRange(const char* name) { nvtxRangePushA(name); }
+  ~NvtxRange() { nvtxRangePop(); }
+};
+#define VINP_NVTX() ::vinp::NvtxRange vinp_nvtx_range_(__func__)
 
 constexpr int kPatch = 125;   // 5x5x5
 constexpr int kR = 2;         // patch radius

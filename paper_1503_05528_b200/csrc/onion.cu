@@ -150,6 +150,7 @@ vinp_status vinp_onion_peel(vinp_level* lv, vinp_nnf* a, vinp_nnf* b, const vinp
                             const int32_t* steps, int n_steps, int sign_policy, int n_layers, float* out_rgb,
                             float* out_tex, unsigned long long* counter, void* ws, size_t ws_bytes,
                             void* stream) {
+  VINP_NVTX();
   vinp_status st = check_level(lv, "vinp_onion_peel");
   if (st) return st;
   VINP_REQUIRE(lv->layer && lv->targets && lv->holes && a && b && a->e && b->e && a->e != b->e && prm &&

@@ -387,11 +387,13 @@ vinp_status launch_reconstruct(vinp_level* lv, const vinp_nnf* nnf, int mode, in
 extern "C" {
 vinp_status vinp_reconstruct(vinp_level* lv, const vinp_nnf* nnf, int mode, int layer_j, int32_t hb,
                              int32_t he, float* out_rgb, float* out_tex, int commit, void* stream) {
+  VINP_NVTX();
   return launch_reconstruct(lv, nnf, mode, layer_j, hb, he, nullptr, out_rgb, out_tex, commit, stream);
 }
 
 vinp_status vinp_commit(vinp_level* lv, const float* out_rgb, const float* out_tex, int layer_j,
                         int32_t hb, int32_t he, void* stream) {
+  VINP_NVTX();
   vinp_status st = check_level(lv, "vinp_commit");
   if (st) return st;
   VINP_REQUIRE(out_rgb && out_tex && lv->holes, "vinp_commit: null buffers");
@@ -406,6 +408,7 @@ vinp_status vinp_commit(vinp_level* lv, const float* out_rgb, const float* out_t
 }
 
 vinp_status vinp_change_l1(const float* a, const float* b, int64_t n, int64_t* out, void* stream) {
+  VINP_NVTX();
   VINP_REQUIRE(out && n >= 0 && (n == 0 || (a && b)), "vinp_change_l1: bad args");
   if (n > 0) {
     int g = (int)std::min<int64_t>(nblk(n, 256), 148 * 8);
@@ -416,6 +419,7 @@ vinp_status vinp_change_l1(const float* a, const float* b, int64_t n, int64_t* o
 }
 
 vinp_status vinp_change_l2(const float* a, const float* b, int64_t n, int64_t* out, void* stream) {
+  VINP_NVTX();
   VINP_REQUIRE(out && n >= 0 && (n == 0 || (a && b)), "vinp_change_l2: bad args");
   if (n > 0) {
     int g = (int)std::min<int64_t>(nblk(n, 256), 148 * 8);
@@ -426,6 +430,7 @@ vinp_status vinp_change_l2(const float* a, const float* b, int64_t n, int64_t* o
 }
 
 vinp_status vinp_energy(const vinp_level* lv, const vinp_nnf* nnf, double* out, void* stream) {
+  VINP_NVTX();
   vinp_status st = check_level(lv, "vinp_energy");
   if (st) return st;
   VINP_REQUIRE(nnf && nnf->e && nnf->n && out && lv->holes && lv->slot, "vinp_energy: null buffers");

@@ -391,6 +391,7 @@ int vinp_version(void) { return 1; }
 uint64_t vinp_launch_count(void) { return g_launches.load(); }
 
 vinp_status vinp_level_dims(int W, int H, int T, int L, int32_t* dims_out) {
+  VINP_NVTX();
   VINP_REQUIRE(dims_out && W >= 1 && H >= 1 && T >= 1 && L >= 1 && L <= 16, "vinp_level_dims: bad arguments");
   if ((int64_t)W * H * T >= (1ll << 31)) {
     set_error("vinp_level_dims: %dx%dx%d voxels exceed the 2^31 limit", W, H, T);
@@ -408,6 +409,7 @@ vinp_status vinp_level_dims(int W, int H, int T, int L, int32_t* dims_out) {
 
 vinp_status vinp_build_pyramid(const uint8_t* rgb, const uint8_t* mask, vinp_level* lv, int L,
                                void* stream) {
+  VINP_NVTX();
   VINP_REQUIRE(rgb && mask && lv && L >= 1 && L <= 16, "vinp_build_pyramid: bad arguments");
   for (int l = 0; l < L; ++l) {
     vinp_status st = check_level(&lv[l], "vinp_build_pyramid");
@@ -432,6 +434,7 @@ vinp_status vinp_build_pyramid(const uint8_t* rgb, const uint8_t* mask, vinp_lev
 }
 
 vinp_status vinp_output_rgb(const vinp_level* lv1, uint8_t* out, void* stream) {
+  VINP_NVTX();
   vinp_status st = check_level(lv1, "vinp_output_rgb");
   if (st) return st;
   VINP_REQUIRE(out, "vinp_output_rgb: null output");
@@ -447,6 +450,7 @@ size_t vinp_texture_ws_bytes(const vinp_level* lv1) {
 
 vinp_status vinp_texture_features(const vinp_params* prm, vinp_level* lv, int L, void* ws,
                                   size_t ws_bytes, void* stream) {
+  VINP_NVTX();
   VINP_REQUIRE(prm && lv && L >= 1 && L <= 16 && ws, "vinp_texture_features: bad arguments");
   VINP_REQUIRE(ws_bytes >= vinp_texture_ws_bytes(&lv[0]), "vinp_texture_features: ws too small");
   int h = prm->tex_half >= 0 ? prm->tex_half : (L >= 2 ? (1 << (L - 2)) : 1);
@@ -474,6 +478,7 @@ size_t vinp_sets_ws_bytes(const vinp_level* lv1) {
 
 vinp_status vinp_build_sets(vinp_level* lv, int L, int32_t* counts_out, void* ws, size_t ws_bytes,
                             void* stream) {
+  VINP_NVTX();
   VINP_REQUIRE(lv && L >= 1 && L <= 16 && counts_out && ws, "vinp_build_sets: bad arguments");
   VINP_REQUIRE(ws_bytes >= vinp_sets_ws_bytes(&lv[0]), "vinp_build_sets: ws too small");
   cudaStream_t s = S(stream);
@@ -506,6 +511,7 @@ vinp_status vinp_build_sets(vinp_level* lv, int L, int32_t* counts_out, void* ws
 }
 
 vinp_status vinp_build_lists(vinp_level* lv, int L, void* ws, size_t ws_bytes, void* stream) {
+  VINP_NVTX();
   VINP_REQUIRE(lv && L >= 1 && L <= 16 && ws, "vinp_build_lists: bad arguments");
   VINP_REQUIRE(ws_bytes >= vinp_sets_ws_bytes(&lv[0]), "vinp_build_lists: ws too small");
   cudaStream_t s = S(stream);
@@ -526,6 +532,7 @@ vinp_status vinp_build_lists(vinp_level* lv, int L, void* ws, size_t ws_bytes, v
 }
 
 vinp_status vinp_layers(vinp_level* lv, int32_t* n_layers_out, void* ws, void* stream) {
+  VINP_NVTX();
   VINP_REQUIRE(lv && lv->layer && n_layers_out && ws, "vinp_layers: bad arguments");
   vinp_status st = check_level(lv, "vinp_layers");
   if (st) return st;

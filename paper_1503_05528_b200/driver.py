@@ -47,6 +47,9 @@ class Config:
     # multi-GPU: a level with fewer targets than this runs replicated on every rank (no exchange;
     # its work counted once): a coarse level split W ways is launch- and exchange-bound
     replicate_below: int = 1 << 21
+    # per-level stage dumps (.npy, rank 0): after the onion peel and after each level's outer loop,
+    # the NNF (entries, n), the hole values (fp32) and the level's u8 voxel words; None = off
+    dump_dir: Optional[str] = None
     stop_rule: int = 0          # 0: R19 e = ||u_H - v_H||_1 / (3|H|); 1: literal P:988 ||.||_2 / (3|H|)
     skip_stale: bool = True     # R41: exact skip of stale propagation candidates (NNF unchanged)
 
@@ -316,6 +319,20 @@ class Inpainter:
                 self.ex.gather(st.cur_tex, n)
                 self.V.commit(lv, st.cur_rgb, st.cur_tex, layer_j, 0, n)
 
+    def _dump(self, tag: str, st: LevelState):
+        """Stage dump (Config.dump_dir): `<tag>_{nnf_e,nnf_n,holes,hole_rgb,hole_tex,vox}.npy`."""
+        import os
+        import numpy as np
+        if self.ex.rank != 0:
+            return
+        lv = st.lv
+        nt, nh = lv.n_targets, lv.n_holes
+        os.makedirs(self.cfg.dump_dir, exist_ok=True)
+        arrs = dict(nnf_e=st.a.e[:nt], nnf_n=st.a.n[:nt], targets=lv.targets[:nt], holes=lv.holes[:nh],
+                    hole_rgb=st.cur_rgb[:nh], hole_tex=st.cur_tex[:nh], vox=lv.vox)
+        for k, t in arrs.items():
+            np.save(os.path.join(self.cfg.dump_dir, f"{tag}_{k}.npy"), t.cpu().numpy())
+
     def replicated(self, l: int) -> bool:
         """Level l runs replicated on every rank (multi-GPU only): fewer than replicate_below targets."""
         return self.ex.world > 1 and self.states[l - 1].lv.n_targets < self.cfg.replicate_below
@@ -361,6 +378,8 @@ class Inpainter:
             st = self.states[-1]
             self.V.nnf_init_random(st.lv, st.a, self.prm, 0)
         e_on = ev(); e_on.record()
+        if cfg.dump_dir:
+            self._dump("onion", self.states[-1])
         onion_pu = self.counter.clone()  # replicated work: counted once (rank 0) in the job total
         snaps = {}  # counter after each level (device tensors: no extra host syncs)
         repl = {l: self.replicated(l) for l in range(1, L + 1)}
@@ -392,6 +411,8 @@ class Inpainter:
                     if stop_now(e_fixed, lv.n_holes, k, cfg.max_outer, cfg.stop_rule):
                         break
             self.stats.levels[l - 1]["change_fixed"] = changes
+            if cfg.dump_dir:
+                self._dump(f"level{l}", st)
             if l == 1:
                 self.reconstruct(st, V.BEST_PATCH, full=True, replicated=rp)  # Eq. 6; every rank gets u
             else:

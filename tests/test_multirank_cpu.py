@@ -208,3 +208,24 @@ def test_replicated_coarse_levels_equal_single_rank(tmp_path, exchange):
         outs.append((np.load(out), np.load(out + ".stats.npy")))
     assert np.array_equal(outs[0][0], outs[1][0])
     assert np.array_equal(outs[0][1], outs[1][1])
+
+
+def test_stage_dumps(tmp_path):
+    """Config.dump_dir writes the per-level stage arrays; the last one is the final level-1 state"""
+    import oracle_ops
+    from paper_1503_05528_b200 import Config, Inpainter
+    v, m, _ = _vol(8)
+    T, H, W, _ = v.shape
+    d = str(tmp_path / "dump")
+    ip = Inpainter(W, H, T, Config(levels=2, pm_iters=2, max_outer=2, dump_dir=d), "cpu", ops=oracle_ops)
+    ip.load(v, m)
+    ip.run(timing=False)
+    names = sorted(os.listdir(d))
+    for tag in ("onion", "level2", "level1"):
+        for k in ("nnf_e", "nnf_n", "targets", "holes", "hole_rgb", "hole_tex", "vox"):
+            assert f"{tag}_{k}.npy" in names
+    st = ip.states[0]
+    nt = st.lv.n_targets
+    e = np.load(os.path.join(d, "level1_nnf_e.npy"))
+    assert np.array_equal(e, st.a.e[:nt].numpy())  # level 1 dumped before best-patch, after its loop
+    assert np.load(os.path.join(d, "level1_hole_rgb.npy")).shape == (st.lv.n_holes, 3)
