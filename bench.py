@@ -165,6 +165,7 @@ def main():
                     help="time the oracle on one whole level-1 outer iteration of the config (all host "
                          "cores; several minutes) and write profiles/r02_cpu_full_outer.json")
     ap.add_argument("--one-core-sample", action="store_true", help=argparse.SUPPRESS)
+    ap.add_argument("--no-quality", action="store_true", help="skip the quality line (PatchMatch vs exact NN)")
     args = ap.parse_args()
     if args.impl == "reference":
         return run_reference(args)
@@ -271,6 +272,12 @@ def main():
         e2e = {"value": pu2 / (float(t2.item()) / 1000.0), "unit": "patch-updates/s",
                "h2d_bytes_per_step": int(v.numel() + m.numel()), "d2h_bytes_per_step": int(res.numel())}
 
+    quality = None
+    if rank == 0 and world == 1 and not args.no_extra and not args.no_quality:
+        del ip
+        torch.cuda.empty_cache()
+        quality = measure_quality(args.config, dev)
+
     cpu = None
     if rank == 0 and world == 1 and not args.no_cpu and not args.no_extra:
         frames, t0, iters = CPU_SAMPLE
@@ -309,12 +316,104 @@ def main():
                 # R41: stale propagation candidates proven unable to win, skipped (not patch-updates)
                 "stale_skipped_per_step": stale // args.steps, "sec_per_step": ms / args.steps / 1000.0,
                 "sec_per_level": levels,
-                "roofline": roof, "cpu_baseline": cpu, "e2e": e2e, "gpu_launches": launches,
+                "roofline": roof, "cpu_baseline": cpu, "e2e": e2e, "quality": quality, "gpu_launches": launches,
                 "clocks": clk.summary()}
         print(json.dumps(line), flush=True)
     if world > 1:
         dist.destroy_process_group()
     return 0
+
+
+QUALITY_SAMPLE = 512  # level-1 targets of the bench config checked against the exact NN (CUDA cores)
+
+
+def _level1_first_iteration(name, dev):
+    """An Inpainter at the state SURVEY §8(d) names for the quality line: level 1, first outer
+    iteration, right after upsampling (onion peel; each coarser level run with Alg. 4's stopping rule)."""
+    import torch
+    from gen.synth import generate, CONFIGS
+    from paper_1503_05528_b200 import Inpainter, vinp as V
+    from paper_1503_05528_b200.driver import stop_now
+    c = CONFIGS[name]
+    v, m, _ = generate(name, device=dev)
+    ip = Inpainter(c.W, c.H, c.T, _cfg(name), dev)
+    ip.load(v, m)
+    ip.onion_peel()
+    for l in range(c.levels, 1, -1):
+        s_, f_ = ip.states[l - 1], ip.states[l - 2]
+        k = 0
+        while True:
+            s_.prev_rgb.copy_(s_.cur_rgb)
+            ip.ann_search(s_, k)
+            ip.reconstruct(s_, V.WEIGHTED)
+            ip.change.zero_()
+            V.change_l1(s_.cur_rgb[:s_.lv.n_holes], s_.prev_rgb[:s_.lv.n_holes], ip.change)
+            k += 1
+            if c.fixed_outer and k >= c.fixed_outer or not c.fixed_outer and stop_now(
+                    int(ip.change.item()), s_.lv.n_holes, k, c.max_outer):
+                break
+        V.nnf_upsample(s_.lv, s_.a, f_.lv, f_.a, ip.prm)
+        ip.reconstruct(f_, V.UNWEIGHTED)
+    torch.cuda.synchronize()
+    return ip, v, m
+
+
+def _excess(lv, pm, bf, slots):
+    """mean d^2 (PatchMatch) / mean d^2 (exact NN) - 1 and the fraction at the exact NN, over slots."""
+    import torch
+    Dp, Db = (pm.e[slots] >> 32).double(), (bf.e[slots] >> 32).double()
+    npm, nbf = pm.n[slots].double(), bf.n[slots].double()
+    assert bool((Dp >= Db).all()) and torch.equal(npm, nbf), "PatchMatch below the exact minimum"
+    d_pm, d_bf = (Dp / (4 * npm)).mean().item(), (Db / (4 * nbf)).mean().item()
+    return {"ratio_minus_1": round(d_pm / d_bf - 1, 5) if d_bf > 0 else 0.0,
+            "frac_exact": round((pm.e[slots] == bf.e[slots]).double().mean().item(), 4),
+            "mean_d2_patchmatch": d_pm, "mean_d2_exact": d_bf}
+
+
+def measure_quality(name, dev):
+    """north_star quality line: mean NN distance after the configured PatchMatch iterations vs the
+    exact NN (a13).  (a) SURVEY §8(d)'s point (level 1, first outer iteration, same u and initial NNF)
+    on the bench config, on QUALITY_SAMPLE evenly spaced level-1 targets (exact NN on CUDA cores:
+    the tensor-core form needs the whole source im2col, 115 GB at c5); (b) the same point and (c) the
+    steady state (one more ANN search after the whole Alg. 4, on the final u) on c2, every target,
+    exact NN on the tensor cores."""
+    import torch
+    from gen.synth import CONFIGS
+    from paper_1503_05528_b200 import vinp as V
+    out = {"target": "<= 0.05 (north_star)"}
+    t0 = time.perf_counter()
+    for cfg_name, sample in ((name, QUALITY_SAMPLE), ("c2", None)):
+        c = CONFIGS[cfg_name]
+        ip, v, m = _level1_first_iteration(cfg_name, dev)
+        st = ip.states[0]
+        lv = st.lv
+        n = lv.n_targets
+        V.ann_search(lv, st.a, st.b, ip.prm, 0, c.pm_iters, tuple(ip.cfg.steps), counter=ip.counter)
+        bf = V.NNF.alloc(n, dev)
+        if sample:
+            k = min(sample, n)
+            slots = (torch.arange(k, device=dev, dtype=torch.int64) * (n - 1) // max(k - 1, 1)).to(torch.int32)
+            V.brute_force_list(lv, bf, ip.prm, slots)
+            idx = slots.long()
+        else:
+            V.brute_force_tc(lv, bf, ip.prm, 0, n)
+            idx = torch.arange(n, device=dev)
+        torch.cuda.synchronize()
+        key = f"{cfg_name}_level1_first_iteration" + (f"_sample{idx.numel()}" if sample else "")
+        out[key] = _excess(lv, st.a, bf, idx)
+        if not sample:  # steady state on c2: after the whole Alg. 4, one more ANN search
+            ip.load(v, m)
+            ip.run(timing=False)
+            st = ip.states[0]
+            V.nnf_evaluate(lv, st.a, ip.prm)
+            V.brute_force_tc(lv, bf, ip.prm, 0, n)
+            V.ann_search(lv, st.a, st.b, ip.prm, 1 << 20, c.pm_iters, tuple(ip.cfg.steps), counter=ip.counter)
+            torch.cuda.synchronize()
+            out[f"{cfg_name}_steady_state"] = _excess(lv, st.a, bf, idx)
+        del ip, v, m, bf
+        torch.cuda.empty_cache()
+    out["s"] = round(time.perf_counter() - t0, 1)
+    return out
 
 
 def measure_roofline(ip, v, m, dev):

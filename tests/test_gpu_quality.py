@@ -92,8 +92,9 @@ def test_patchmatch_quality_after_full_run(name):
     with open(os.path.join(ROOT, "gpurun_out", f"quality_final_{name}.json"), "w") as f:
         json.dump(q, f)
     print(json.dumps(q))
-    # measured (deterministic): c1 +2.8%, c2 +5.4%, c3 +2.3%; the bounds catch regressions
-    assert q["ratio_minus_1"] <= {"c1": 0.04, "c2": 0.065, "c3": 0.035}[name]
+    # north_star: <= 5%.  Measured (deterministic): c1 +2.8%, c2 +5.4%, c3 +2.3%: met on c1 and c3;
+    # on c2 no schedule sweeps below +5.4%, so its bound is the measured level
+    assert q["ratio_minus_1"] <= {"c1": 0.05, "c2": 0.065, "c3": 0.05}[name]
 
 
 @pytest.mark.parametrize("name", ["c1", "c2", "c3"])
@@ -106,3 +107,14 @@ def test_patchmatch_quality_vs_brute_force(name):
     # The north_star target is 5%; at this hardest point (right after upsampling) the measured
     # levels are c1 +5.4%, c2 +7.3%, c3 +20.4%; the bounds catch regressions
     assert q["ratio_minus_1"] <= {"c1": 0.065, "c2": 0.085, "c3": 0.22}[name]
+
+
+def test_patchmatch_quality_c5_sampled():
+    """The bench config at SURVEY §8(d)'s point (level 1, first outer iteration), 512 evenly spaced
+    targets against the exact NN (CUDA-core brute force over all 179.9 M sources): <= 5% (measured
+    +4.0%, bench.py `quality`)."""
+    import bench
+    q = bench.measure_quality("c5", torch.device("cuda", 0))
+    print(json.dumps(q))
+    assert q["c5_level1_first_iteration_sample512"]["ratio_minus_1"] <= 0.05
+    assert abs(q["c2_level1_first_iteration"]["ratio_minus_1"] - 0.0716) < 0.01
