@@ -40,6 +40,14 @@ MUTATIONS = [
      "      if (dup) continue;\n", "      (void)dup;\n", 1),
     ("percentile_rank_floor", "R10 P:495-496 (nearest rank ceil(0.75 m))",
      "int r = (3 * m + 3) / 4;", "int r = (3 * m) / 4 + (m < 4);", None),
+    ("stale_own_entry", "R41 (stale: the neighbour's entry, not the target's)",
+     "if (prev && prev->dx[rs] == vx && prev->dy[rs] == vy && prev->dt[rs] == vt) nst += 1;",
+     "if (prev && prev->dx[s] == vx && prev->dy[s] == vy && prev->dt[s] == vt) nst += 1;", None),
+    ("stale_before_dedup", "R41 (stale counted among evaluated candidates, after R33)",
+     "      if (dup) continue;\n      seen[nseen][0] = vx; seen[nseen][1] = vy; seen[nseen][2] = vt; ++nseen;\n      /* R41",
+     "      if (prev && prev->dx[rs] == vx && prev->dy[rs] == vy && prev->dt[rs] == vt) nst += 1;\n"
+     "      if (dup) continue;\n      seen[nseen][0] = vx; seen[nseen][1] = vy; seen[nseen][2] = vt; ++nseen;\n      /* R41",
+     None),
     ("best_patch_tie_last", "R13 / S:324 (ties -> smallest q)",
      "if (key_less(nnf->D[cs[i]], nnf->n[cs[i]], nnf->D[cs[best]], nnf->n[cs[best]])) best = i;",
      "if (!key_less(nnf->D[cs[best]], nnf->n[cs[best]], nnf->D[cs[i]], nnf->n[cs[i]])) best = i;", None),
