@@ -50,6 +50,10 @@ class Config:
     # per-level stage dumps (.npy, rank 0): after the onion peel and after each level's outer loop,
     # the NNF (entries, n), the hole values (fp32) and the level's u8 voxel words; None = off
     dump_dir: Optional[str] = None
+    # single GPU: each outer iteration's fixed launch sequence (copy of the hole values, the ANN
+    # search, the weighted reconstruction, the change) is captured once per (level, iteration) as a
+    # CUDA graph and replayed on later runs over same-sized buffers
+    graphs: bool = True
     stop_rule: int = 0          # 0: R19 e = ||u_H - v_H||_1 / (3|H|); 1: literal P:988 ||.||_2 / (3|H|)
     skip_stale: bool = True     # R41: exact skip of stale propagation candidates (NNF unchanged)
 
@@ -184,6 +188,7 @@ class Inpainter:
         self.n_layers = 0
         self.native = True  # False: every pass through its own C-ABI call (per-launch timing)
         self.native_onion = False  # True: Alg. 3 through vinp_onion_peel even when native is False
+        self._graphs = {}  # (level, outer iteration) -> torch.cuda.CUDAGraph
 
     # ------------------------------------------------------------------ setup (a1-a3)
     def load(self, rgb: torch.Tensor, mask: torch.Tensor):
@@ -202,6 +207,7 @@ class Inpainter:
         self.V.build_lists(self.levels, self.ws)
         old = {id(st.lv): st for st in self.states}
         self.states = []
+        reused = 0
         for lv in self.levels:
             # >= 1 row so that an empty H (nothing to inpaint) still passes valid device pointers
             npad = max(self.ex.padded(lv.n_targets), 1)
@@ -209,6 +215,7 @@ class Inpainter:
             st = old.get(id(lv))
             if st is not None and st.a.e.numel() == npad and st.cur_rgb.shape[0] == hpad:
                 self.states.append(st)  # same sizes: reuse the buffers (repeated calls)
+                reused += 1
                 continue
             # every NNF entry / hole value is written (init, upsample, evaluate, reconstruct)
             # before it is read, so no zero fill is needed
@@ -216,6 +223,8 @@ class Inpainter:
             b = V.NNF.alloc(npad, self.device, n=a.n, zero=False, stamp=self.cfg.skip_stale)
             z = lambda k: torch.empty((hpad, k), dtype=torch.float32, device=self.device)
             self.states.append(LevelState(lv, a, b, z(3), z(2), z(3), z(2)))
+        if reused != len(self.levels):
+            self._graphs = {}  # captured graphs hold the old buffers' addresses
         self.halo = self.cfg.exchange == "halo" and self.ex.world > 1
         if self.halo:
             self._halo_ranges()
@@ -319,6 +328,37 @@ class Inpainter:
                 self.ex.gather(st.cur_tex, n)
                 self.V.commit(lv, st.cur_rgb, st.cur_tex, layer_j, 0, n)
 
+    def _outer_body(self, st: LevelState, k: int, rp: bool):
+        """One outer iteration of Alg. 4 up to the change e: v <- u_H, ANN search,
+        weighted reconstruction, e (device scalar self.change)."""
+        lv, cfg = st.lv, self.cfg
+        st.prev_rgb.copy_(st.cur_rgb)
+        st.prev_tex.copy_(st.cur_tex)
+        self.ann_search(st, k, replicated=rp)
+        self.reconstruct(st, V.WEIGHTED, replicated=rp)
+        self.change.zero_()
+        hb, he = (0, lv.n_holes) if rp else self.ex.slab(lv.n_holes)
+        chg = self.V.change_l2 if cfg.stop_rule == 1 else self.V.change_l1
+        chg(st.cur_rgb[hb:he], st.prev_rgb[hb:he], self.change)
+        if not rp:
+            self.ex.allreduce_sum(self.change)
+
+    def _outer_iteration(self, l: int, st: LevelState, k: int, rp: bool):
+        """The outer-iteration body, eagerly or as a CUDA graph (single GPU, native passes): the
+        first run of each (level, k) captures it, later runs over the same buffers replay it."""
+        use = (self.cfg.graphs and self.native and self.ex.world == 1 and self.device.type == "cuda"
+               and self.V is V)
+        if not use:
+            return self._outer_body(st, k, rp)
+        g = self._graphs.get((l, k))
+        if g is None:
+            torch.cuda.synchronize(self.device)
+            g = torch.cuda.CUDAGraph()
+            with torch.cuda.graph(g):
+                self._outer_body(st, k, rp)
+            self._graphs[(l, k)] = g
+        g.replay()
+
     def _dump(self, tag: str, st: LevelState):
         """Stage dump (Config.dump_dir): `<tag>_{nnf_e,nnf_n,holes,hole_rgb,hole_tex,vox}.npy`."""
         import os
@@ -390,16 +430,7 @@ class Inpainter:
             k = 0
             changes = []
             while True:
-                st.prev_rgb.copy_(st.cur_rgb)
-                st.prev_tex.copy_(st.cur_tex)
-                self.ann_search(st, k, replicated=rp)
-                self.reconstruct(st, V.WEIGHTED, replicated=rp)
-                self.change.zero_()
-                hb, he = (0, lv.n_holes) if rp else self.ex.slab(lv.n_holes)
-                chg = self.V.change_l2 if cfg.stop_rule == 1 else self.V.change_l1
-                chg(st.cur_rgb[hb:he], st.prev_rgb[hb:he], self.change)
-                if not rp:
-                    self.ex.allreduce_sum(self.change)
+                self._outer_iteration(l, st, k, rp)
                 k += 1
                 if cfg.fixed_outer > 0:
                     changes.append(self.change.clone())  # read once at the end (no sync here)

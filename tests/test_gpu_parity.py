@@ -372,3 +372,30 @@ def test_pipeline_c2_full_config_end_to_end(orc):
     assert [l["stale_skipped"] for l in stats.levels] == st["stale"]
     assert [l["patch_updates"] for l in stats.levels] == [a - b for a, b in zip(st["patch_updates"], st["stale"])]
     assert np.array_equal(out.cpu().numpy(), ref)
+
+
+def test_cuda_graph_replay_equals_eager(orc):
+    """Config.graphs: the first run captures each (level, outer iteration) body, the second run
+    replays the graphs; both equal the eager driver (video, counts, stopping statistics)."""
+    from paper_1503_05528_b200 import Config, Inpainter
+    from gen.synth import CONFIGS
+    c = CONFIGS["c2"]
+    v, m, _ = generate("c2")
+    T, H, W, _ = v.shape
+    res = []
+    for graphs in (False, True):
+        ip = Inpainter(W, H, T, Config(levels=c.levels, pm_iters=c.pm_iters, max_outer=c.max_outer, lam=c.lam,
+                                       seed=c.seed, graphs=graphs), "cuda")
+        for _ in range(2 if graphs else 1):
+            ip.load(v.cuda(), m.cuda())
+            st = ip.run(timing=False)
+            res.append((ip.output(v.cuda()).cpu(), [dict(d) for d in st.levels], st.total_patch_updates,
+                        st.total_stale_skipped))
+        if graphs:
+            assert len(ip._graphs) == sum(d["outer"] for d in st.levels)
+    ref = res[0]
+    for r in res[1:]:
+        assert torch.equal(r[0], ref[0])
+        assert [d["outer"] for d in r[1]] == [d["outer"] for d in ref[1]]
+        assert [d["change_fixed"] for d in r[1]] == [d["change_fixed"] for d in ref[1]]
+        assert r[2:] == ref[2:]

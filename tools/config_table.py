@@ -22,7 +22,7 @@ def main():
         c = CONFIGS[name]
         v, m, _ = generate(name, device="cuda")
         cfg = Config(levels=c.levels, pm_iters=c.pm_iters, fixed_outer=c.fixed_outer, max_outer=c.max_outer,
-                     lam=c.lam, seed=c.seed)
+                     lam=c.lam, seed=c.seed, graphs=os.environ.get("VINP_NO_GRAPHS") is None)
         ip = Inpainter(c.W, c.H, c.T, cfg, "cuda")
         ip.load(v, m)
         ip.run()  # warm-up
@@ -35,7 +35,8 @@ def main():
         total = a.elapsed_time(b) / 1000
         pu = st.total_patch_updates
         row = dict(config=name, dims=[c.W, c.H, c.T], levels=c.levels, step_s=total,
-                   patch_updates=pu, patch_updates_per_s=pu / total,
+                   patch_updates=pu, stale_skipped=st.total_stale_skipped, patch_updates_per_s=pu / total,
+                   graphs=cfg.graphs,
                    model_frac_of_hbm=(625 * pu / total / 1e9) / HBM,
                    levels_detail=[dict(level=l["level"], outer=l["outer"], s=l["ms"] / 1000) for l in st.levels],
                    onion_s=st.onion_ms / 1000, onion_layers=st.onion_layers,
