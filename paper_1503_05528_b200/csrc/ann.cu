@@ -108,6 +108,12 @@ __global__ void k_upsample(LevelArgs c, const uint64_t* __restrict__ ce, LevelAr
 #ifndef VINP_PROP_SPARSE
 #define VINP_PROP_SPARSE 48  // warps with at most this many live propagation candidates: group path (A/B: 12 -> 48 = -4% per ANN search)
 #endif
+#ifndef VINP_PROP_LIGHT
+#define VINP_PROP_LIGHT 1  // R41-active propagation passes run the light kernel
+#endif
+#ifndef VINP_PROP_LIGHT_MINB
+#define VINP_PROP_LIGHT_MINB 8  // 128-thread blocks per SM the light kernel is compiled for (A/B: 8 < 12, 16)
+#endif
 #ifndef VINP_RS_SMALL
 #define VINP_RS_SMALL (148 * 32 * 8)  // random-search launches below this many targets: 8 per warp
 #endif
@@ -334,8 +340,12 @@ __global__ void __launch_bounds__(256) k_evaluate(LevelArgs a, uint64_t* __restr
 // Lane = target (thread-per-target, coherent candidates).  Candidates of rank 1..3 are evaluated
 // one rank at a time by all lanes that have one, each against the running best of its own target
 // (strict improvement in rank order, R25).
-template <int NCMAX>  // 3: one sign per pass; 6: both signs (sign = 0)
-__global__ void __launch_bounds__(256, VINP_PROP_MINB) k_propagate(LevelArgs a, const uint64_t* __restrict__ ein,
+// NCMAX 3: one sign per pass; 6: both signs (sign = 0).  LIGHT: every warp takes the column-group
+// path (no frame-major per-lane path), compiled for more resident warps — the passes of an ANN
+// search after the first same-(step, sign) pass, where the R41 skip leaves few live candidates and
+// the candidate-generation latency chain is the cost.
+template <int NCMAX, bool LIGHT>
+__global__ void __launch_bounds__(LIGHT ? 128 : 256, LIGHT ? VINP_PROP_LIGHT_MINB : VINP_PROP_MINB) k_propagate(LevelArgs a, const uint64_t* __restrict__ ein,
                                                    uint64_t* __restrict__ eout,
                                                    const uint8_t* __restrict__ sin,
                                                    uint8_t* __restrict__ sout, int lambda, int step,
@@ -454,8 +464,9 @@ __global__ void __launch_bounds__(256, VINP_PROP_MINB) k_propagate(LevelArgs a, 
       if ((threadIdx.x & 31) >= d) incl += y;
     }
     const int P = __shfl_sync(kFull, incl, 31);
-    if (P <= VINP_PROP_SPARSE) {  // warp-uniform
-      __shared__ int2 s_pairs[256 / 32][VINP_PROP_SPARSE];
+    if (LIGHT || P <= VINP_PROP_SPARSE) {  // warp-uniform
+      constexpr int kCap = LIGHT ? 32 * NCMAX : VINP_PROP_SPARSE;
+      __shared__ int2 s_pairs[(LIGHT ? 128 : 256) / 32][kCap];
       int2* pairs = s_pairs[threadIdx.x >> 5];
 #pragma unroll
       for (int c = 0; c < NCMAX; ++c)
@@ -475,6 +486,7 @@ __global__ void __launch_bounds__(256, VINP_PROP_MINB) k_propagate(LevelArgs a, 
     }
   }
 #endif
+  if constexpr (!LIGHT) {
   bool full = act && kb < 0 && px >= 2 && px < a.g.W - 2 && py >= 2 && py < a.g.H - 2 && pt >= 2 &&
               pt < a.g.T - 2;
   bool allfull = __all_sync(kFull, full || !act);
@@ -568,6 +580,7 @@ __global__ void __launch_bounds__(256, VINP_PROP_MINB) k_propagate(LevelArgs a, 
   if ((threadIdx.x & 31) == 0) {
     flush_count(counter, cnt);
     if (counter && nstale) flush_count(counter + 1, nstale);
+  }
   }
 }
 
@@ -1124,14 +1137,20 @@ vinp_status launch_propagate(const vinp_level* lv, const vinp_nnf* in, vinp_nnf*
       k_propagate_wide<<<nblk((int64_t)(e - b) * 32, VINP_WIDE_BLOCK), VINP_WIDE_BLOCK, 0, S(stream)>>>(
           args_of(lv), in->e, out->e, in->stamp, out->stamp, prm->lambda, step, sign, kb, only_layer, b, e,
           pass, since, list, counter);
-    else if (sign == 0)
-      k_propagate<6><<<nblk(e - b, pb), pb, 0, S(stream)>>>(
-          args_of(lv), in->e, out->e, in->stamp, out->stamp, prm->lambda, step, sign, kb, only_layer, b, e,
-          pass, since, list, counter);
-    else
-      k_propagate<3><<<nblk(e - b, pb), pb, 0, S(stream)>>>(
-          args_of(lv), in->e, out->e, in->stamp, out->stamp, prm->lambda, step, sign, kb, only_layer, b, e,
-          pass, since, list, counter);
+    else {
+      // R41 active (a previous same-(step, sign) pass exists): the light all-group-path kernel
+      const bool light = VINP_PROP_LIGHT && since > 0;
+#define VINP_PROP_LAUNCH(NC, L)                                                                     \
+  k_propagate<NC, L><<<nblk(e - b, pb), pb, 0, S(stream)>>>(args_of(lv), in->e, out->e, in->stamp,      \
+                                                            out->stamp, prm->lambda, step, sign, kb,     \
+                                                            only_layer, b, e, pass, since, list, counter)
+      if (sign == 0) {
+        if (light) VINP_PROP_LAUNCH(6, true); else VINP_PROP_LAUNCH(6, false);
+      } else {
+        if (light) VINP_PROP_LAUNCH(3, true); else VINP_PROP_LAUNCH(3, false);
+      }
+#undef VINP_PROP_LAUNCH
+    }
     count_launch();
   }
   return check_launch("vinp_propagate");
