@@ -114,6 +114,9 @@ __global__ void k_upsample(LevelArgs c, const uint64_t* __restrict__ ce, LevelAr
 #ifndef VINP_PROP_LIGHT_MINB
 #define VINP_PROP_LIGHT_MINB 8  // 128-thread blocks per SM the light kernel is compiled for (A/B: 8 < 12, 16)
 #endif
+#ifndef VINP_RS_ORDER
+#define VINP_RS_ORDER 1  // random-search pair list: 0 lane-major, 1/2 rank-major (ascending/descending); A/B: 1 is -0.7%
+#endif
 #ifndef VINP_RS_SMALL
 #define VINP_RS_SMALL (148 * 32 * 8)  // random-search launches below this many targets: 8 per warp
 #endif
@@ -146,8 +149,10 @@ __device__ __forceinline__ void group_eval(const LevelArgs& a, const int2* pairs
   // per loop iteration, and as soon as the pair aborts or completes the group takes the next
   // unassigned pair, so a surviving pair never holds other groups idle.  Sequential application
   // in rank order with strict improvement (R25) equals the lexicographic minimum of (D, pair index)
-  // over {incumbent (D_inc, -1)} + candidates; a pair is dropped once its partial sum proves it
-  // cannot reach that minimum (partial > best D, or == best D with a later index): exact (R35).
+  // over {incumbent (D_inc, -1)} + candidates, the index being the candidate's rank among its
+  // owner's candidates (carried in the pair: y = rank << 5 | owner lane), so the list may be in any
+  // order; a pair is dropped once its partial sum proves it cannot reach that minimum (partial >
+  // best D, or == best D with a later rank): exact (R35).
   int bestJ = -1;
   int j = -1, dtc = -2, t = 0, pi = 0, ty = 0, tt = 0, sq = 0;
   bool colok = false;
@@ -162,12 +167,12 @@ __device__ __forceinline__ void group_eval(const LevelArgs& a, const int2* pairs
       int jj = next + __popc(nb & ((1u << gbase) - 1u));
       bool take = need && jj < P;
       int2 pr = take ? pairs[jj] : make_int2(0, lane);
-      int src = take ? pr.y : lane;
+      int src = take ? (pr.y & 31) : lane;
       int npi = __shfl_sync(kFull, p, src), ntx = __shfl_sync(kFull, px, src);
       int nty = __shfl_sync(kFull, py, src), ntt = __shfl_sync(kFull, pt, src);
       if (take) {
-        j = jj;
-        t = pr.y;
+        j = pr.y >> 5;  // the candidate's rank among its owner's candidates (R25 tie key)
+        t = pr.y & 31;
         sq = pr.x;
         pi = npi;
         ty = nty;
@@ -470,7 +475,7 @@ __global__ void __launch_bounds__(LIGHT ? 128 : 256, LIGHT ? VINP_PROP_LIGHT_MIN
       int2* pairs = s_pairs[threadIdx.x >> 5];
 #pragma unroll
       for (int c = 0; c < NCMAX; ++c)
-        if (c < ncand) pairs[incl - ncand + c] = make_int2(cq[c], threadIdx.x & 31);
+        if (c < ncand) pairs[incl - ncand + c] = make_int2(cq[c], (c << 5) | (threadIdx.x & 31));
       __syncwarp();
       group_eval(a, pairs, P, threadIdx.x & 31, p, px, py, pt, lambda, bestD, bestq);
       if (have) {
@@ -816,7 +821,22 @@ __global__ void __launch_bounds__(32 * WPB, VINP_MINB * 8 / WPB) k_random_search
     if (lane >= d) incl += y;
   }
   int P = __shfl_sync(kFull, incl, 31);
-  for (int j = 0; j < nc; ++j) pairs[incl - nc + j] = make_int2(cand[j * 32 + lane], lane);
+#if VINP_RS_ORDER == 0
+  // lane-major (owner, rank) order
+  for (int j = 0; j < nc; ++j) pairs[incl - nc + j] = make_int2(cand[j * 32 + lane], (j << 5) | lane);
+#else
+  // rank-major: all owners' candidates of one rank together (1: rank 0 first, 2: last rank first),
+  // so that a warp iteration's pairs have similar radii; the rank stays the tie key
+  {
+    int base = 0;
+    for (int jr = 0; jr < NC; ++jr) {
+      const int j = VINP_RS_ORDER == 1 ? jr : NC - 1 - jr;
+      const unsigned mk = __ballot_sync(kFull, j < nc);
+      if (j < nc) pairs[base + __popc(mk & ((1u << lane) - 1u))] = make_int2(cand[j * 32 + lane], (j << 5) | lane);
+      base += __popc(mk);
+    }
+  }
+#endif
   __syncwarp();
   uint32_t bestD = e_D(inc);
   int bestq = e_q(inc);
