@@ -70,12 +70,27 @@ typedef struct {
   int32_t* sources; int32_t n_sources;
 } vinp_level;
 
+/* Other ranks' copies of one NNF buffer (NEXT #4 second stage, multi-GPU "fused" exchange): every
+ * entry a pass writes into the buffer is also stored, from the same kernel, into each peer copy
+ * (peer-mapped device pointers, e.g. torch symmetric memory; P2P stores over NVLink) and/or through
+ * an NVLS multicast address of the e array (multimem.st: one store reaches every GPU's copy).  The
+ * caller orders passes across ranks (a barrier after each pass); the library never waits. */
+#define VINP_MAX_PEERS 7
+typedef struct {
+  int32_t n_peers;                    /* 0..VINP_MAX_PEERS */
+  uint64_t* e[VINP_MAX_PEERS];        /* peer copies of e */
+  uint8_t* n[VINP_MAX_PEERS];         /* peer copies of n (written by evaluate), or NULL */
+  uint8_t* stamp[VINP_MAX_PEERS];     /* peer copies of stamp, or NULL */
+  uint64_t* mc_e;                     /* NVLS multicast address of e, or NULL (then e[] is used) */
+} vinp_mirror;
+
 typedef struct {
   uint64_t* e;      /* [n_targets] (D << 32) | source index */
   uint8_t* n;       /* [n_targets] patch voxel count; may be shared by ping-pong buffers */
   uint8_t* stamp;   /* [n_targets] or NULL: index of the pass of the current ANN search that last
                        changed e[s] (0 = unchanged since its evaluate); one array per ping-pong
                        buffer.  Enables the exact stale-candidate skip of vinp_propagate (R41). */
+  const vinp_mirror* mirror;  /* NULL, or where the entries written into this buffer also go */
 } vinp_nnf;
 
 typedef struct {

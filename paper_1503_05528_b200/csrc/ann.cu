@@ -307,11 +307,11 @@ __global__ void __launch_bounds__(256) k_evaluate(LevelArgs a, uint64_t* __restr
                                                   uint8_t* __restrict__ en, uint8_t* __restrict__ es,
                                                   int lambda, int kb, int only_layer, int32_t b,
                                                   int32_t e, const int32_t* __restrict__ list,
-                                                  unsigned long long* counter) {
+                                                  unsigned long long* counter, Mirror mo) {
   int idx = b + blockIdx.x * blockDim.x + threadIdx.x;
   bool act = idx < e;
   int s = act ? (list ? __ldg(list + idx) : idx) : 0;
-  if (act && es) es[s] = 0;  // pass 0 of the ANN search (R41)
+  if (act && es) put_u8(es, mo.st, mo.n, s, 0);  // pass 0 of the ANN search (R41)
   int p = act ? __ldg(a.targets + s) : 0;
   act = act && (only_layer < 0 || a.layer[p] == only_layer);
   unsigned cnt = 0;
@@ -333,8 +333,8 @@ __global__ void __launch_bounds__(256) k_evaluate(LevelArgs a, uint64_t* __restr
                 (kb < 0 || a.layer[p + dt * a.g.HW + dy * a.g.W + dx] < kb))
               ++n;
     }
-    ee[s] = pack_e(D, q);
-    en[s] = (uint8_t)n;
+    put_e(ee, mo, s, pack_e(D, q));
+    put_u8(en, mo.nn, mo.n, s, (uint8_t)n);
     cnt = 1;
   }
   cnt = __reduce_add_sync(kFull, cnt);
@@ -357,7 +357,7 @@ __global__ void __launch_bounds__(LIGHT ? 128 : 256, LIGHT ? VINP_PROP_LIGHT_MIN
                                                    int sign, int kb, int only_layer, int32_t b,
                                                    int32_t e, int pass, int since,
                                                    const int32_t* __restrict__ list,
-                                                   unsigned long long* counter) {
+                                                   unsigned long long* counter, Mirror mo) {
   int idx = b + blockIdx.x * blockDim.x + threadIdx.x;
   bool have = idx < e;
   int s = have ? (list ? __ldg(list + idx) : idx) : 0;
@@ -479,8 +479,8 @@ __global__ void __launch_bounds__(LIGHT ? 128 : 256, LIGHT ? VINP_PROP_LIGHT_MIN
       __syncwarp();
       group_eval(a, pairs, P, threadIdx.x & 31, p, px, py, pt, lambda, bestD, bestq);
       if (have) {
-        eout[s] = pack_e(bestD, bestq);
-        if (sout) sout[s] = bestq != q0 ? (uint8_t)pass : __ldg(sin + s);
+        put_e(eout, mo, s, pack_e(bestD, bestq));
+        if (sout) put_u8(sout, mo.st, mo.n, s, bestq != q0 ? (uint8_t)pass : __ldg(sin + s));
       }
       nstale = __reduce_add_sync(kFull, nstale);
       if ((threadIdx.x & 31) == 0) {
@@ -549,8 +549,8 @@ __global__ void __launch_bounds__(LIGHT ? 128 : 256, LIGHT ? VINP_PROP_LIGHT_MIN
       }
     }
     if (have) {
-      eout[s] = pack_e(bestD, bestq);
-      if (sout) sout[s] = bestq != q0 ? (uint8_t)pass : __ldg(sin + s);
+      put_e(eout, mo, s, pack_e(bestD, bestq));
+      if (sout) put_u8(sout, mo.st, mo.n, s, bestq != q0 ? (uint8_t)pass : __ldg(sin + s));
     }
     cnt = __reduce_add_sync(kFull, cnt);
     nstale = __reduce_add_sync(kFull, nstale);
@@ -577,8 +577,8 @@ __global__ void __launch_bounds__(LIGHT ? 128 : 256, LIGHT ? VINP_PROP_LIGHT_MIN
     }
   }
   if (have) {
-    eout[s] = pack_e(bestD, bestq);
-    if (sout) sout[s] = bestq != q0 ? (uint8_t)pass : __ldg(sin + s);
+    put_e(eout, mo, s, pack_e(bestD, bestq));
+    if (sout) put_u8(sout, mo.st, mo.n, s, bestq != q0 ? (uint8_t)pass : __ldg(sin + s));
   }
   cnt = __reduce_add_sync(kFull, cnt);
   nstale = __reduce_add_sync(kFull, nstale);
@@ -643,7 +643,7 @@ __global__ void __launch_bounds__(VINP_WIDE_BLOCK) k_propagate_wide(
     LevelArgs a, const uint64_t* __restrict__ ein, uint64_t* __restrict__ eout,
     const uint8_t* __restrict__ sin, uint8_t* __restrict__ sout, int lambda, int step, int sign,
     int kb, int only_layer, int32_t b, int32_t e, int pass, int since,
-    const int32_t* __restrict__ list, unsigned long long* counter) {
+    const int32_t* __restrict__ list, unsigned long long* counter, Mirror mo) {
   const int lane = threadIdx.x & 31;
   const int idx = b + (int)((blockIdx.x * (unsigned)blockDim.x + threadIdx.x) >> 5);
   if (idx >= e) return;  // warp-uniform
@@ -654,8 +654,8 @@ __global__ void __launch_bounds__(VINP_WIDE_BLOCK) k_propagate_wide(
   // (vinp_onion_peel) every target is in the layer, and the test waits until the end
   if (!list && only_layer >= 0 && a.layer[p] != only_layer) {
     if (lane == 0) {
-      eout[s] = inc;
-      if (sout) sout[s] = sin[s];
+      put_e(eout, mo, s, inc);
+      if (sout) put_u8(sout, mo.st, mo.n, s, sin[s]);
     }
     return;
   }
@@ -727,8 +727,8 @@ __global__ void __launch_bounds__(VINP_WIDE_BLOCK) k_propagate_wide(
     ++cnt;
   }
   if (lane == 0) {
-    eout[s] = pack_e(bestD, bestq);
-    if (sout) sout[s] = bestq != q0 ? (uint8_t)pass : sin[s];
+    put_e(eout, mo, s, pack_e(bestD, bestq));
+    if (sout) put_u8(sout, mo.st, mo.n, s, bestq != q0 ? (uint8_t)pass : sin[s]);
     flush_count(counter, cnt);
     if (counter && nstale) flush_count(counter + 1, nstale);
   }
@@ -741,12 +741,12 @@ __global__ void __launch_bounds__(VINP_WIDE_BLOCK) k_evaluate_wide(LevelArgs a, 
                                                                    uint8_t* __restrict__ es, int lambda,
                                                                    int kb, int only_layer, int32_t b,
                                                                    int32_t e, const int32_t* __restrict__ list,
-                                                                   unsigned long long* counter) {
+                                                                   unsigned long long* counter, Mirror mo) {
   const int lane = threadIdx.x & 31;
   const int idx = b + (int)((blockIdx.x * (unsigned)blockDim.x + threadIdx.x) >> 5);
   if (idx >= e) return;  // warp-uniform
   const int s = list ? __ldg(list + idx) : idx;
-  if (es && lane == 0) es[s] = 0;  // pass 0 of the ANN search (R41)
+  if (es && lane == 0) put_u8(es, mo.st, mo.n, s, 0);  // pass 0 of the ANN search (R41)
   const int p = __ldg(a.targets + s);
   if (only_layer >= 0 && a.layer[p] != only_layer) return;
   int px, py, pt;
@@ -758,8 +758,8 @@ __global__ void __launch_bounds__(VINP_WIDE_BLOCK) k_evaluate_wide(LevelArgs a, 
   const uint32_t D = __reduce_add_sync(kFull, w.part(reinterpret_cast<const unsigned long long*>(a.vox), q, lambda));
   const uint32_t n = __reduce_add_sync(kFull, (uint32_t)(w.ok[0] + w.ok[1] + w.ok[2] + w.ok[3]));
   if (lane == 0) {
-    ee[s] = pack_e(D, q);
-    en[s] = (uint8_t)n;
+    put_e(ee, mo, s, pack_e(D, q));
+    put_u8(en, mo.nn, mo.n, s, (uint8_t)n);
     flush_count(counter, 1);
   }
 }
@@ -775,7 +775,7 @@ __global__ void __launch_bounds__(32 * WPB, VINP_MINB * 8 / WPB) k_random_search
     LevelArgs a, const uint64_t* __restrict__ ein, uint64_t* __restrict__ eout,
     const uint8_t* __restrict__ sin, uint8_t* __restrict__ sout, int lambda, Radii rad,
     uint64_t seed, uint32_t oc, int pm_iter, int only_layer, int32_t b, int32_t e, int pass,
-    const int32_t* __restrict__ list, unsigned long long* counter) {
+    const int32_t* __restrict__ list, unsigned long long* counter, Mirror mo) {
   // TPW targets per warp (32; 8 for small launches, so that more warps share
   // the pair evaluations — the result does not depend on it)
   int lane = threadIdx.x & 31;
@@ -842,8 +842,8 @@ __global__ void __launch_bounds__(32 * WPB, VINP_MINB * 8 / WPB) k_random_search
   int bestq = e_q(inc);
   group_eval(a, pairs, P, lane, p, px, py, pt, lambda, bestD, bestq);
   if (have) {
-    eout[s] = pack_e(bestD, bestq);
-    if (sout) sout[s] = bestq != e_q(inc) ? (uint8_t)pass : __ldg(sin + s);
+    put_e(eout, mo, s, pack_e(bestD, bestq));
+    if (sout) put_u8(sout, mo.st, mo.n, s, bestq != e_q(inc) ? (uint8_t)pass : __ldg(sin + s));
   }
   if (lane == 0) flush_count(counter, (unsigned)P);
 }
@@ -857,7 +857,7 @@ __global__ void __launch_bounds__(VINP_WIDE_BLOCK) k_random_search_wide(
     LevelArgs a, const uint64_t* __restrict__ ein, uint64_t* __restrict__ eout,
     const uint8_t* __restrict__ sin, uint8_t* __restrict__ sout, int lambda, Radii rad,
     uint64_t seed, uint32_t oc, int pm_iter, int kb, int only_layer, int32_t b, int32_t e, int pass,
-    const int32_t* __restrict__ list, unsigned long long* counter) {
+    const int32_t* __restrict__ list, unsigned long long* counter, Mirror mo) {
   const int lane = threadIdx.x & 31;
   const int idx = b + (int)((blockIdx.x * (unsigned)blockDim.x + threadIdx.x) >> 5);
   if (idx >= e) return;  // warp-uniform
@@ -866,8 +866,8 @@ __global__ void __launch_bounds__(VINP_WIDE_BLOCK) k_random_search_wide(
   const uint64_t inc = __ldg(reinterpret_cast<const unsigned long long*>(ein) + s);
   if (!list && only_layer >= 0 && a.layer[p] != only_layer) {  // as k_propagate_wide
     if (lane == 0) {
-      eout[s] = inc;
-      if (sout) sout[s] = sin[s];
+      put_e(eout, mo, s, inc);
+      if (sout) put_u8(sout, mo.st, mo.n, s, sin[s]);
     }
     return;
   }
@@ -923,8 +923,8 @@ __global__ void __launch_bounds__(VINP_WIDE_BLOCK) k_random_search_wide(
     }
   }
   if (lane == 0) {
-    eout[s] = pack_e(bestD, bestq);
-    if (sout) sout[s] = bestq != q0 ? (uint8_t)pass : sin[s];
+    put_e(eout, mo, s, pack_e(bestD, bestq));
+    if (sout) put_u8(sout, mo.st, mo.n, s, bestq != q0 ? (uint8_t)pass : sin[s]);
     flush_count(counter, cnt);
   }
 }
@@ -1121,10 +1121,12 @@ vinp_status launch_evaluate(const vinp_level* lv, vinp_nnf* nnf, const vinp_para
   if (e > b) {
     if (kb >= 0)  // K-restricted (onion) launch: warp per target
       k_evaluate_wide<<<nblk((int64_t)(e - b) * 32, VINP_WIDE_BLOCK), VINP_WIDE_BLOCK, 0, S(stream)>>>(
-          args_of(lv), nnf->e, nnf->n, nnf->stamp, prm->lambda, kb, only_layer, b, e, list, counter);
+          args_of(lv), nnf->e, nnf->n, nnf->stamp, prm->lambda, kb, only_layer, b, e, list, counter,
+          mirror_of(nnf));
     else
       k_evaluate<<<nblk(e - b, VINP_EVAL_BLOCK), VINP_EVAL_BLOCK, 0, S(stream)>>>(
-          args_of(lv), nnf->e, nnf->n, nnf->stamp, prm->lambda, kb, only_layer, b, e, list, counter);
+          args_of(lv), nnf->e, nnf->n, nnf->stamp, prm->lambda, kb, only_layer, b, e, list, counter,
+          mirror_of(nnf));
     count_launch();
   }
   return check_launch("vinp_nnf_evaluate");
@@ -1156,14 +1158,15 @@ vinp_status launch_propagate(const vinp_level* lv, const vinp_nnf* in, vinp_nnf*
     if (kb >= 0)  // K-restricted (onion) launch: warp per target
       k_propagate_wide<<<nblk((int64_t)(e - b) * 32, VINP_WIDE_BLOCK), VINP_WIDE_BLOCK, 0, S(stream)>>>(
           args_of(lv), in->e, out->e, in->stamp, out->stamp, prm->lambda, step, sign, kb, only_layer, b, e,
-          pass, since, list, counter);
+          pass, since, list, counter, mirror_of(out));
     else {
       // R41 active (a previous same-(step, sign) pass exists): the light all-group-path kernel
       const bool light = VINP_PROP_LIGHT && since > 0;
 #define VINP_PROP_LAUNCH(NC, L)                                                                     \
   k_propagate<NC, L><<<nblk(e - b, pb), pb, 0, S(stream)>>>(args_of(lv), in->e, out->e, in->stamp,      \
                                                             out->stamp, prm->lambda, step, sign, kb,     \
-                                                            only_layer, b, e, pass, since, list, counter)
+                                                            only_layer, b, e, pass, since, list, counter, \
+                                                            mirror_of(out))
       if (sign == 0) {
         if (light) VINP_PROP_LAUNCH(6, true); else VINP_PROP_LAUNCH(6, false);
       } else {
@@ -1216,7 +1219,7 @@ vinp_status launch_random_search(const vinp_level* lv, const vinp_nnf* in, vinp_
   if (e > b && kb >= 0) {  // K-restricted (onion) launch: warp per target (M <= 32 lanes)
     k_random_search_wide<<<nblk((int64_t)(e - b) * 32, VINP_WIDE_BLOCK), VINP_WIDE_BLOCK, 0, S(stream)>>>(
         args_of(lv), in->e, out->e, in->stamp, out->stamp, prm->lambda, r, prm->seed, outer_code, pm_iter, kb,
-        only_layer, b, e, pass, list, counter);
+        only_layer, b, e, pass, list, counter, mirror_of(out));
     count_launch();
   } else if (e > b) {
     cudaStream_t cs = S(stream);
@@ -1225,7 +1228,7 @@ vinp_status launch_random_search(const vinp_level* lv, const vinp_nnf* in, vinp_
 #define VINP_RS2(NC, WPB, TPW)                                                                       \
   k_random_search<NC, WPB, TPW><<<nblk(e - b, TPW * WPB), 32 * WPB, 0, cs>>>(                           \
       la, in->e, out->e, in->stamp, out->stamp, prm->lambda, r, prm->seed, outer_code, pm_iter, only_layer, b, e, \
-      pass, list, counter)
+      pass, list, counter, mirror_of(out))
 #define VINP_RS(NC, WPB)          \
   do {                            \
     if (small)                    \

@@ -158,6 +158,48 @@ __device__ __forceinline__ uint4 draw(uint32_t p, uint32_t k, int level, int str
                 (uint32_t)seed, (uint32_t)(seed >> 32));
 }
 
+// ---------------------------------------------------------------- NNF mirrors (NEXT #4 stage 2)
+// Passed by value to the pass kernels: the epilogue stores every written entry into the peer
+// copies too (P2P stores), and e through the NVLS multicast address when there is one.
+struct Mirror {
+  int n;
+  uint64_t* e[VINP_MAX_PEERS];
+  uint8_t* nn[VINP_MAX_PEERS];
+  uint8_t* st[VINP_MAX_PEERS];
+  uint64_t* mc_e;
+};
+inline Mirror mirror_of(const vinp_nnf* f) {
+  Mirror m{};
+  if (f && f->mirror) {
+    const vinp_mirror* s = f->mirror;
+    m.n = s->n_peers;
+    for (int i = 0; i < s->n_peers && i < VINP_MAX_PEERS; ++i) {
+      m.e[i] = s->e[i];
+      m.nn[i] = s->n[i];
+      m.st[i] = s->stamp[i];
+    }
+    m.mc_e = s->mc_e;
+  }
+  return m;
+}
+__device__ __forceinline__ void multimem_st_u64(uint64_t* mc, uint64_t v) {
+  asm volatile("multimem.st.relaxed.sys.global.u64 [%0], %1;" ::"l"(mc), "l"(v) : "memory");
+}
+__device__ __forceinline__ void put_e(uint64_t* __restrict__ dst, const Mirror& m, int s, uint64_t v) {
+  dst[s] = v;
+  if (m.mc_e) {
+    multimem_st_u64(m.mc_e + s, v);
+  } else {
+    for (int i = 0; i < m.n; ++i) m.e[i][s] = v;
+  }
+}
+__device__ __forceinline__ void put_u8(uint8_t* __restrict__ dst, uint8_t* const* peers, int np, int s,
+                                       uint8_t v) {
+  dst[s] = v;
+  for (int i = 0; i < np; ++i)
+    if (peers[i]) peers[i][s] = v;
+}
+
 // ---------------------------------------------------------------- NNF entry packing
 __device__ __forceinline__ uint64_t pack_e(uint32_t D, int32_t q) {
   return ((uint64_t)D << 32) | (uint32_t)q;

@@ -43,7 +43,10 @@ class Config:
     align_levels: int = 3       # R36: estimation pyramid levels
     align_iters: int = 20       # R38: IRLS iterations per level
     align_tol: float = 1e-4     # R38: update-norm stop
-    exchange: str = "halo"      # multi-GPU: "halo" (NEXT #4: the rows a rank reads, P2P) or "allgather"
+    # multi-GPU: "halo" (NEXT #4: the rows a rank reads, P2P), "allgather", or "fused" (NEXT #4
+    # second stage: the pass kernels store their slab into every rank's NNF copy themselves, through
+    # peer pointers / an NVLS multicast address of symmetric-memory buffers; one barrier per pass)
+    exchange: str = "halo"
     # multi-GPU: a level with fewer targets than this runs replicated on every rank (no exchange;
     # its work counted once): a coarse level split W ways is launch- and exchange-bound
     replicate_below: int = 1 << 21
@@ -100,6 +103,40 @@ class Exchange:
     def allreduce_sum(self, t: torch.Tensor):
         if self.world > 1:
             self.dist.all_reduce(t, group=self.group)
+
+    # ---- NEXT #4 second stage ("fused"): symmetric-memory NNF buffers written by every rank's kernels
+    def alloc_nnf(self, key, npad: int, device, n=None, stamp=True):
+        """An NNF buffer whose e (and n, stamp) live in symmetric memory, peer-mapped on every rank."""
+        import torch.distributed._symmetric_memory as sm
+        gname = (self.group or self.dist.group.WORLD).group_name
+        self._sym = getattr(self, "_sym", {})
+
+        def sym(dtype):
+            t = sm.empty(npad, dtype=dtype, device=device)
+            return t, sm.rendezvous(t, gname)
+
+        e, he = sym(torch.int64)
+        nn, hn = (n, self._sym.get(("n", key[0]))) if n is not None else sym(torch.uint8)
+        st, hs = sym(torch.uint8) if stamp else (None, None)
+        self._sym[key] = (he, hn, hs)
+        self._sym[("n", key[0])] = hn
+        self._barrier_handle = he
+        return V.NNF(e, nn, st, key=key)
+
+    def mirror(self, key):
+        """The peer copies of buffer `key` for the pass kernels' epilogues."""
+        he, hn, hs = self._sym[key]
+        peers = [r for r in range(self.world) if r != self.rank]
+        mc = int(he.multicast_ptr) if getattr(he, "has_multicast_support", lambda: False)() else 0
+        return V.Mirror(e=[] if mc else [int(he.buffer_ptrs[r]) for r in peers],
+                        n=[int(hn.buffer_ptrs[r]) for r in peers] if hn is not None else [],
+                        stamp=[int(hs.buffer_ptrs[r]) for r in peers] if hs is not None else [],
+                        mc_e=mc)
+
+    def pass_barrier(self):
+        """After a fused pass: every rank's stores are visible before any rank reads (device-side
+        barrier on the current stream)."""
+        self._barrier_handle.barrier(channel=0)
 
     def slabs(self, n: int):
         c = self.padded(n) // self.world
@@ -219,13 +256,20 @@ class Inpainter:
                 continue
             # every NNF entry / hole value is written (init, upsample, evaluate, reconstruct)
             # before it is read, so no zero fill is needed
-            a = V.NNF.alloc(npad, self.device, zero=False, stamp=self.cfg.skip_stale)
-            b = V.NNF.alloc(npad, self.device, n=a.n, zero=False, stamp=self.cfg.skip_stale)
+            li = lv.level - 1
+            if self.cfg.exchange == "fused" and self.ex.world > 1:
+                a = self.ex.alloc_nnf((li, 0), npad, self.device, stamp=self.cfg.skip_stale)
+                b = self.ex.alloc_nnf((li, 1), npad, self.device, n=a.n, stamp=self.cfg.skip_stale)
+            else:
+                a = V.NNF.alloc(npad, self.device, zero=False, stamp=self.cfg.skip_stale)
+                b = V.NNF.alloc(npad, self.device, n=a.n, zero=False, stamp=self.cfg.skip_stale)
+            a.key, b.key = (li, 0), (li, 1)
             z = lambda k: torch.empty((hpad, k), dtype=torch.float32, device=self.device)
             self.states.append(LevelState(lv, a, b, z(3), z(2), z(3), z(2)))
         if reused != len(self.levels):
             self._graphs = {}  # captured graphs hold the old buffers' addresses
-        self.halo = self.cfg.exchange == "halo" and self.ex.world > 1
+        self.fused = self.cfg.exchange == "fused" and self.ex.world > 1
+        self.halo = self.cfg.exchange in ("halo", "fused") and self.ex.world > 1
         if self.halo:
             self._halo_ranges()
         top = self.levels[-1]
@@ -289,26 +333,45 @@ class Inpainter:
                 gather1(f.stamp)
 
         use = st.a.stamp is not None and cfg.pm_iters * (len(cfg.steps) + 1) <= 255
-        a_nnf, b_nnf = (st.a, st.b) if use else (V.NNF(st.a.e, st.a.n), V.NNF(st.b.e, st.b.n))
-        self.V.nnf_evaluate(lv, a_nnf, prm, kb, only_layer, b, e, self.counter)
-        gather(a_nnf)
-        gather1(a_nnf.n)
+        a_nnf, b_nnf = (st.a, st.b) if use else (V.NNF(st.a.e, st.a.n, key=st.a.key),
+                                                 V.NNF(st.b.e, st.b.n, key=st.b.key))
+        fused = self.fused and not replicated
+
+        def out(f):  # the buffer a pass writes: with the fused exchange, also every peer's copy
+            f.mirror = self.ex.mirror(f.key) if fused else None
+            if fused and f.stamp is None:
+                f.mirror.stamp = []
+            return f
+
+        def published(f):  # make the pass's output readable by the next pass on every rank
+            if fused:
+                self.ex.pass_barrier()
+            else:
+                gather(f)
+
+        if fused:  # evaluate rewrites every rank's copy of `a`: no rank may still be reading it
+            self.ex.pass_barrier()
+        self.V.nnf_evaluate(lv, out(a_nnf), prm, kb, only_layer, b, e, self.counter)
+        published(a_nnf)
+        if not fused:
+            gather1(a_nnf.n)
         clk = V.PassClock()
         for k in range(1, cfg.pm_iters + 1):
             sign = 0 if cfg.sign_policy else (1 if k % 2 == 1 else -1)
             for s in cfg.steps:
-                self.V.propagate(lv, a_nnf, b_nnf, prm, s, sign, kb, only_layer, b, e, self.counter,
+                self.V.propagate(lv, a_nnf, out(b_nnf), prm, s, sign, kb, only_layer, b, e, self.counter,
                                  pass_id=clk.pass_id, since=clk.since(s, sign))
                 clk.tick(s, sign)
                 a_nnf, b_nnf = b_nnf, a_nnf
                 st.a, st.b = st.b, st.a
-                gather(a_nnf)
-            self.V.random_search(lv, a_nnf, b_nnf, prm, outer_code, k, kb, only_layer, b, e, self.counter,
+                published(a_nnf)
+            self.V.random_search(lv, a_nnf, out(b_nnf), prm, outer_code, k, kb, only_layer, b, e, self.counter,
                                  pass_id=clk.pass_id)
             clk.tick()
             a_nnf, b_nnf = b_nnf, a_nnf
             st.a, st.b = st.b, st.a
-            gather(a_nnf)
+            published(a_nnf)
+        a_nnf.mirror = b_nnf.mirror = None
 
     def reconstruct(self, st: LevelState, mode: int, layer_j=-1, replicated=False, full=False):
         lv = st.lv

@@ -33,8 +33,16 @@ class _Level(C.Structure):
                 ("sources", C.c_void_p), ("n_sources", C.c_int32)]
 
 
+MAX_PEERS = 7
+
+
+class _Mirror(C.Structure):
+    _fields_ = [("n_peers", C.c_int32), ("e", C.c_void_p * MAX_PEERS), ("n", C.c_void_p * MAX_PEERS),
+                ("stamp", C.c_void_p * MAX_PEERS), ("mc_e", C.c_void_p)]
+
+
 class _NNF(C.Structure):
-    _fields_ = [("e", C.c_void_p), ("n", C.c_void_p), ("stamp", C.c_void_p)]
+    _fields_ = [("e", C.c_void_p), ("n", C.c_void_p), ("stamp", C.c_void_p), ("mirror", C.POINTER(_Mirror))]
 
 
 class _Params(C.Structure):
@@ -197,10 +205,40 @@ class Level:
 
 
 @dataclass
+class Mirror:
+    """Peer copies of an NNF buffer (NEXT #4 second stage): the kernels that write the buffer also
+    store every entry into these (P2P), or e through an NVLS multicast address."""
+    e: list = field(default_factory=list)       # peer e tensors / device pointers (ints)
+    n: list = field(default_factory=list)       # peer n (or None)
+    stamp: list = field(default_factory=list)   # peer stamps (or None)
+    mc_e: int = 0                               # multicast address of e, 0 = none
+
+    def struct(self):
+        m = _Mirror()
+        m.n_peers = len(self.e)
+        if m.n_peers > MAX_PEERS:
+            raise VinpError(f"at most {MAX_PEERS} peers")
+        for i in range(m.n_peers):
+            m.e[i] = _addr(self.e[i])
+            m.n[i] = _addr(self.n[i]) if i < len(self.n) else None
+            m.stamp[i] = _addr(self.stamp[i]) if i < len(self.stamp) else None
+        m.mc_e = self.mc_e or None
+        return m
+
+
+def _addr(x):
+    if x is None:
+        return None
+    return x if isinstance(x, int) else x.data_ptr()
+
+
+@dataclass
 class NNF:
     e: torch.Tensor
     n: torch.Tensor
     stamp: Optional[torch.Tensor] = None  # R41 change stamps (one per ping-pong buffer) or None
+    mirror: Optional[Mirror] = None       # NEXT #4 stage 2: peer copies written by the same kernels
+    key: object = None                    # (level index, ping-pong index): names the peer copies
     _s: object = field(default=None, repr=False)
 
     @classmethod
@@ -213,7 +251,9 @@ class NNF:
         return cls(e, n, st)
 
     def struct(self):
-        self._s = _NNF(_ptr(self.e), _ptr(self.n), _ptr(self.stamp))
+        self._m = self.mirror.struct() if self.mirror is not None else None
+        self._s = _NNF(_ptr(self.e), _ptr(self.n), _ptr(self.stamp),
+                       C.pointer(self._m) if self._m is not None else None)
         return C.byref(self._s)
 
 

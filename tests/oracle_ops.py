@@ -68,19 +68,35 @@ def _to_orc(lv, nnf):
     return f
 
 
-def _from_orc(lv, f, nnf):
+def _from_orc(lv, f, nnf, b=0, e=None):
+    """Write the oracle NNF back into the slots [b, e) of the vinp buffer (a pass writes only its
+    slab: under the fused exchange, other ranks fill the rest of the buffer concurrently)."""
     nt = lv.n_targets
-    p = lv.targets.numpy()[:nt].astype(np.int64)
+    e = nt if e is None else e
+    p = lv.targets.numpy()[b:e].astype(np.int64)
     HW = lv.H * lv.W
-    q = ((p // HW + f.dt[:nt]) * lv.H + (p // lv.W) % lv.H + f.dy[:nt]) * lv.W + p % lv.W + f.dx[:nt]
-    e = (f.D[:nt].astype(np.uint64) << np.uint64(32)) | q.astype(np.uint64)
-    nnf.e[:nt] = torch.from_numpy(e.view(np.int64).copy())
-    nnf.n[:nt] = torch.from_numpy(f.n[:nt].copy())
+    q = ((p // HW + f.dt[b:e]) * lv.H + (p // lv.W) % lv.H + f.dy[b:e]) * lv.W + p % lv.W + f.dx[b:e]
+    w = (f.D[b:e].astype(np.uint64) << np.uint64(32)) | q.astype(np.uint64)
+    nnf.e[b:e] = torch.from_numpy(w.view(np.int64).copy())
+    nnf.n[b:e] = torch.from_numpy(f.n[b:e].copy())
 
 
 def _count(counter, c):
     if counter is not None:
         counter[0] += int(c)
+
+
+def _mirror(f, b, e, with_n=False):
+    """NEXT #4 second stage: the slab this call wrote also goes into the peer copies (tensors)."""
+    m = getattr(f, "mirror", None)
+    if m is None:
+        return
+    for i, pe in enumerate(m.e):
+        pe[b:e] = f.e[b:e]
+        if f.stamp is not None and i < len(m.stamp) and m.stamp[i] is not None:
+            m.stamp[i][b:e] = f.stamp[b:e]
+        if with_n and i < len(m.n) and m.n[i] is not None:
+            m.n[i][b:e] = f.n[b:e]
 
 
 def _stamp(lv, nin, nout, b, e, pass_id):
@@ -180,9 +196,10 @@ def nnf_evaluate(lv, nnf, prm, kb=-1, only_layer=-1, b=0, e=None, counter=None):
     ol = _OLevel(lv)
     f = _to_orc(lv, nnf)
     _count(counter, orc.evaluate(ol, f, prm.lam, kb, only_layer, b, e))
-    _from_orc(lv, f, nnf)
+    _from_orc(lv, f, nnf, b, e)
     if nnf.stamp is not None:
         nnf.stamp[b:e] = 0
+    _mirror(nnf, b, e, with_n=True)
 
 
 def propagate(lv, nin, nout, prm, step, sign, kb=-1, only_layer=-1, b=0, e=None, counter=None,
@@ -191,8 +208,9 @@ def propagate(lv, nin, nout, prm, step, sign, kb=-1, only_layer=-1, b=0, e=None,
     ol = _OLevel(lv)
     fi, fo = _to_orc(lv, nin), _to_orc(lv, nout)
     _count(counter, orc.propagate(ol, fi, fo, prm.lam, step, sign, kb, only_layer, b, e))
-    _from_orc(lv, fo, nout)
+    _from_orc(lv, fo, nout, b, e)
     _stamp(lv, nin, nout, b, e, pass_id)
+    _mirror(nout, b, e)
 
 
 def random_search(lv, nin, nout, prm, outer_code, pm_iter, kb=-1, only_layer=-1, b=0, e=None,
@@ -203,8 +221,9 @@ def random_search(lv, nin, nout, prm, outer_code, pm_iter, kb=-1, only_layer=-1,
     rmax = prm.rmax if prm.rmax > 0 else ol.rmax
     _count(counter, orc.random_search(ol, fi, fo, prm.lam, prm.seed, prm.rho, rmax, lv.level, outer_code,
                                       pm_iter, kb, only_layer, b, e))
-    _from_orc(lv, fo, nout)
+    _from_orc(lv, fo, nout, b, e)
     _stamp(lv, nin, nout, b, e, pass_id)
+    _mirror(nout, b, e)
 
 
 def ann_search(lv, a, b, prm, outer_code, K, steps=(8, 4, 2, 1), kb=-1, only_layer=-1, counter=None,

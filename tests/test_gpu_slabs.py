@@ -127,6 +127,7 @@ class _Hub:
         self.world = world
         self.bar = threading.Barrier(world, timeout=600)
         self.box = [None] * world
+        self.nnf = [dict() for _ in range(world)]  # fused exchange: each rank's NNF buffers by key
         self.error = None
 
     def sync(self):
@@ -145,6 +146,26 @@ def _emulated_exchange(hub, rank):
             self.rank = rank
             self.gathers = 0
             self.halos = 0
+            self.barriers = 0
+
+        # NEXT #4 second stage: the "symmetric" buffers are plain device tensors of the emulated
+        # ranks (one GPU), the peers' copies are their tensors, the barrier is a host barrier
+        def alloc_nnf(self, key, npad, device, n=None, stamp=True):
+            from paper_1503_05528_b200 import vinp as V
+            f = V.NNF.alloc(npad, device, n=n, zero=False, stamp=stamp)
+            f.key = key
+            hub.nnf[rank][key] = f
+            return f
+
+        def mirror(self, key):
+            from paper_1503_05528_b200 import vinp as V
+            peers = [hub.nnf[r][key] for r in range(hub.world) if r != rank]
+            return V.Mirror(e=[f.e for f in peers], n=[f.n for f in peers],
+                            stamp=[f.stamp for f in peers if f.stamp is not None])
+
+        def pass_barrier(self):
+            hub.sync()
+            self.barriers += 1
 
         def gather(self, t, n):
             c = self.padded(n) // self.world
@@ -196,7 +217,7 @@ def _run_world(v, m, cfg, world):
             out = ip.output(v).clone()
             torch.cuda.synchronize()
             res[rank] = (out, [dict(d) for d in st.levels], st.total_patch_updates,
-                         getattr(ex, "gathers", 0), getattr(ex, "halos", 0))
+                         getattr(ex, "gathers", 0), getattr(ex, "halos", 0), getattr(ex, "barriers", 0))
         except BaseException as exc:  # surface the first failure, release the others
             hub.error = hub.error or exc
             hub.bar.abort()
@@ -227,7 +248,7 @@ def test_emulated_ranks_bit_identical_to_one(case, exchange, world):
     cfg1 = Config(levels=L, exchange=exchange, replicate_below=0)  # every level in slabs
     ref = _run_world(v, m, cfg1, 1)[0]
     got = _run_world(v, m, cfg1, world)
-    for rank, (out, lev, pu, ng, nh) in enumerate(got):
+    for rank, (out, lev, pu, ng, nh, nb) in enumerate(got):
         assert torch.equal(out, ref[0]), (rank, "output video")
         assert [d["outer"] for d in lev] == [d["outer"] for d in ref[1]], rank
         assert [d["patch_updates"] for d in lev] == [d["patch_updates"] for d in ref[1]], rank
@@ -242,8 +263,26 @@ def test_emulated_ranks_replicated_coarse_level(world):
     v, m = CASES["c2"]()
     cfg = Config(levels=2, exchange="halo", replicate_below=100_000)
     ref = _run_world(v, m, Config(levels=2), 1)[0]
-    for rank, (out, lev, pu, ng, nh) in enumerate(_run_world(v, m, cfg, world)):
+    for rank, (out, lev, pu, ng, nh, nb) in enumerate(_run_world(v, m, cfg, world)):
         assert torch.equal(out, ref[0]), (rank, "output video")
         assert [d["outer"] for d in lev] == [d["outer"] for d in ref[1]], rank
         assert [d["patch_updates"] for d in lev] == [d["patch_updates"] for d in ref[1]], rank
         assert pu == ref[2] and nh > 0
+
+
+@pytest.mark.parametrize("case", list(CASES))
+@pytest.mark.parametrize("world", [2, 4, 8])
+def test_emulated_ranks_fused_exchange(case, world):
+    """NEXT #4 second stage: every pass kernel stores its slab into all emulated ranks' NNF copies
+    (vinp_mirror peer pointers), a barrier per pass, no NNF collective: bit-identical to one rank"""
+    from paper_1503_05528_b200 import Config
+    v, m = CASES[case]()
+    L = 2 if case == "c2" else 3
+    ref = _run_world(v, m, Config(levels=L), 1)[0]
+    got = _run_world(v, m, Config(levels=L, exchange="fused", replicate_below=0), world)
+    for rank, (out, lev, pu, ng, nh, nb) in enumerate(got):
+        assert torch.equal(out, ref[0]), (rank, "output video")
+        assert [d["outer"] for d in lev] == [d["outer"] for d in ref[1]], rank
+        assert [d["patch_updates"] for d in lev] == [d["patch_updates"] for d in ref[1]], rank
+        assert [d["stale_skipped"] for d in lev] == [d["stale_skipped"] for d in ref[1]], rank
+        assert pu == ref[2] and nb > 0

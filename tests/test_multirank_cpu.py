@@ -229,3 +229,101 @@ def test_stage_dumps(tmp_path):
     e = np.load(os.path.join(d, "level1_nnf_e.npy"))
     assert np.array_equal(e, st.a.e[:nt].numpy())  # level 1 dumped before best-patch, after its loop
     assert np.load(os.path.join(d, "level1_hole_rgb.npy")).shape == (st.lv.n_holes, 3)
+
+
+def _cpu_emulated_world(v, m, cfg, world):
+    """W ranks as threads in one process (CPU, oracle ops): the exchanges through shared tensors and
+    a host barrier, the fused exchange's peer copies are the other ranks' tensors."""
+    import threading
+    import oracle_ops
+    from paper_1503_05528_b200 import Exchange, Inpainter, vinp as V
+
+    bar = threading.Barrier(world, timeout=600)
+    box = [None] * world
+    nnf = [dict() for _ in range(world)]
+    res = [None] * world
+    err = []
+
+    class Emu(Exchange):
+        def __init__(self, rank):
+            self.dist, self.group, self.world, self.rank = None, None, world, rank
+            self.barriers = 0
+
+        def gather(self, t, n):
+            c = self.padded(n) // self.world
+            box[self.rank] = t
+            bar.wait()
+            for r in range(self.world):
+                if r != self.rank:
+                    t[r * c:(r + 1) * c].copy_(box[r][r * c:(r + 1) * c])
+            bar.wait()
+
+        def allreduce_sum(self, t):
+            box[self.rank] = t.clone()
+            bar.wait()
+            tot = sum(b.to(torch.int64) for b in box).to(t.dtype)
+            bar.wait()
+            t.copy_(tot)
+
+        def halo(self, t, n, need):
+            sl = self.slabs(n)
+            box[self.rank] = t
+            bar.wait()
+            lo, hi = need[self.rank]
+            for r in range(self.world):
+                if r != self.rank:
+                    r0, r1 = max(sl[r][0], lo), min(sl[r][1], hi)
+                    if r1 > r0:
+                        t[r0:r1].copy_(box[r][r0:r1])
+            bar.wait()
+
+        def alloc_nnf(self, key, npad, device, n=None, stamp=True):
+            f = V.NNF.alloc(npad, device, n=n, stamp=stamp)
+            nnf[self.rank][key] = f
+            return f
+
+        def mirror(self, key):
+            peers = [nnf[r][key] for r in range(self.world) if r != self.rank]
+            return V.Mirror(e=[f.e for f in peers], n=[f.n for f in peers],
+                            stamp=[f.stamp for f in peers if f.stamp is not None])
+
+        def pass_barrier(self):
+            bar.wait()
+            self.barriers += 1
+
+    def body(rank):
+        try:
+            ex = Emu(rank)
+            T, H, W, _ = v.shape
+            ip = Inpainter(W, H, T, cfg, "cpu", exchange=ex, ops=oracle_ops)
+            ip.load(v, m)
+            st = ip.run(timing=False)
+            res[rank] = (ip.output(v).clone(), [d["outer"] for d in st.levels], st.total_patch_updates, ex.barriers)
+        except BaseException as exc:  # release the others
+            err.append(exc)
+            bar.abort()
+
+    th = [threading.Thread(target=body, args=(r,)) for r in range(world)]
+    for t in th:
+        t.start()
+    for t in th:
+        t.join()
+    if err:
+        raise err[0]
+    return res
+
+
+@pytest.mark.parametrize("world", [2, 3])
+def test_fused_exchange_host_logic(world, orc):
+    """NEXT #4 second stage, host logic on CPU: passes store their slab into every rank's copy
+    (oracle ops honour vinp_mirror), one barrier before each evaluate and after each pass, no NNF
+    collective: every rank's video equals the oracle's whole pipeline"""
+    from paper_1503_05528_b200 import Config
+    v, m, _ = _vol(10)
+    cfg = Config(exchange="fused", **CFG)
+    res = _cpu_emulated_world(v, m, cfg, world)
+    ref, st = orc.inpaint(v.numpy(), m.numpy(), CFG["levels"], pm_iters=CFG["pm_iters"],
+                          max_outer=CFG["max_outer"])
+    for out, outer, pu, nb in res:
+        assert np.array_equal(out.numpy(), ref)
+        assert outer == st["outer_iters"] and pu == sum(st["patch_updates"]) and nb > 0
