@@ -154,7 +154,7 @@ def main():
     ap.add_argument("--warmup", type=int, default=3)
     ap.add_argument("--impl", default="vinp", choices=["vinp", "reference"])
     ap.add_argument("--config", default="c5")
-    ap.add_argument("--exchange", default="halo", choices=["allgather", "halo"],
+    ap.add_argument("--exchange", default="halo", choices=["allgather", "halo", "fused"],
                     help="multi-GPU NNF / hole-value exchange (halo = NEXT #4 point-to-point of the rows each "
                          "rank reads; levels below Config.replicate_below targets run replicated), N > 1 only")
     ap.add_argument("--no-e2e", action="store_true")
