@@ -225,7 +225,8 @@ class Inpainter:
         self.n_layers = 0
         self.native = True  # False: every pass through its own C-ABI call (per-launch timing)
         self.native_onion = False  # True: Alg. 3 through vinp_onion_peel even when native is False
-        self._graphs = {}  # (level, outer iteration) -> torch.cuda.CUDAGraph
+        self._graphs = {}  # (level, outer iteration) -> (torch.cuda.CUDAGraph, libvinp kernels in it)
+        self.graph_launches = 0
 
     # ------------------------------------------------------------------ setup (a1-a3)
     def load(self, rgb: torch.Tensor, mask: torch.Tensor):
@@ -417,10 +418,13 @@ class Inpainter:
         if g is None:
             torch.cuda.synchronize(self.device)
             g = torch.cuda.CUDAGraph()
+            n0 = V.launch_count()
             with torch.cuda.graph(g):
                 self._outer_body(st, k, rp)
-            self._graphs[(l, k)] = g
-        g.replay()
+            self._graphs[(l, k)] = (g, V.launch_count() - n0)
+            g = self._graphs[(l, k)]
+        g[0].replay()
+        self.graph_launches += g[1]  # libvinp kernels this replay ran (the library counts launches, not replays)
 
     def _dump(self, tag: str, st: LevelState):
         """Stage dump (Config.dump_dir): `<tag>_{nnf_e,nnf_n,holes,hole_rgb,hole_tex,vox}.npy`."""

@@ -393,6 +393,7 @@ def test_cuda_graph_replay_equals_eager(orc):
                         st.total_stale_skipped))
         if graphs:
             assert len(ip._graphs) == sum(d["outer"] for d in st.levels)
+            assert ip.graph_launches > 0
     ref = res[0]
     for r in res[1:]:
         assert torch.equal(r[0], ref[0])
