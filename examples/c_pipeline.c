@@ -95,6 +95,8 @@ int main(int argc, char** argv) {
 
   const int32_t nt = lv.n_targets, nh = lv.n_holes;
   vinp_nnf a, b;
+  memset(&a, 0, sizeof(a)); /* mirror = NULL: no peer copies (single process) */
+  memset(&b, 0, sizeof(b));
   a.e = (uint64_t*)dalloc(8 * (size_t)nt);
   a.n = (uint8_t*)dalloc((size_t)nt);
   b.e = (uint64_t*)dalloc(8 * (size_t)nt);
