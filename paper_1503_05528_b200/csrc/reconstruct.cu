@@ -46,6 +46,76 @@ __device__ __forceinline__ uint8_t round_u8(float x) {
   return (uint8_t)floor((double)x + 0.5);
 }
 
+#ifndef VINP_REC_V2
+#define VINP_REC_V2 1  // adaptive rank search, table-driven weights (0: the round-1 forms, for A/B)
+#endif
+
+// 2^(j/128) = hi (1 + tail), j = 0..127 (tools/gen_exp_table.py); staged in shared memory per block
+__device__ const double2 kExpTab[128] = {
+#include "exp_tab.inc"
+};
+
+// round(2^36 exp(-a)), a >= 0, the weight of Eq. 5 in the fixed point of R31.  exp by the usual
+// table-driven reduction: -a = (128 k + j) ln2/128 + r, |r| <= ln2/256, exp(-a) = 2^k 2^(j/128) e^r
+// with a degree-5 polynomial for e^r - 1 (|error| < 2^-60) and a (hi, tail) table entry, about
+// 0.51 ulp; 2^36 is folded into the exponent and the rounding to an integer is the 1.5 * 2^52
+// shift (round half to even, as llrint).  Against glibc's exp followed by llrint: 2 of 6.5e8 weights
+// differ, by one unit of 2^-36 (host prototype of the same arithmetic).
+__device__ __forceinline__ int64_t weight36(double a, const double2* __restrict__ tab) {
+  const double InvLn2N = 0x1.71547652b82fep+7, Shift = 0x1.8p52;
+  const double Ln2hiN = 0x1.62e42fefa0000p-8, Ln2loN = 0x1.cf79abc9e3b3ap-47;
+  const double x = -fmin(a, 64.0);  // 2^36 exp(-64) < 2^-56 rounds to 0 like every larger a
+  const double t = __fma_rn(x, InvLn2N, Shift);
+  const int ki = __double2loint(t);
+  const double kd = __dadd_rn(t, -Shift);
+  double r = __fma_rn(kd, -Ln2hiN, x);
+  r = __fma_rn(kd, -Ln2loN, r);
+  const double r2 = __dmul_rn(r, r);
+  const double pa = __fma_rn(r, 1.0 / 6, 0.5), pb = __fma_rn(r, 1.0 / 120, 1.0 / 24);
+  const double2 T = tab[ki & 127];
+  double tmp = __dadd_rn(T.y, r);
+  tmp = __fma_rn(r2, pa, tmp);
+  tmp = __fma_rn(__dmul_rn(r2, r2), pb, tmp);
+  const double sc = __hiloint2double(__double2hiint(T.x) + (((ki >> 7) + 36) << 20), __double2loint(T.x));
+  const double u = __dadd_rn(__fma_rn(sc, tmp, sc), Shift);
+  return ((int64_t)(__double2hiint(u) - 0x43380000) << 32) | (uint32_t)__double2loint(u);
+}
+
+// The r-th smallest (1-based) of the warp's valid 32-bit keys k[0..3] per lane (invalid = ~0, valid
+// < 2^31; m >= r valid keys in the warp): bitwise rank search from the first bit where the keys
+// differ, one REDUX.SUM per bit, ended as soon as a round's count c = #{keys <= T} is r or r - 1:
+// the wanted key is then the largest key <= T or the smallest key > T (one REDUX.MAX / MIN) — a
+// few rounds instead of one per bit.
+__device__ __forceinline__ uint32_t select_rank32(const uint32_t (&k)[4], unsigned valid, uint32_t r, uint32_t m) {
+  const uint32_t kmin = __reduce_min_sync(kFull, min(min(k[0], k[1]), min(k[2], k[3])));
+  const uint32_t kmax = __reduce_max_sync(kFull, max(max((valid & 1) ? k[0] : 0u, (valid & 2) ? k[1] : 0u),
+                                                     max((valid & 4) ? k[2] : 0u, (valid & 8) ? k[3] : 0u)));
+  if (r == 1) return kmin;
+  if (r == m) return kmax;
+  const uint32_t x = kmax ^ kmin;
+  if (x == 0) return kmin;  // all keys equal
+  uint32_t ans = kmin & ~(0xffffffffu >> __clz(x));
+  for (uint32_t b = 0x80000000u >> __clz(x); b; b >>= 1) {
+    const uint32_t T = ans | (b - 1);
+    uint32_t c = (k[0] <= T) + (k[1] <= T) + (k[2] <= T) + (k[3] <= T);
+    c = __reduce_add_sync(kFull, c);
+    if (c == r) {  // the wanted key is the largest key <= T
+      uint32_t v = 0;
+#pragma unroll
+      for (int i = 0; i < 4; ++i) v = max(v, k[i] <= T ? k[i] : 0u);
+      return __reduce_max_sync(kFull, v);
+    }
+    if (c + 1 == r) {  // ... or the smallest key > T (invalid keys are ~0, above every valid one)
+      uint32_t v = 0xffffffffu;
+#pragma unroll
+      for (int i = 0; i < 4; ++i) v = min(v, k[i] > T ? k[i] : 0xffffffffu);
+      return __reduce_min_sync(kFull, v);
+    }
+    if (c < r) ans |= b;
+  }
+  return ans;
+}
+
 struct ReconArgs {
   Geo g;
   uint64_t* vox;
@@ -66,7 +136,7 @@ struct LaneVox {
 
 __device__ __forceinline__ void recon_hole(const ReconArgs& a, const LaneVox& LV, int lane, int mode, int layer_j,
                                            int h, float* __restrict__ out_rgb, float* __restrict__ out_tex,
-                                           int commit) {
+                                           int commit, const double2* __restrict__ tab) {
   int p = a.holes[h];
   if (layer_j >= 0 && a.layer[p] != layer_j) return;
   int px, py, pt;
@@ -158,6 +228,9 @@ __device__ __forceinline__ void recon_hole(const ReconArgs& a, const LaneVox& LV
       hi[i] = n125 ? (uint32_t)key[i] : (uint32_t)(key[i] >> 32);  // ~0 for invalid
       lo[i] = n125 ? 0u : (uint32_t)key[i];
     }
+#if VINP_REC_V2
+    const uint32_t ans = select_rank32(hi, valid, r, m);
+#else
     uint32_t hmin = __reduce_min_sync(kFull, min(min(hi[0], hi[1]), min(hi[2], hi[3])));
     uint32_t hmax = __reduce_max_sync(kFull, max(max((valid & 1) ? hi[0] : 0u, (valid & 2) ? hi[1] : 0u),
                                                  max((valid & 4) ? hi[2] : 0u, (valid & 8) ? hi[3] : 0u)));
@@ -173,6 +246,7 @@ __device__ __forceinline__ void recon_hole(const ReconArgs& a, const LaneVox& LV
       c = __reduce_add_sync(kFull, c);
       if (c < r) ans |= 1u << bit;
     }
+#endif
     uint32_t lans = 0;
     if (!n125) {
       uint32_t below = 0, lmin = 0xffffffffu, lmax = 0;
@@ -218,11 +292,28 @@ __device__ __forceinline__ void recon_hole(const ReconArgs& a, const LaneVox& LV
       Ds = __shfl_sync(kFull, myD, src);
       ns = __shfl_sync(kFull, myn, src);
     }
+#if VINP_REC_V2
+    // a = D_q / (2 D_s) with all n = 125: the correctly rounded quotient from the correctly rounded
+    // reciprocal y = RN(1/b) (once per hole), q = RN(a y), r = a - q b (exact, FMA), RN(q + r y)
+    // (Markstein's theorem; b = 2 D_s < 2^32 has no all-ones significand) — equal to __ddiv_rn
+    // (host check of the same arithmetic: 3.2e9 random and 3.6e8 exhaustive small pairs, 0 differ)
+    const double den = (double)(2ull * Ds), rcp = Ds ? __drcp_rn(den) : 0.0;
+#endif
 #pragma unroll
     for (int i = 0; i < 4; ++i) {
       if (!(valid >> i & 1)) { w[i] = 0; continue; }
       if (Ds == 0) {
         w[i] = Dq[i] == 0;
+#if VINP_REC_V2
+      } else if (n125) {
+        const double an = __dadd_rn(__hiloint2double(0x43300000, (int)Dq[i]), -4503599627370496.0);  // (double)D_q
+        const double q0 = __dmul_rn(an, rcp);
+        const double aa = __fma_rn(__fma_rn(-q0, den, an), rcp, q0);
+        w[i] = weight36(aa, tab);
+      } else {
+        const double aa = __ddiv_rn((double)((uint64_t)Dq[i] * ns), (double)(2ull * nq[i] * Ds));
+        w[i] = weight36(aa, tab);
+#else
       } else {
         // a = D_q n_s / (2 n_q D_s): one correctly rounded division of exact operands (with all
         // n = 125 the same real quotient as D_q / (2 D_s), hence the same double)
@@ -230,6 +321,7 @@ __device__ __forceinline__ void recon_hole(const ReconArgs& a, const LaneVox& LV
         double ad = n125 ? (double)(2ull * Ds) : (double)(2ull * nq[i] * Ds);
         double aa = __ddiv_rn(an, ad);
         w[i] = __double2ll_rn(__dmul_rn(exp(-aa), 68719476736.0));
+#endif
       }
     }
   }
@@ -280,6 +372,9 @@ __global__ void __launch_bounds__(256, 4) k_reconstruct(ReconArgs a, int mode, i
                                                      float* __restrict__ out_rgb,
                                                      float* __restrict__ out_tex, int commit) {
   const int lane = threadIdx.x & 31;
+  __shared__ double2 s_tab[128];
+  if (threadIdx.x < 128) s_tab[threadIdx.x] = kExpTab[threadIdx.x];
+  __syncthreads();
   LaneVox LV;
 #pragma unroll
   for (int i = 0; i < 4; ++i) {
@@ -294,7 +389,7 @@ __global__ void __launch_bounds__(256, 4) k_reconstruct(ReconArgs a, int mode, i
   }
   const int nw = gridDim.x * kWPB;
   for (int idx = hb + blockIdx.x * kWPB + (threadIdx.x >> 5); idx < he; idx += nw)
-    recon_hole(a, LV, lane, mode, layer_j, list ? __ldg(list + idx) : idx, out_rgb, out_tex, commit);
+    recon_hole(a, LV, lane, mode, layer_j, list ? __ldg(list + idx) : idx, out_rgb, out_tex, commit, s_tab);
 }
 
 __global__ void k_commit(Geo g, uint64_t* __restrict__ vox, const uint8_t* __restrict__ layer,
@@ -356,10 +451,6 @@ __global__ void k_energy(const int32_t* __restrict__ holes, int32_t nh, const in
 }  // namespace vinp
 
 using namespace vinp;
-
-extern "C" {
-
-}  // extern "C"
 
 namespace vinp {
 vinp_status launch_reconstruct(vinp_level* lv, const vinp_nnf* nnf, int mode, int layer_j, int32_t hb,
