@@ -68,6 +68,8 @@ typedef struct {
   int32_t* targets; int32_t n_targets;
   int32_t* holes;   int32_t n_holes;
   int32_t* sources; int32_t n_sources;
+  uint16_t* psum;    /* [T][H][W][8] patch sums for the random-search lower bound (R42), or NULL:
+                        see vinp_patch_sums */
 } vinp_level;
 
 /* Other ranks' copies of one NNF buffer (NEXT #4 second stage, multi-GPU "fused" exchange): every
@@ -179,6 +181,23 @@ vinp_status vinp_propagate(const vinp_level* lv, const vinp_nnf* in, vinp_nnf* o
                            const vinp_params* prm, int step, int sign, int kb, int only_layer,
                            int32_t b, int32_t e, int pass, int since, unsigned long long* counter,
                            void* stream);
+
+/* ---- patch sums for an exact lower-bound rejection in random search (R42; an early termination
+ * that changes no comparison, like R35) ----
+ * psum[p] = (S_R, S_G, S_B, S_Tx, S_Ty, 0, 0, 0), u16: the sums of the five channels of vox over
+ * the 125 voxels of N_p, defined for voxels whose whole patch lies in Omega (others: 0, never used).
+ * For a target p with a full patch and a source q in D~ (whose patch is always full), Cauchy-Schwarz
+ * over the 125 voxels gives, with the integer distance D of this header,
+ *     125 D(p, q) >= 4 (dS_R^2 + dS_G^2 + dS_B^2) + lambda (dS_Tx^2 + dS_Ty^2),  dS = S(p) - S(q),
+ * so a candidate whose right-hand side is >= 125 D_incumbent cannot strictly improve (R25) and is
+ * rejected by vinp_random_search (kb < 0 launches) before any patch row is read.  It still counts
+ * as a patch-update: results and counts equal those without psum.
+ * which = 0: every voxel (once per level, after vinp_texture_features: covers D~, which never
+ * changes); which = 1: the targets of slots [b, e) on the current u.  vinp_nnf_evaluate with kb < 0
+ * and only_layer < 0 refreshes the targets of its slots itself when lv->psum is set, so a search
+ * that starts with evaluate (as every ANN search does) always sees sums of the current u.
+ * VINP_E_INVALID if lv->psum is NULL. */
+vinp_status vinp_patch_sums(const vinp_level* lv, int which, int32_t b, int32_t e, void* stream);
 
 /* ---- a7: random search (Eq. 3, Alg. 1; R1, R3, R7) ----
  * v0 = in(p); for i = 1, 2, ...: R_i = rmax * rho^i (repeated fp64 multiplication) while

@@ -28,10 +28,12 @@ struct LevelArgs {
   const int32_t* sources;
   int32_t n_sources;
   int level;
+  const uint4* psum;  // R42 patch sums, or null
 };
 static LevelArgs args_of(const vinp_level* lv) {
   return LevelArgs{geo_of(lv), lv->vox,     lv->flags,     lv->layer, lv->slot,
-                   lv->targets, lv->sources, lv->n_sources, lv->level};
+                   lv->targets, lv->sources, lv->n_sources, lv->level,
+                   reinterpret_cast<const uint4*>(lv->psum)};
 }
 
 __device__ __forceinline__ int lin(const Geo& g, int x, int y, int t) {
@@ -339,6 +341,93 @@ __global__ void __launch_bounds__(256) k_evaluate(LevelArgs a, uint64_t* __restr
   }
   cnt = __reduce_add_sync(kFull, cnt);
   if ((threadIdx.x & 31) == 0) flush_count(counter, cnt);
+}
+
+// ------------------------------------------------------------------ R42: patch sums
+// psum[p] = the five channel sums of vox over N_p (u16 each: <= 125 * 255), for voxels whose whole
+// patch lies in Omega.  With them 125 D(p, q) >= 4 |dS_rgb|^2 + lambda |dS_T|^2 (Cauchy-Schwarz
+// over the 125 voxels), the exact lower bound random search tests before reading any patch row.
+__device__ __forceinline__ void vox_add(uint64_t w, uint32_t (&s)[5]) {
+  const uint32_t lo = (uint32_t)w, hi = (uint32_t)(w >> 32);
+  s[0] = __dp4a(lo, 0x00000001u, s[0]);
+  s[1] = __dp4a(lo, 0x00000100u, s[1]);
+  s[2] = __dp4a(lo, 0x00010000u, s[2]);
+  s[3] = __dp4a(hi, 0x00000001u, s[3]);
+  s[4] = __dp4a(hi, 0x00000100u, s[4]);
+}
+__device__ __forceinline__ uint4 psum_pack(const uint32_t (&s)[5]) {
+  return make_uint4(s[0] | (s[1] << 16), s[2] | (s[3] << 16), s[4], 0u);
+}
+__device__ __forceinline__ bool interior(const Geo& g, int x, int y, int t) {
+  return x >= 2 && x < g.W - 2 && y >= 2 && y < g.H - 2 && t >= 2 && t < g.T - 2;
+}
+
+// every voxel: one thread per (x, y) column marching along t with a ring of the last five
+// per-frame 5x5 sums (25 gathers per voxel instead of 125)
+__global__ void __launch_bounds__(128) k_patch_sums_dense(LevelArgs a, uint4* __restrict__ psum) {
+  const int i = blockIdx.x * blockDim.x + threadIdx.x;
+  if (i >= a.g.HW) return;
+  const int y = i / a.g.W, x = i - y * a.g.W;
+  const bool ok = x >= 2 && x < a.g.W - 2 && y >= 2 && y < a.g.H - 2;
+  const unsigned long long* v = reinterpret_cast<const unsigned long long*>(a.vox);
+  uint32_t f0[5] = {0, 0, 0, 0, 0}, f1[5] = {0, 0, 0, 0, 0}, f2[5] = {0, 0, 0, 0, 0}, f3[5] = {0, 0, 0, 0, 0};
+  uint32_t S[5] = {0, 0, 0, 0, 0};  // sum of the ring
+  for (int t = 0; t < a.g.T; ++t) {
+    uint32_t n[5] = {0, 0, 0, 0, 0};
+    if (ok) {
+      const unsigned long long* c = v + (int64_t)t * a.g.HW + i;
+#pragma unroll
+      for (int dy = -2; dy <= 2; ++dy)
+#pragma unroll
+        for (int dx = -2; dx <= 2; ++dx) vox_add(__ldg(c + dy * a.g.W + dx), n);
+    }
+#pragma unroll
+    for (int c = 0; c < 5; ++c) {
+      S[c] += n[c];  // ring = frames t-4 .. t, centre t-2
+    }
+    if (t >= 4) psum[(int64_t)(t - 2) * a.g.HW + i] = ok ? psum_pack(S) : make_uint4(0, 0, 0, 0);
+#pragma unroll
+    for (int c = 0; c < 5; ++c) {
+      S[c] -= f0[c];
+      f0[c] = f1[c];
+      f1[c] = f2[c];
+      f2[c] = f3[c];
+      f3[c] = n[c];
+    }
+  }
+  // centres without a full patch along t
+  for (int t = 0; t < a.g.T; ++t)
+    if (t < 2 || t >= a.g.T - 2) psum[(int64_t)t * a.g.HW + i] = make_uint4(0, 0, 0, 0);
+}
+
+// the targets of slots [b, e) on the current u (thread per target, x-adjacent lanes)
+__global__ void __launch_bounds__(128) k_patch_sums_targets(LevelArgs a, uint4* __restrict__ psum, int32_t b,
+                                                            int32_t e) {
+  const int s = b + blockIdx.x * blockDim.x + threadIdx.x;
+  if (s >= e) return;
+  const int p = __ldg(a.targets + s);
+  int px, py, pt;
+  decode(a.g, p, px, py, pt);
+  if (!interior(a.g, px, py, pt)) return;
+  const unsigned long long* v = reinterpret_cast<const unsigned long long*>(a.vox) + p;
+  uint32_t S[5] = {0, 0, 0, 0, 0};
+#pragma unroll 1
+  for (int dt = -2; dt <= 2; ++dt)
+#pragma unroll
+    for (int dy = -2; dy <= 2; ++dy)
+#pragma unroll
+      for (int dx = -2; dx <= 2; ++dx) vox_add(__ldg(v + dt * a.g.HW + dy * a.g.W + dx), S);
+  psum[p] = psum_pack(S);
+}
+
+// 4 |dS_rgb|^2 + lambda |dS_T|^2 >= 125 D_incumbent: the candidate cannot strictly improve
+__device__ __forceinline__ bool lb_reject(const uint4 sp, const uint4 sq, int lambda, uint64_t thr) {
+  const int dR = (int)(sp.x & 0xffffu) - (int)(sq.x & 0xffffu), dG = (int)(sp.x >> 16) - (int)(sq.x >> 16);
+  const int dB = (int)(sp.y & 0xffffu) - (int)(sq.y & 0xffffu), dX = (int)(sp.y >> 16) - (int)(sq.y >> 16);
+  const int dY = (int)(sp.z & 0xffffu) - (int)(sq.z & 0xffffu);
+  const uint32_t c = (uint32_t)(dR * dR) + (uint32_t)(dG * dG) + (uint32_t)(dB * dB);  // <= 3 * 31875^2 < 2^32
+  const uint64_t t = (uint64_t)(uint32_t)(dX * dX) + (uint32_t)(dY * dY);
+  return 4ull * c + (uint64_t)lambda * t >= thr;
 }
 
 // ------------------------------------------------------------------ a6: propagation pass
@@ -792,6 +881,7 @@ __global__ void __launch_bounds__(32 * WPB, VINP_MINB * 8 / WPB) k_random_search
   int* cand = s_cand[threadIdx.x >> 5];
   int2* pairs = s_pairs[threadIdx.x >> 5];
   int nc = 0;
+  unsigned rej = 0;  // R42: bit j = candidate j rejected by the lower bound
   int px = 0, py = 0, pt = 0;
   if (act) {
     decode(a.g, p, px, py, pt);
@@ -812,9 +902,29 @@ __global__ void __launch_bounds__(32 * WPB, VINP_MINB * 8 / WPB) k_random_search
         if (!dup) cand[(nc++) * 32 + lane] = qq;
       }
     }
+    // R42: candidates whose patch-sum lower bound already reaches the incumbent's D cannot win;
+    // they stay in `cand` (de-duplication, counts) but are not evaluated
+    if (a.psum && nc > 0 && interior(a.g, px, py, pt)) {
+      const uint64_t thr = 125ull * e_D(inc);
+      if (thr == 0) {
+        rej = 0xffffffffu;
+      } else {
+        const uint4 sp = __ldg(a.psum + p);
+#pragma unroll 1
+        for (int j0 = 0; j0 < nc; j0 += 4) {
+          uint4 sq[4];
+#pragma unroll
+          for (int j = 0; j < 4; ++j) sq[j] = __ldg(a.psum + (j0 + j < nc ? cand[(j0 + j) * 32 + lane] : p));
+#pragma unroll
+          for (int j = 0; j < 4; ++j)
+            if (j0 + j < nc && lb_reject(sp, sq[j], lambda, thr)) rej |= 1u << (j0 + j);
+        }
+      }
+    }
   }
-  // flatten (owner lane, rank) pairs in lane order
-  int incl = nc;
+  // flatten (owner lane, rank) pairs in lane order: the candidates that are left
+  const int ns = nc - __popc(rej & (nc >= 32 ? 0xffffffffu : ((1u << nc) - 1u)));
+  int incl = ns;
 #pragma unroll
   for (int d = 1; d < 32; d <<= 1) {
     int y = __shfl_up_sync(kFull, incl, d);
@@ -823,7 +933,8 @@ __global__ void __launch_bounds__(32 * WPB, VINP_MINB * 8 / WPB) k_random_search
   int P = __shfl_sync(kFull, incl, 31);
 #if VINP_RS_ORDER == 0
   // lane-major (owner, rank) order
-  for (int j = 0; j < nc; ++j) pairs[incl - nc + j] = make_int2(cand[j * 32 + lane], (j << 5) | lane);
+  for (int j = 0, o = incl - ns; j < nc; ++j)
+    if (!((rej >> j) & 1u)) pairs[o++] = make_int2(cand[j * 32 + lane], (j << 5) | lane);
 #else
   // rank-major: all owners' candidates of one rank together (1: rank 0 first, 2: last rank first),
   // so that a warp iteration's pairs have similar radii; the rank stays the tie key
@@ -831,8 +942,9 @@ __global__ void __launch_bounds__(32 * WPB, VINP_MINB * 8 / WPB) k_random_search
     int base = 0;
     for (int jr = 0; jr < NC; ++jr) {
       const int j = VINP_RS_ORDER == 1 ? jr : NC - 1 - jr;
-      const unsigned mk = __ballot_sync(kFull, j < nc);
-      if (j < nc) pairs[base + __popc(mk & ((1u << lane) - 1u))] = make_int2(cand[j * 32 + lane], (j << 5) | lane);
+      const bool keep = j < nc && !((rej >> j) & 1u);
+      const unsigned mk = __ballot_sync(kFull, keep);
+      if (keep) pairs[base + __popc(mk & ((1u << lane) - 1u))] = make_int2(cand[j * 32 + lane], (j << 5) | lane);
       base += __popc(mk);
     }
   }
@@ -845,7 +957,9 @@ __global__ void __launch_bounds__(32 * WPB, VINP_MINB * 8 / WPB) k_random_search
     put_e(eout, mo, s, pack_e(bestD, bestq));
     if (sout) put_u8(sout, mo.st, mo.n, s, bestq != e_q(inc) ? (uint8_t)pass : __ldg(sin + s));
   }
-  if (lane == 0) flush_count(counter, (unsigned)P);
+  // rejected candidates count as patch-updates too (R34: tested against the incumbent)
+  const unsigned tot = __reduce_add_sync(kFull, (unsigned)nc);
+  if (lane == 0) flush_count(counter, tot);
 }
 
 // Random search for onion (K-restricted) launches, warp per target: lane i < M draws candidate
@@ -1128,6 +1242,12 @@ vinp_status launch_evaluate(const vinp_level* lv, vinp_nnf* nnf, const vinp_para
           args_of(lv), nnf->e, nnf->n, nnf->stamp, prm->lambda, kb, only_layer, b, e, list, counter,
           mirror_of(nnf));
     count_launch();
+    if (kb < 0 && lv->psum) {  // R42: the targets' patch sums on the u this search runs on
+      const int32_t sb = list ? 0 : b, se = list ? lv->n_targets : e;  // list launches: every target
+      k_patch_sums_targets<<<nblk(se - sb, 128), 128, 0, S(stream)>>>(args_of(lv), reinterpret_cast<uint4*>(lv->psum),
+                                                                      sb, se);
+      count_launch();
+    }
   }
   return check_launch("vinp_nnf_evaluate");
 }
@@ -1344,6 +1464,27 @@ vinp_status vinp_brute_force_list(const vinp_level* lv, vinp_nnf* out, const vin
     count_launch();
   }
   return check_launch("vinp_brute_force_list");
+}
+
+vinp_status vinp_patch_sums(const vinp_level* lv, int which, int32_t b, int32_t e, void* stream) {
+  VINP_NVTX();
+  vinp_status st = check_level(lv, "vinp_patch_sums");
+  if (st) return st;
+  VINP_REQUIRE(lv->psum, "vinp_patch_sums: lv->psum is NULL");
+  VINP_REQUIRE(which == 0 || which == 1, "vinp_patch_sums: which must be 0 (all voxels) or 1 (targets)");
+  if (which == 0) {
+    k_patch_sums_dense<<<nblk(lv->W * lv->H, 128), 128, 0, S(stream)>>>(args_of(lv),
+                                                                        reinterpret_cast<uint4*>(lv->psum));
+    count_launch();
+  } else {
+    VINP_REQUIRE(lv->targets && b >= 0 && b <= e && e <= lv->n_targets, "vinp_patch_sums: bad slot range");
+    if (e > b) {
+      k_patch_sums_targets<<<nblk(e - b, 128), 128, 0, S(stream)>>>(args_of(lv), reinterpret_cast<uint4*>(lv->psum),
+                                                                    b, e);
+      count_launch();
+    }
+  }
+  return check_launch("vinp_patch_sums");
 }
 
 vinp_status vinp_patch_ssd(const vinp_level* lv, const int32_t* p, const int32_t* q, int64_t n,

@@ -46,6 +46,15 @@ __device__ __forceinline__ uint8_t round_u8(float x) {
   return (uint8_t)floor((double)x + 0.5);
 }
 
+#ifndef VINP_REC_PREFETCH
+#define VINP_REC_PREFETCH 0  // 1: stage A (slot gathers) of the next hole issued before this hole's arithmetic (A/B: 17.5 vs 17.5-17.9 ms, 44 B of spills at 64 registers; 85 registers: 18.9 ms)
+#endif
+#ifndef VINP_REC_WAVES
+#define VINP_REC_WAVES 2
+#endif
+#ifndef VINP_REC_MINB
+#define VINP_REC_MINB 4
+#endif
 #ifndef VINP_REC_V2
 #define VINP_REC_V2 1  // adaptive rank search, table-driven weights (0: the round-1 forms, for A/B)
 #endif
@@ -134,20 +143,22 @@ struct LaneVox {
   bool real[4];  // v < 125
 };
 
-__device__ __forceinline__ void recon_hole(const ReconArgs& a, const LaneVox& LV, int lane, int mode, int layer_j,
-                                           int h, float* __restrict__ out_rgb, float* __restrict__ out_tex,
-                                           int commit, const double2* __restrict__ tab) {
-  int p = a.holes[h];
-  if (layer_j >= 0 && a.layer[p] != layer_j) return;
+// Stage A of a hole: its voxel, which of the lane's four contributors exist, and their slot loads.
+// Issued one hole ahead by the persistent loop (VINP_REC_PREFETCH), so that two of the four
+// dependent gather rounds of a hole overlap the arithmetic of the previous one.
+struct HoleA {
+  int h, p;
+  int sl[4];
+  unsigned cand;  // bit i: contributor i is a voxel of N_p in Omega (and in an earlier layer)
+};
+
+__device__ __forceinline__ HoleA recon_stage_a(const ReconArgs& a, const LaneVox& LV, int layer_j, int h) {
+  HoleA A;
+  A.h = h;
+  const int p = a.holes[h];
+  A.p = p;
   int px, py, pt;
   decode(a.g, p, px, py, pt);
-  // Gather in three dependent rounds with all four contributors of the lane in flight per round
-  // (branch-free: out-of-range entries read a safe address and are masked): slot[q]; then the NNF
-  // entry and n of that slot; then the proposed value u(p + phi(q)) = vox[src_q - off].
-  uint32_t Dq[4], nq[4];
-  uint64_t val[4];
-  unsigned valid = 0;
-  bool n125 = true;
   const int* off = LV.off;
   bool cand[4];
   // interior hole (the usual case): every voxel of N_p is in the volume, no per-voxel test
@@ -156,12 +167,38 @@ __device__ __forceinline__ void recon_hole(const ReconArgs& a, const LaneVox& LV
   for (int i = 0; i < 4; ++i)
     cand[i] = LV.real[i] && (interior || inside(a.g, px + LV.dx[i], py + LV.dy[i], pt + LV.dt[i]));
   if (layer_j >= 0) {
+    const bool mine = a.layer[p] == layer_j;  // other layers' holes: no contributor, nothing written
 #pragma unroll
-    for (int i = 0; i < 4; ++i) cand[i] = cand[i] && a.layer[p + (cand[i] ? off[i] : 0)] < layer_j;
+    for (int i = 0; i < 4; ++i) cand[i] = cand[i] && mine && a.layer[p + (cand[i] ? off[i] : 0)] < layer_j;
   }
+  A.cand = 0;
+#pragma unroll
+  for (int i = 0; i < 4; ++i) {
+    A.sl[i] = __ldg(a.slot + p + (cand[i] ? off[i] : 0));
+    A.cand |= (unsigned)cand[i] << i;
+  }
+  return A;
+}
+
+__device__ __forceinline__ void recon_hole(const ReconArgs& a, const LaneVox& LV, int lane, int mode, int layer_j,
+                                           const HoleA& A, float* __restrict__ out_rgb, float* __restrict__ out_tex,
+                                           int commit, const double2* __restrict__ tab) {
+  const int h = A.h, p = A.p;
+  // Gather in three dependent rounds with all four contributors of the lane in flight per round
+  // (branch-free: out-of-range entries read a safe address and are masked): slot[q] (stage A); then
+  // the NNF entry and n of that slot; then the proposed value u(p + phi(q)) = vox[src_q - off].
+  uint32_t Dq[4], nq[4];
+  uint64_t val[4];
+  unsigned valid = 0;
+  bool n125 = true;
+  const int* off = LV.off;
+  bool cand[4];
   int sl[4];
 #pragma unroll
-  for (int i = 0; i < 4; ++i) sl[i] = __ldg(a.slot + p + (cand[i] ? off[i] : 0));
+  for (int i = 0; i < 4; ++i) {
+    cand[i] = (A.cand >> i) & 1u;
+    sl[i] = A.sl[i];
+  }
   uint64_t ev[4];
   uint32_t nv[4];
 #pragma unroll
@@ -367,7 +404,7 @@ __device__ __forceinline__ void recon_hole(const ReconArgs& a, const LaneVox& LV
 }
 
 // persistent warps over the holes [hb, he) (or list[hb..he)): the lane geometry is set up once
-__global__ void __launch_bounds__(256, 4) k_reconstruct(ReconArgs a, int mode, int layer_j, int32_t hb,
+__global__ void __launch_bounds__(32 * kWPB, VINP_REC_MINB * 8 / kWPB) k_reconstruct(ReconArgs a, int mode, int layer_j, int32_t hb,
                                                      int32_t he, const int32_t* __restrict__ list,
                                                      float* __restrict__ out_rgb,
                                                      float* __restrict__ out_tex, int commit) {
@@ -388,8 +425,24 @@ __global__ void __launch_bounds__(256, 4) k_reconstruct(ReconArgs a, int mode, i
     LV.real[i] = v < kPatch;
   }
   const int nw = gridDim.x * kWPB;
-  for (int idx = hb + blockIdx.x * kWPB + (threadIdx.x >> 5); idx < he; idx += nw)
-    recon_hole(a, LV, lane, mode, layer_j, list ? __ldg(list + idx) : idx, out_rgb, out_tex, commit, s_tab);
+  int idx = hb + blockIdx.x * kWPB + (threadIdx.x >> 5);
+  if (idx >= he) return;
+#if VINP_REC_PREFETCH
+  HoleA cur = recon_stage_a(a, LV, layer_j, list ? __ldg(list + idx) : idx);
+  for (;;) {
+    const int nidx = idx + nw;
+    const bool more = nidx < he;
+    const HoleA nxt = recon_stage_a(a, LV, layer_j, more ? (list ? __ldg(list + nidx) : nidx) : cur.h);
+    recon_hole(a, LV, lane, mode, layer_j, cur, out_rgb, out_tex, commit, s_tab);
+    if (!more) break;
+    cur = nxt;
+    idx = nidx;
+  }
+#else
+  for (; idx < he; idx += nw)
+    recon_hole(a, LV, lane, mode, layer_j, recon_stage_a(a, LV, layer_j, list ? __ldg(list + idx) : idx), out_rgb,
+               out_tex, commit, s_tab);
+#endif
 }
 
 __global__ void k_commit(Geo g, uint64_t* __restrict__ vox, const uint8_t* __restrict__ layer,
@@ -466,7 +519,7 @@ vinp_status launch_reconstruct(vinp_level* lv, const vinp_nnf* nnf, int mode, in
   VINP_REQUIRE(layer_j < 0 || lv->layer, "vinp_reconstruct: layer map required");
   if (he > hb) {
     ReconArgs a{geo_of(lv), lv->vox, lv->layer, lv->slot, lv->holes, nnf->e, nnf->n};
-    const int grid = (int)std::min<int64_t>(nblk(he - hb, kWPB), 148 * (64 / kWPB));  // persistent warps
+    const int grid = (int)std::min<int64_t>(nblk(he - hb, kWPB), 148 * (VINP_REC_MINB * 8 / kWPB) * VINP_REC_WAVES);  // persistent warps
     k_reconstruct<<<grid, 32 * kWPB, 0, S(stream)>>>(a, mode, layer_j, hb, he, list,
                                                                   out_rgb, out_tex, commit);
     count_launch();

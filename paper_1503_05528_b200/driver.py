@@ -59,6 +59,7 @@ class Config:
     graphs: bool = True
     stop_rule: int = 0          # 0: R19 e = ||u_H - v_H||_1 / (3|H|); 1: literal P:988 ||.||_2 / (3|H|)
     skip_stale: bool = True     # R41: exact skip of stale propagation candidates (NNF unchanged)
+    lower_bound: bool = True    # R42: exact patch-sum lower-bound rejection in random search (NNF unchanged)
 
     def params(self) -> V.Params:
         return V.Params(lam=self.lam, tex_half=self.tex_half, seed=self.seed, rho=self.rho)
@@ -214,6 +215,8 @@ class Inpainter:
         self.levels: List[V.Level] = []
         for l, (w, h, _) in enumerate(V.level_dims(W, H, T, cfg.levels), start=1):
             self.levels.append(V.Level.alloc(w, h, T, l, self.device))
+            if cfg.lower_bound and self.device.type == "cuda":  # 16 B per voxel (R42)
+                self.levels[-1].psum = torch.empty((w * h * T, 8), dtype=torch.int16, device=self.device)
         n1 = W * H * T
         self.ws = torch.empty(max(self.V.texture_ws_bytes(self.levels[0]), self.V.sets_ws_bytes(self.levels[0])) + 256,
                               dtype=torch.uint8, device=self.device)
@@ -237,6 +240,9 @@ class Inpainter:
         mask = mask.contiguous()
         self.V.build_pyramid(rgb, mask, self.levels)
         self.V.texture_features(self.prm, self.levels, self.ws)
+        for lv in self.levels:
+            if lv.psum is not None:
+                self.V.patch_sums(lv, 0)  # every voxel once (D~ never changes); targets: at each evaluate
         counts = self.V.build_sets(self.levels, self.ws)
         for lv in self.levels:
             if lv.n_sources == 0:

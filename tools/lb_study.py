@@ -41,6 +41,24 @@ def frame_sums(lv):
     return out
 
 
+def half_moments(lv):
+    """[3 axes, 5 channels, N] float32: sum of sign(offset along the axis) * channel over the 5x5x5 patch."""
+    vox = lv.vox.view(1, 1, lv.T, lv.H, lv.W)
+    sgn = torch.tensor([-1.0, -1.0, 0.0, 1.0, 1.0], device=vox.device)
+    one = torch.ones(5, device=vox.device)
+    ks = []
+    for ax in range(3):  # t, y, x kernels [5,5,5]
+        w = [one, one, one]
+        w[ax] = sgn
+        ks.append((w[0].view(5, 1, 1) * w[1].view(1, 5, 1) * w[2].view(1, 1, 5)).view(1, 1, 5, 5, 5))
+    out = torch.empty((3, 5, lv.T * lv.H * lv.W), dtype=torch.float32, device=vox.device)
+    for c, sh in enumerate((0, 8, 16, 32, 40)):
+        ch = ((vox >> sh) & 255).float()
+        for ax in range(3):
+            out[ax, c] = F.conv3d(ch, ks[ax], padding=2).round().view(-1)
+    return out
+
+
 def main():
     ap = argparse.ArgumentParser()
     ap.add_argument("--config", default="c5")
@@ -68,11 +86,12 @@ def main():
     rows = []
     V.nnf_evaluate(lv, st.a, ip.prm)
     e0 = st.a.e.clone()
-    for probe in (0, 2, 6):  # PM iterations already run when the candidates are drawn
+    for probe in (0, 4):  # PM iterations already run when the candidates are drawn
         if probe:
             st.a.e.copy_(e0)
             V.ann_search(lv, st.a, st.b, ip.prm, 0, probe)
         Fs = frame_sums(lv)
+        Hm = half_moments(lv)
         sl = torch.arange(args.sample, device="cuda", dtype=torch.int64) * (n // args.sample)
         p = lv.targets[:n][sl].long()
         e = st.a.e[:n][sl]
@@ -81,7 +100,7 @@ def main():
         px, py, pt = p % W, (p // W) % H, p // (W * H)
         interior = (px >= 2) & (px < W - 2) & (py >= 2) & (py < H - 2) & (pt >= 2) & (pt < T - 2)
         q0x, q0y, q0t = q0 % W, (q0 // W) % H, q0 // (W * H)
-        tot = dict(valid=0, lose=0, A=0, B=0, C=0, Aonly=0)
+        tot = dict(valid=0, lose=0, A=0, B=0, C=0, D=0, E=0, zero=0)
         per_radius = []
         R = float(max(W, H, T))
         i = 0
@@ -113,20 +132,28 @@ def main():
             lbB = (40 * (d[:3] ** 2).sum((0, 1)) + lam * dT ** 2) / 250.0
             # C: per-frame, all channels: 25 D >= 4 sum dS_fc^2 + lam sum dS_fT^2
             lbC = (4 * (d[:3] ** 2).sum((0, 1)) + lam * (d[3:] ** 2).sum((0, 1))) / 25.0
+            # D: A + half-difference moments (sign(dx), sign(dy), sign(dt)) of R, G, B;  E: of T too
+            dH = (Hm[:, :, pp] - Hm[:, :, qq]).double()  # [3, 5, n]
+            lbD = lbA + 4 * (dH[:, :3] ** 2).sum((0, 1)) / 100.0
+            lbE = lbD + lam * (dH[:, 3:] ** 2).sum((0, 1)) / 100.0
+            assert bool((lbE <= D + 1e-6).all())
             assert bool((lbA <= D + 1e-6).all()) and bool((lbB <= D + 1e-6).all()) and bool((lbC <= D + 1e-6).all())
             Dd = Di.double()
             r = dict(i=i, R=R, valid=int(ok.sum()), lose=int((D >= Di).sum()), A=int((lbA >= Dd).sum()),
-                     B=int((lbB >= Dd).sum()), C=int((lbC >= Dd).sum()))
+                     B=int((lbB >= Dd).sum()), C=int((lbC >= Dd).sum()), D=int((lbD >= Dd).sum()),
+                     E=int((lbE >= Dd).sum()), zero=int((Di == 0).sum()))
             per_radius.append(r)
-            for k in ("valid", "lose", "A", "B", "C"):
+            for k in ("valid", "lose", "A", "B", "C", "D", "E", "zero"):
                 tot[k] += r[k]
         row = dict(pm_iters_done=probe, targets=int(p.numel()), candidates=tot["valid"],
                    frac_lose=round(tot["lose"] / tot["valid"], 4),
                    reject_A=round(tot["A"] / tot["valid"], 4), reject_B=round(tot["B"] / tot["valid"], 4),
-                   reject_C=round(tot["C"] / tot["valid"], 4), per_radius=per_radius)
+                   reject_C=round(tot["C"] / tot["valid"], 4), reject_D=round(tot["D"] / tot["valid"], 4),
+                   reject_E=round(tot["E"] / tot["valid"], 4),
+                   frac_incumbent_zero=round(tot["zero"] / tot["valid"], 4), per_radius=per_radius)
         rows.append(row)
         print(json.dumps(row), flush=True)
-        del Fs
+        del Fs, Hm
 
 
 if __name__ == "__main__":
