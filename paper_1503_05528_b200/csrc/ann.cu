@@ -99,7 +99,7 @@ __global__ void k_upsample(LevelArgs c, const uint64_t* __restrict__ ce, LevelAr
 #define VINP_PROP_BIG (1 << 23)
 #endif
 #ifndef VINP_MINB
-#define VINP_MINB 3
+#define VINP_MINB 4
 #endif
 #ifndef VINP_PROP_MINB
 #define VINP_PROP_MINB 4
@@ -118,6 +118,12 @@ __global__ void k_upsample(LevelArgs c, const uint64_t* __restrict__ ce, LevelAr
 #endif
 #ifndef VINP_RS_ORDER
 #define VINP_RS_ORDER 1  // random-search pair list: 0 lane-major, 1/2 rank-major (ascending/descending); A/B: 1 is -0.7%
+#endif
+#ifndef VINP_RS_GEN_CHUNK
+#define VINP_RS_GEN_CHUNK 4  // random-search candidate generation: D~ flag loads in flight together per chunk
+#endif
+#ifndef VINP_PROP_LB
+#define VINP_PROP_LB 1  // R42 lower bound in propagation too
 #endif
 #ifndef VINP_RS_SMALL
 #define VINP_RS_SMALL (148 * 32 * 8)  // random-search launches below this many targets: 8 per warp
@@ -465,7 +471,7 @@ __global__ void __launch_bounds__(LIGHT ? 128 : 256, LIGHT ? VINP_PROP_LIGHT_MIN
   }
   int px = 0, py = 0, pt = 0;
   int q0 = e_q(inc);
-  unsigned nstale = 0;
+  unsigned nstale = 0, nlb = 0;
   if (act) {
     decode(a.g, p, px, py, pt);
     // candidate generation in three branch-free rounds, every load of a round in flight together
@@ -526,6 +532,35 @@ __global__ void __launch_bounds__(LIGHT ? 128 : 256, LIGHT ? VINP_PROP_LIGHT_MIN
         q[c] = -1;
         ++nstale;
       }
+#if VINP_PROP_LB
+    // R42: then the candidates whose patch-sum lower bound reaches the incumbent's D (every one if
+    // that D is 0): tested against the incumbent, hence counted, but no patch row is read
+    if (a.psum && kb < 0 && interior(a.g, px, py, pt)) {
+      bool any = false;
+#pragma unroll
+      for (int c = 0; c < NCMAX; ++c) any |= q[c] >= 0;
+      const uint64_t thr = 125ull * e_D(inc);
+      if (any && thr == 0) {
+#pragma unroll
+        for (int c = 0; c < NCMAX; ++c)
+          if (q[c] >= 0) {
+            q[c] = -1;
+            ++nlb;
+          }
+      } else if (!LIGHT && any) {  // (the R41-active passes keep only the free D = 0 test: A/B)
+        const uint4 sp = __ldg(a.psum + p);
+        uint4 sq[NCMAX];
+#pragma unroll
+        for (int c = 0; c < NCMAX; ++c) sq[c] = __ldg(a.psum + (q[c] >= 0 ? q[c] : p));
+#pragma unroll
+        for (int c = 0; c < NCMAX; ++c)
+          if (q[c] >= 0 && lb_reject(sp, sq[c], lambda, thr)) {
+            q[c] = -1;
+            ++nlb;
+          }
+      }
+    }
+#endif
   }
   // compact this lane's candidates to the front (rank order kept), so that the warp runs the
   // SSD loop once per candidate *slot* rather than once per neighbour rank any lane has
@@ -544,7 +579,7 @@ __global__ void __launch_bounds__(LIGHT ? 128 : 256, LIGHT ? VINP_PROP_LIGHT_MIN
   }
   uint32_t bestD = e_D(inc);
   int bestq = q0;
-  unsigned cnt = 0;
+  unsigned cnt = nlb;  // R42 rejections are patch-updates too
 #if VINP_PROP_SPARSE > 0
   {
     // Sparse warp (few live candidates, typical once the R41 skip has removed the stale ones):
@@ -572,8 +607,9 @@ __global__ void __launch_bounds__(LIGHT ? 128 : 256, LIGHT ? VINP_PROP_LIGHT_MIN
         if (sout) put_u8(sout, mo.st, mo.n, s, bestq != q0 ? (uint8_t)pass : __ldg(sin + s));
       }
       nstale = __reduce_add_sync(kFull, nstale);
+      cnt = __reduce_add_sync(kFull, cnt);
       if ((threadIdx.x & 31) == 0) {
-        flush_count(counter, (unsigned)P);
+        flush_count(counter, (unsigned)P + cnt);
         if (counter && nstale) flush_count(counter + 1, nstale);
       }
       return;
@@ -599,7 +635,7 @@ __global__ void __launch_bounds__(LIGHT ? 128 : 256, LIGHT ? VINP_PROP_LIGHT_MIN
       accc[c] = acct[c] = 0;
       if (c < ncand) alive |= 1u << c;
     }
-    cnt = ncand;
+    cnt += ncand;
     const uint32_t thr = bestD;
 #pragma unroll 1
     for (int dt = -2; dt <= 2; ++dt) {
@@ -888,6 +924,36 @@ __global__ void __launch_bounds__(32 * WPB, VINP_MINB * 8 / WPB) k_random_search
     int q0 = e_q(inc);
     int q0x, q0y, q0t;
     decode(a.g, q0, q0x, q0y, q0t);
+#if VINP_RS_GEN_CHUNK > 1
+    // candidates i + 1 of Eq. 3 in chunks: the Philox draws of a chunk, then its D~ flag loads in
+    // flight together, then the de-duplication in rank order
+    for (int i0 = 0; i0 < rad.M; i0 += VINP_RS_GEN_CHUNK) {
+      int qv[VINP_RS_GEN_CHUNK];
+#pragma unroll
+      for (int j = 0; j < VINP_RS_GEN_CHUNK; ++j) {
+        const int i = min(i0 + j, rad.M - 1);
+        uint4 u = draw((uint32_t)p, (uint32_t)pm_iter, a.level, kStreamRS, i + 1, oc, seed);
+        double R = rad.R[i];
+        int ox = (int)floor(__dmul_rn(R, __dmul_rn((double)u.x - 2147483648.0, 4.656612873077392578125e-10)));
+        int oy = (int)floor(__dmul_rn(R, __dmul_rn((double)u.y - 2147483648.0, 4.656612873077392578125e-10)));
+        int ot = (int)floor(__dmul_rn(R, __dmul_rn((double)u.z - 2147483648.0, 4.656612873077392578125e-10)));
+        int qx = q0x + ox, qy = q0y + oy, qt = q0t + ot;
+        qv[j] = (i0 + j < rad.M && inside(a.g, qx, qy, qt)) ? lin(a.g, qx, qy, qt) : -1;
+      }
+      uint32_t fl[VINP_RS_GEN_CHUNK];
+#pragma unroll
+      for (int j = 0; j < VINP_RS_GEN_CHUNK; ++j) fl[j] = __ldg(a.flags + (qv[j] >= 0 ? qv[j] : p));
+#pragma unroll
+      for (int j = 0; j < VINP_RS_GEN_CHUNK; ++j) {
+        if (qv[j] >= 0 && (fl[j] & 2)) {
+          const int qq = qv[j];
+          bool dup = qq == q0;
+          for (int k = 0; k < nc; ++k) dup |= (cand[k * 32 + lane] == qq);
+          if (!dup) cand[(nc++) * 32 + lane] = qq;
+        }
+      }
+    }
+#else
     for (int i = 0; i < rad.M; ++i) {  // candidate i + 1 of Eq. 3
       uint4 u = draw((uint32_t)p, (uint32_t)pm_iter, a.level, kStreamRS, i + 1, oc, seed);
       double R = rad.R[i];
@@ -902,6 +968,7 @@ __global__ void __launch_bounds__(32 * WPB, VINP_MINB * 8 / WPB) k_random_search
         if (!dup) cand[(nc++) * 32 + lane] = qq;
       }
     }
+#endif
     // R42: candidates whose patch-sum lower bound already reaches the incumbent's D cannot win;
     // they stay in `cand` (de-duplication, counts) but are not evaluated
     if (a.psum && nc > 0 && interior(a.g, px, py, pt)) {

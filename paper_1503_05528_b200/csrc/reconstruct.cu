@@ -55,9 +55,6 @@ __device__ __forceinline__ uint8_t round_u8(float x) {
 #ifndef VINP_REC_MINB
 #define VINP_REC_MINB 4
 #endif
-#ifndef VINP_REC_V2
-#define VINP_REC_V2 1  // adaptive rank search, table-driven weights (0: the round-1 forms, for A/B)
-#endif
 
 // 2^(j/128) = hi (1 + tail), j = 0..127 (tools/gen_exp_table.py); staged in shared memory per block
 __device__ const double2 kExpTab[128] = {
@@ -265,25 +262,7 @@ __device__ __forceinline__ void recon_hole(const ReconArgs& a, const LaneVox& LV
       hi[i] = n125 ? (uint32_t)key[i] : (uint32_t)(key[i] >> 32);  // ~0 for invalid
       lo[i] = n125 ? 0u : (uint32_t)key[i];
     }
-#if VINP_REC_V2
     const uint32_t ans = select_rank32(hi, valid, r, m);
-#else
-    uint32_t hmin = __reduce_min_sync(kFull, min(min(hi[0], hi[1]), min(hi[2], hi[3])));
-    uint32_t hmax = __reduce_max_sync(kFull, max(max((valid & 1) ? hi[0] : 0u, (valid & 2) ? hi[1] : 0u),
-                                                 max((valid & 4) ? hi[2] : 0u, (valid & 8) ? hi[3] : 0u)));
-    uint32_t x = hmax ^ hmin;
-    uint32_t ans = hmin & ~(x ? (0xffffffffu >> __clz(x)) : 0u);
-    // invalid keys are ~0, above every threshold T (valid high halves are < 2^31: D < 2^31, and
-    // a positive double has sign bit 0), so the counts need no validity test
-    for (int bit = 31 - (x ? __clz(x) : 32); bit >= 0; --bit) {
-      uint32_t T = ans | ((1u << bit) - 1);
-      uint32_t c = 0;
-#pragma unroll
-      for (int i = 0; i < 4; ++i) c += hi[i] <= T;
-      c = __reduce_add_sync(kFull, c);
-      if (c < r) ans |= 1u << bit;
-    }
-#endif
     uint32_t lans = 0;
     if (!n125) {
       uint32_t below = 0, lmin = 0xffffffffu, lmax = 0;
@@ -329,36 +308,32 @@ __device__ __forceinline__ void recon_hole(const ReconArgs& a, const LaneVox& LV
       Ds = __shfl_sync(kFull, myD, src);
       ns = __shfl_sync(kFull, myn, src);
     }
-#if VINP_REC_V2
-    // a = D_q / (2 D_s) with all n = 125: the correctly rounded quotient from the correctly rounded
-    // reciprocal y = RN(1/b) (once per hole), q = RN(a y), r = a - q b (exact, FMA), RN(q + r y)
-    // (Markstein's theorem; b = 2 D_s < 2^32 has no all-ones significand) — equal to __ddiv_rn
-    // (host check of the same arithmetic: 3.2e9 random and 3.6e8 exhaustive small pairs, 0 differ)
-    const double den = (double)(2ull * Ds), rcp = Ds ? __drcp_rn(den) : 0.0;
-#endif
+    if (Ds == 0) {  // sigma_p = 0: the mean over the zero-distance contributors (R11)
 #pragma unroll
-    for (int i = 0; i < 4; ++i) {
-      if (!(valid >> i & 1)) { w[i] = 0; continue; }
-      if (Ds == 0) {
-        w[i] = Dq[i] == 0;
-#if VINP_REC_V2
-      } else if (n125) {
+      for (int i = 0; i < 4; ++i) w[i] = ((valid >> i) & 1u) && Dq[i] == 0;
+    } else if (n125) {
+      // a = D_q / (2 D_s) with all n = 125: the correctly rounded quotient from the correctly rounded
+      // reciprocal y = RN(1/b) (once per hole), q = RN(a y), r = a - q b (exact, FMA), RN(q + r y)
+      // (Markstein's theorem; b = 2 D_s < 2^32 has no all-ones significand) — equal to __ddiv_rn
+      // (host check of the same arithmetic: 3.2e9 random and 3.6e8 exhaustive small pairs, 0 differ).
+      // Branch-free over the lane's four contributors (an absent one has D_q = 0 and is masked).
+      const double den = (double)(2ull * Ds), rcp = __drcp_rn(den);
+#pragma unroll
+      for (int i = 0; i < 4; ++i) {
         const double an = __dadd_rn(__hiloint2double(0x43300000, (int)Dq[i]), -4503599627370496.0);  // (double)D_q
         const double q0 = __dmul_rn(an, rcp);
         const double aa = __fma_rn(__fma_rn(-q0, den, an), rcp, q0);
-        w[i] = weight36(aa, tab);
-      } else {
+        const int64_t wi = weight36(aa, tab);
+        w[i] = ((valid >> i) & 1u) ? wi : 0;
+      }
+    } else {
+      // partial patches (volume border): a = D_q n_s / (2 n_q D_s), one correctly rounded division
+      // of exact operands (R32)
+#pragma unroll
+      for (int i = 0; i < 4; ++i) {
         const double aa = __ddiv_rn((double)((uint64_t)Dq[i] * ns), (double)(2ull * nq[i] * Ds));
-        w[i] = weight36(aa, tab);
-#else
-      } else {
-        // a = D_q n_s / (2 n_q D_s): one correctly rounded division of exact operands (with all
-        // n = 125 the same real quotient as D_q / (2 D_s), hence the same double)
-        double an = n125 ? (double)Dq[i] : (double)((uint64_t)Dq[i] * ns);
-        double ad = n125 ? (double)(2ull * Ds) : (double)(2ull * nq[i] * Ds);
-        double aa = __ddiv_rn(an, ad);
-        w[i] = __double2ll_rn(__dmul_rn(exp(-aa), 68719476736.0));
-#endif
+        const int64_t wi = weight36(aa, tab);
+        w[i] = ((valid >> i) & 1u) ? wi : 0;
       }
     }
   }
