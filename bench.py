@@ -314,10 +314,15 @@ def main():
                            "pm_iters": c.pm_iters, "patch": "5x5x5", "lambda": c.lam,
                            "l2": "inputs larger than L2 (level-1 volume 1.66 GB)",
                            "parallelism": f"target slabs x{world}",
-                           "exchange": args.exchange if world > 1 else None},
+                           "exchange": args.exchange if world > 1 else None,
+                           # False: the R41-active passes flag the targets that read a changed entry
+                           # (vinp_level.active) and never enumerate the stale candidates of the others
+                           "count_stale": bool(cfg.count_stale)},
                 "patch_updates_per_step": pu // args.steps,
-                # R41: stale propagation candidates proven unable to win, skipped (not patch-updates)
-                "stale_skipped_per_step": stale // args.steps, "sec_per_step": ms / args.steps / 1000.0,
+                # R41: stale propagation candidates proven unable to win, skipped (not patch-updates);
+                # counted only with Config(count_stale=True) (2,319,233,053 per c5 step)
+                "stale_skipped_per_step": (stale // args.steps) if cfg.count_stale else None,
+                "sec_per_step": ms / args.steps / 1000.0,
                 "sec_per_level": levels,
                 "roofline": roof, "cpu_baseline": cpu, "e2e": e2e, "quality": quality, "gpu_launches": launches,
                 "clocks": clk.summary()}

@@ -70,6 +70,8 @@ typedef struct {
   int32_t* sources; int32_t n_sources;
   uint16_t* psum;    /* [T][H][W][8] patch sums for the random-search lower bound (R42), or NULL:
                         see vinp_patch_sums */
+  uint32_t* active;  /* workspace of vinp_active_ws_bytes(lv) bytes, zeroed once by the caller, or
+                        NULL: see vinp_propagate */
 } vinp_level;
 
 /* Other ranks' copies of one NNF buffer (NEXT #4 second stage, multi-GPU "fused" exchange): every
@@ -176,7 +178,12 @@ vinp_status vinp_nnf_evaluate(const vinp_level* lv, vinp_nnf* nnf, const vinp_pa
  * `since`; it was then tested against this target (or equalled its incumbent), whose D has not
  * grown since, so it cannot win (strict improvement) and is not evaluated: the NNF is identical
  * to the unskipped pass.  Such candidates are counted in counter[1] (counter then points to two
- * u64), not in counter[0].  out->stamp[s] = pass if e[s] changed, else in->stamp[s]. */
+ * u64), not in counter[0].  out->stamp[s] = pass if e[s] changed, else in->stamp[s].
+ * With lv->active set (whole-range passes with since > 0, only_layer < 0 and no mirror), a first
+ * kernel copies every entry and stamp to `out` and lists the targets that read an entry changed
+ * since `since`; the pass then runs over that list alone: the other targets receive stale proposals
+ * only and keep their entry.  The NNF, the stamps and counter[0] are identical; counter[1] is then
+ * NOT updated (the stale candidates of unlisted targets are never enumerated). */
 vinp_status vinp_propagate(const vinp_level* lv, const vinp_nnf* in, vinp_nnf* out,
                            const vinp_params* prm, int step, int sign, int kb, int only_layer,
                            int32_t b, int32_t e, int pass, int since, unsigned long long* counter,
@@ -198,6 +205,10 @@ vinp_status vinp_propagate(const vinp_level* lv, const vinp_nnf* in, vinp_nnf* o
  * that starts with evaluate (as every ANN search does) always sees sums of the current u.
  * VINP_E_INVALID if lv->psum is NULL. */
 vinp_status vinp_patch_sums(const vinp_level* lv, int which, int32_t b, int32_t e, void* stream);
+
+/* Bytes of the lv->active workspace (list length, a bitmap over the target slots, the list) for
+ * lv->n_targets targets; the caller zeroes it once after vinp_build_sets. */
+size_t vinp_active_ws_bytes(const vinp_level* lv);
 
 /* ---- a7: random search (Eq. 3, Alg. 1; R1, R3, R7) ----
  * v0 = in(p); for i = 1, 2, ...: R_i = rmax * rho^i (repeated fp64 multiplication) while

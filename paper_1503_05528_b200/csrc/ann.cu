@@ -29,11 +29,12 @@ struct LevelArgs {
   int32_t n_sources;
   int level;
   const uint4* psum;  // R42 patch sums, or null
+  int32_t n_targets;
 };
 static LevelArgs args_of(const vinp_level* lv) {
   return LevelArgs{geo_of(lv), lv->vox,     lv->flags,     lv->layer, lv->slot,
                    lv->targets, lv->sources, lv->n_sources, lv->level,
-                   reinterpret_cast<const uint4*>(lv->psum)};
+                   reinterpret_cast<const uint4*>(lv->psum), lv->n_targets};
 }
 
 __device__ __forceinline__ int lin(const Geo& g, int x, int y, int t) {
@@ -436,6 +437,72 @@ __device__ __forceinline__ bool lb_reject(const uint4 sp, const uint4 sq, int la
   return 4ull * c + (uint64_t)lambda * t >= thr;
 }
 
+// ------------------------------------------------------------------ R41: targets with a live proposal
+// Before an R41-active pass over the whole level (single GPU, lv->active): every target copies its
+// entry and stamp to the output buffer, and every target whose entry changed since the previous
+// pass with the same (step, sign) (stamp >= since) appends the targets that read it in this pass,
+// p - sign*step*e_axis (both signs for sign = 0), in a bitmap; k_prop_compact turns it into a list.
+// Only the listed targets can have a non-stale proposal; the propagation kernel then runs over the
+// list alone.  Workspace words: [0] the list length (zeroed by the launcher), [8 ..) the bitmap
+// (all zero between passes), then the list.
+__host__ __device__ inline size_t active_bitmap_words(int32_t n) { return ((size_t)n + 31) / 32; }
+__global__ void __launch_bounds__(256) k_prop_mark(LevelArgs a, const uint64_t* __restrict__ ein,
+                                                   uint64_t* __restrict__ eout, const uint8_t* __restrict__ sin,
+                                                   uint8_t* __restrict__ sout, uint32_t* __restrict__ ws, int step,
+                                                   int sign, int since, int32_t n) {
+  const int s = blockIdx.x * blockDim.x + threadIdx.x;
+  if (s >= n) return;
+  const uint8_t st = __ldg(sin + s);
+  eout[s] = __ldg(reinterpret_cast<const unsigned long long*>(ein) + s);
+  sout[s] = st;
+  if ((int)st < since) return;
+  uint32_t* bitmap = ws + 8;
+  const int p = __ldg(a.targets + s);
+  int px, py, pt;
+  decode(a.g, p, px, py, pt);
+#pragma unroll
+  for (int c = 0; c < 6; ++c) {
+    const int sg = c < 3 ? -1 : 1;  // reader = p - sg' * step * e_axis for each neighbour sign sg' of the pass
+    if (sign != 0 && sg != -sign) continue;
+    const int ax = c % 3;
+    const int x = px + (ax == 0 ? sg * step : 0), y = py + (ax == 1 ? sg * step : 0), t = pt + (ax == 2 ? sg * step : 0);
+    if (!inside(a.g, x, y, t)) continue;
+    const int r = __ldg(a.slot + lin(a.g, x, y, t));
+    if (r < 0) continue;
+    atomicOr(bitmap + (r >> 5), 1u << (r & 31));
+  }
+}
+
+// the flagged slots in ascending order within each group of 1024 (x-adjacent targets stay adjacent,
+// so the pass's gathers coalesce as in the whole-range kernel); clears the bitmap
+__global__ void __launch_bounds__(256) k_prop_compact(uint32_t* __restrict__ ws, int32_t n) {
+  const size_t words = active_bitmap_words(n);
+  const size_t w = (size_t)blockIdx.x * blockDim.x + threadIdx.x;
+  uint32_t* bitmap = ws + 8;
+  int32_t* list = reinterpret_cast<int32_t*>(bitmap + words);
+  uint32_t word = w < words ? bitmap[w] : 0u;
+  if (word) bitmap[w] = 0u;
+  const int lane = threadIdx.x & 31;
+  const int c = __popc(word);
+  int incl = c;
+#pragma unroll
+  for (int d = 1; d < 32; d <<= 1) {
+    const int y = __shfl_up_sync(kFull, incl, d);
+    if (lane >= d) incl += y;
+  }
+  const int total = __shfl_sync(kFull, incl, 31);
+  if (total == 0) return;
+  uint32_t base = 0;
+  if (lane == 31) base = atomicAdd(ws, (uint32_t)total);
+  base = __shfl_sync(kFull, base, 31);
+  uint32_t off = base + incl - c;
+  while (word) {
+    const int bpos = __ffs(word) - 1;
+    word &= word - 1u;
+    list[off++] = (int32_t)(w * 32 + bpos);
+  }
+}
+
 // ------------------------------------------------------------------ a6: propagation pass
 // Lane = target (thread-per-target, coherent candidates).  Candidates of rank 1..3 are evaluated
 // one rank at a time by all lanes that have one, each against the running best of its own target
@@ -452,7 +519,15 @@ __global__ void __launch_bounds__(LIGHT ? 128 : 256, LIGHT ? VINP_PROP_LIGHT_MIN
                                                    int sign, int kb, int only_layer, int32_t b,
                                                    int32_t e, int pass, int since,
                                                    const int32_t* __restrict__ list,
-                                                   unsigned long long* counter, Mirror mo) {
+                                                   unsigned long long* counter, Mirror mo,
+                                                   uint32_t* __restrict__ active) {
+  if (active) {
+    // the pass runs over the list k_prop_mark built (the entries of the other targets are already
+    // copied): [b, e) becomes [0, list length)
+    e = (int32_t)active[0];
+    list = reinterpret_cast<const int32_t*>(active + 8 + active_bitmap_words(a.n_targets));
+    if ((int)(blockIdx.x * blockDim.x) >= e) return;
+  }
   int idx = b + blockIdx.x * blockDim.x + threadIdx.x;
   bool have = idx < e;
   int s = have ? (list ? __ldg(list + idx) : idx) : 0;
@@ -606,7 +681,7 @@ __global__ void __launch_bounds__(LIGHT ? 128 : 256, LIGHT ? VINP_PROP_LIGHT_MIN
         put_e(eout, mo, s, pack_e(bestD, bestq));
         if (sout) put_u8(sout, mo.st, mo.n, s, bestq != q0 ? (uint8_t)pass : __ldg(sin + s));
       }
-      nstale = __reduce_add_sync(kFull, nstale);
+      nstale = active ? 0u : __reduce_add_sync(kFull, nstale);  // no stale count with `active`
       cnt = __reduce_add_sync(kFull, cnt);
       if ((threadIdx.x & 31) == 0) {
         flush_count(counter, (unsigned)P + cnt);
@@ -1349,11 +1424,24 @@ vinp_status launch_propagate(const vinp_level* lv, const vinp_nnf* in, vinp_nnf*
     else {
       // R41 active (a previous same-(step, sign) pass exists): the light all-group-path kernel
       const bool light = VINP_PROP_LIGHT && since > 0;
+      // lv->active (whole-range single-GPU passes): flag the targets with a non-stale proposal first
+      uint32_t* active = (light && lv->active && !list && b == 0 && e == lv->n_targets && only_layer < 0 &&
+                          !in->mirror && !out->mirror)
+                             ? lv->active : nullptr;
+      if (active) {
+        if (cudaMemsetAsync(active, 0, sizeof(uint32_t), S(stream)) != cudaSuccess)
+          return check_launch("vinp_propagate(active)");
+        k_prop_mark<<<nblk(e, 256), 256, 0, S(stream)>>>(args_of(lv), in->e, out->e, in->stamp, out->stamp, active,
+                                                         step, sign, since, e);
+        k_prop_compact<<<nblk((int64_t)active_bitmap_words(e), 256), 256, 0, S(stream)>>>(active, e);
+        count_launch();
+        count_launch();
+      }
 #define VINP_PROP_LAUNCH(NC, L)                                                                     \
   k_propagate<NC, L><<<nblk(e - b, pb), pb, 0, S(stream)>>>(args_of(lv), in->e, out->e, in->stamp,      \
                                                             out->stamp, prm->lambda, step, sign, kb,     \
                                                             only_layer, b, e, pass, since, list, counter, \
-                                                            mirror_of(out))
+                                                            mirror_of(out), active)
       if (sign == 0) {
         if (light) VINP_PROP_LAUNCH(6, true); else VINP_PROP_LAUNCH(6, false);
       } else {
@@ -1531,6 +1619,11 @@ vinp_status vinp_brute_force_list(const vinp_level* lv, vinp_nnf* out, const vin
     count_launch();
   }
   return check_launch("vinp_brute_force_list");
+}
+
+size_t vinp_active_ws_bytes(const vinp_level* lv) {
+  if (!lv || lv->n_targets < 0) return 0;
+  return 4 * (8 + active_bitmap_words(lv->n_targets) + (size_t)lv->n_targets);
 }
 
 vinp_status vinp_patch_sums(const vinp_level* lv, int which, int32_t b, int32_t e, void* stream) {

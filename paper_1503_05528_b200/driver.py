@@ -17,6 +17,7 @@ the voxel, the result is bit-identical for any number of ranks.
 """
 from __future__ import annotations
 
+import os
 import time
 from dataclasses import dataclass, field
 from typing import List, Optional, Sequence
@@ -60,6 +61,12 @@ class Config:
     stop_rule: int = 0          # 0: R19 e = ||u_H - v_H||_1 / (3|H|); 1: literal P:988 ||.||_2 / (3|H|)
     skip_stale: bool = True     # R41: exact skip of stale propagation candidates (NNF unchanged)
     lower_bound: bool = True    # R42: exact patch-sum lower-bound rejection in random search (NNF unchanged)
+    # R41 diagnostics: count the stale candidates skipped (Stats.total_stale_skipped; equal to the
+    # oracle's stale count).  False (single GPU): the R41-active passes first flag the targets that
+    # read a changed entry and only those generate candidates (vinp_level.active): same NNF and
+    # patch-update counts, faster, but the skipped candidates are never enumerated (count reported 0).
+    # Default from VINP_COUNT_STALE (the test suite sets it to 1).
+    count_stale: bool = field(default_factory=lambda: os.environ.get("VINP_COUNT_STALE", "0") == "1")
 
     def params(self) -> V.Params:
         return V.Params(lam=self.lam, tex_half=self.tex_half, seed=self.seed, rho=self.rho)
@@ -248,6 +255,14 @@ class Inpainter:
             if lv.n_sources == 0:
                 raise V.VinpError(f"D~ is empty at level {lv.level} (S:237)")
             lv.alloc_lists()
+            if (not self.cfg.count_stale and self.cfg.skip_stale and self.ex.world == 1
+                    and self.device.type == "cuda"):
+                nw = self.V.active_ws_bytes(lv) // 4
+                if lv.active is None or lv.active.numel() != nw:
+                    lv.active = torch.empty(nw, dtype=torch.int32, device=self.device)
+                lv.active.zero_()
+            else:
+                lv.active = None
         self.V.build_lists(self.levels, self.ws)
         old = {id(st.lv): st for st in self.states}
         self.states = []

@@ -31,7 +31,7 @@ class _Level(C.Structure):
                 ("targets", C.c_void_p), ("n_targets", C.c_int32),
                 ("holes", C.c_void_p), ("n_holes", C.c_int32),
                 ("sources", C.c_void_p), ("n_sources", C.c_int32),
-                ("psum", C.c_void_p)]
+                ("psum", C.c_void_p), ("active", C.c_void_p)]
 
 
 MAX_PEERS = 7
@@ -88,6 +88,7 @@ def _load():
         "vinp_brute_force_tc": (I, [P, P, P, I32, I32, P, C.c_size_t, P]),
         "vinp_patch_ssd": (I, [P, P, P, I64, P, I, P, P, P]),
         "vinp_patch_sums": (I, [P, I, I32, I32, P]),
+        "vinp_active_ws_bytes": (C.c_size_t, [P]),
         "vinp_philox": (I, [P, I64, U64, P, P]),
         "vinp_tc_gemm_u8": (I, [P, P, I, P, P]),
         "vinp_patch_ambiguity": (I, [I, C.c_double, U64, U64, U64, P, P]),
@@ -117,7 +118,7 @@ EXPORTED = [
     "vinp_brute_force_ws_bytes", "vinp_brute_force", "vinp_patch_ssd", "vinp_philox",
     "vinp_tc_gemm_u8", "vinp_patch_ambiguity", "vinp_brute_force_list", "vinp_brute_force_tc_ws_bytes", "vinp_brute_force_tc",
     "vinp_affine_ws_bytes", "vinp_affine_estimate", "vinp_affine_chain", "vinp_align_warp", "vinp_unwarp",
-    "vinp_output_rgb", "vinp_level_dims", "vinp_patch_sums"]
+    "vinp_output_rgb", "vinp_level_dims", "vinp_patch_sums", "vinp_active_ws_bytes"]
 
 
 def _check(rc: int, what: str):
@@ -166,6 +167,7 @@ class Level:
     holes: Optional[torch.Tensor] = None
     sources: Optional[torch.Tensor] = None
     psum: Optional[torch.Tensor] = None  # patch sums (R42), int16 [N, 8], or None = no lower bound
+    active: Optional[torch.Tensor] = None  # zeroed workspace of active_ws_bytes(lv) (see vinp_propagate), or None
     n_targets: int = 0
     n_holes: int = 0
     n_sources: int = 0
@@ -191,7 +193,8 @@ class Level:
     def struct(self):
         s = _Level(self.W, self.H, self.T, self.level, _ptr(self.vox), _ptr(self.flags),
                    _ptr(self.layer), _ptr(self.slot), _ptr(self.targets), self.n_targets,
-                   _ptr(self.holes), self.n_holes, _ptr(self.sources), self.n_sources, _ptr(self.psum))
+                   _ptr(self.holes), self.n_holes, _ptr(self.sources), self.n_sources, _ptr(self.psum),
+                   _ptr(self.active))
         self._s = s
         return C.byref(s)
 
@@ -332,6 +335,10 @@ def nnf_evaluate(lv, nnf, prm, kb=-1, only_layer=-1, b=0, e=None, counter=None):
     e = lv.n_targets if e is None else e
     _check(_lib.vinp_nnf_evaluate(lv.struct(), nnf.struct(), C.byref(prm.struct()), kb, only_layer,
                                   b, e, _ptr(counter), _stream()), "vinp_nnf_evaluate")
+
+
+def active_ws_bytes(lv) -> int:
+    return int(_lib.vinp_active_ws_bytes(lv.struct()))
 
 
 def patch_sums(lv, which=0, b=0, e=None):

@@ -3,6 +3,11 @@ import sys
 
 import pytest
 
+# The suite checks the R41 stale counts against the oracle, so Config.count_stale defaults to True
+# here; the product default (flagged targets, no stale count) has its own parity tests
+# (tests/test_gpu_active.py) and is what bench.py and smoke() run.
+os.environ.setdefault("VINP_COUNT_STALE", "1")
+
 ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
 if ROOT not in sys.path:
     sys.path.insert(0, ROOT)
