@@ -9,6 +9,7 @@
 // IDP.4A per colour / texture word); early aborts change no comparison.  Every pass reads NNF
 // buffer `in` and writes `out` (double buffering): no atomics on the NNF, results independent of
 // scheduling.
+#include <cstdlib>
 #include <vector>
 
 #include "common.cuh"
@@ -122,6 +123,9 @@ __global__ void k_upsample(LevelArgs c, const uint64_t* __restrict__ ce, LevelAr
 #endif
 #ifndef VINP_RS_GEN_CHUNK
 #define VINP_RS_GEN_CHUNK 4  // random-search candidate generation: D~ flag loads in flight together per chunk
+#endif
+#ifndef VINP_ACTIVE_MIN
+#define VINP_ACTIVE_MIN (1 << 20)
 #endif
 #ifndef VINP_PROP_LB
 #define VINP_PROP_LB 1  // R42 lower bound in propagation too
@@ -1094,7 +1098,9 @@ __global__ void __launch_bounds__(32 * WPB, VINP_MINB * 8 / WPB) k_random_search
   __syncwarp();
   uint32_t bestD = e_D(inc);
   int bestq = e_q(inc);
+#ifndef VINP_RS_NOEVAL  // (profiling builds time the candidate generation alone)
   group_eval(a, pairs, P, lane, p, px, py, pt, lambda, bestD, bestq);
+#endif
   if (have) {
     put_e(eout, mo, s, pack_e(bestD, bestq));
     if (sout) put_u8(sout, mo.st, mo.n, s, bestq != e_q(inc) ? (uint8_t)pass : __ldg(sin + s));
@@ -1403,6 +1409,16 @@ static vinp_status check_stamps(const vinp_nnf* in, const vinp_nnf* out, int pas
   return VINP_OK;
 }
 
+// smallest level (targets) whose R41-active passes use lv->active; VINP_ACTIVE_MIN in the
+// environment overrides the compiled default (the test suite sets 0 to exercise it on small cases)
+static int active_min() {
+  static const int v = [] {
+    const char* s = getenv("VINP_ACTIVE_MIN");
+    return s ? atoi(s) : (int)VINP_ACTIVE_MIN;
+  }();
+  return v;
+}
+
 vinp_status launch_propagate(const vinp_level* lv, const vinp_nnf* in, vinp_nnf* out,
                              const vinp_params* prm, int step, int sign, int kb, int only_layer,
                              int32_t b, int32_t e, int pass, int since, const int32_t* list,
@@ -1425,8 +1441,10 @@ vinp_status launch_propagate(const vinp_level* lv, const vinp_nnf* in, vinp_nnf*
       // R41 active (a previous same-(step, sign) pass exists): the light all-group-path kernel
       const bool light = VINP_PROP_LIGHT && since > 0;
       // lv->active (whole-range single-GPU passes): flag the targets with a non-stale proposal first
+      // (levels below VINP_ACTIVE_MIN targets keep the whole-range kernel: three launches instead
+      // of one cost more than they save there; c5 level 4, 335 K targets: 16.5 vs 21.1 ms per step)
       uint32_t* active = (light && lv->active && !list && b == 0 && e == lv->n_targets && only_layer < 0 &&
-                          !in->mirror && !out->mirror)
+                          !in->mirror && !out->mirror && e >= active_min())
                              ? lv->active : nullptr;
       if (active) {
         if (cudaMemsetAsync(active, 0, sizeof(uint32_t), S(stream)) != cudaSuccess)

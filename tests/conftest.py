@@ -7,6 +7,9 @@ import pytest
 # here; the product default (flagged targets, no stale count) has its own parity tests
 # (tests/test_gpu_active.py) and is what bench.py and smoke() run.
 os.environ.setdefault("VINP_COUNT_STALE", "1")
+# ... and that default is used from 2^20 targets per level on (libvinp, VINP_ACTIVE_MIN): 0 here, so
+# that the small test volumes run it too (read once, when the library first launches a pass)
+os.environ.setdefault("VINP_ACTIVE_MIN", "0")
 
 ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
 if ROOT not in sys.path:
