@@ -179,9 +179,10 @@ vinp_status vinp_nnf_evaluate(const vinp_level* lv, vinp_nnf* nnf, const vinp_pa
  * grown since, so it cannot win (strict improvement) and is not evaluated: the NNF is identical
  * to the unskipped pass.  Such candidates are counted in counter[1] (counter then points to two
  * u64), not in counter[0].  out->stamp[s] = pass if e[s] changed, else in->stamp[s].
- * With lv->active set (whole-range passes with since > 0, only_layer < 0 and no mirror), a first
- * kernel copies every entry and stamp to `out` and lists the targets that read an entry changed
- * since `since`; the pass then runs over that list alone: the other targets receive stale proposals
+ * With lv->active set (passes with since > 0, only_layer < 0 and no mirror), a first kernel copies
+ * the entries and stamps of [b, e) to `out` and lists the targets of [b, e) that read an entry
+ * changed since `since` (in->stamp must be current for every target those targets read: the whole
+ * level, or a slab plus its halo rows); the pass then runs over that list alone: the other targets receive stale proposals
  * only and keep their entry.  The NNF, the stamps and counter[0] are identical; counter[1] is then
  * NOT updated (the stale candidates of unlisted targets are never enumerated). */
 vinp_status vinp_propagate(const vinp_level* lv, const vinp_nnf* in, vinp_nnf* out,

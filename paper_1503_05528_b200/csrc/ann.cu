@@ -264,10 +264,26 @@ __device__ __forceinline__ void group_eval(const LevelArgs& a, const int2* pairs
     accc = __dp4a(dc, dc, accc);                                              \
     acct = __dp4a(dx_, dx_, acct);                                            \
   }
-template <bool ABORT>
+// R42 helpers: channel sums of a voxel word, packed patch sums, full-patch test
+__device__ __forceinline__ void vox_add(uint64_t w, uint32_t (&s)[5]) {
+  const uint32_t lo = (uint32_t)w, hi = (uint32_t)(w >> 32);
+  s[0] = __dp4a(lo, 0x00000001u, s[0]);
+  s[1] = __dp4a(lo, 0x00000100u, s[1]);
+  s[2] = __dp4a(lo, 0x00010000u, s[2]);
+  s[3] = __dp4a(hi, 0x00000001u, s[3]);
+  s[4] = __dp4a(hi, 0x00000100u, s[4]);
+}
+__device__ __forceinline__ uint4 psum_pack(const uint32_t (&s)[5]) {
+  return make_uint4(s[0] | (s[1] << 16), s[2] | (s[3] << 16), s[4], 0u);
+}
+__device__ __forceinline__ bool interior(const Geo& g, int x, int y, int t) {
+  return x >= 2 && x < g.W - 2 && y >= 2 && y < g.H - 2 && t >= 2 && t < g.T - 2;
+}
+
+template <bool ABORT, bool SUMS = false>
 __device__ __forceinline__ uint32_t thread_ssd(const LevelArgs& a, int p, int px, int py, int pt,
                                                int q, int lambda, int kb, bool full, uint32_t thr,
-                                               bool& alive) {
+                                               bool& alive, uint32_t* psums = nullptr) {
   const unsigned long long* v = reinterpret_cast<const unsigned long long*>(a.vox);
   uint32_t accc = 0, acct = 0;
 #pragma unroll 1
@@ -289,6 +305,10 @@ __device__ __forceinline__ uint32_t thread_ssd(const LevelArgs& a, int p, int px
         uint32_t dx_ = __vabsdiffu4((uint32_t)(tv[k] >> 32), (uint32_t)(sv[k] >> 32));
         accc = __dp4a(dc, dc, accc);
         acct = __dp4a(dx_, dx_, acct);
+        if (SUMS) {  // R42: the target patch's channel sums on the way (evaluate)
+          uint32_t(&S)[5] = *reinterpret_cast<uint32_t(*)[5]>(psums);
+          vox_add(tv[k], S);
+        }
       }
     } else {  // border target: one branch-guarded voxel at a time (rare)
 #pragma unroll
@@ -334,7 +354,11 @@ __global__ void __launch_bounds__(256) k_evaluate(LevelArgs a, uint64_t* __restr
     int q = e_q(ee[s]);
     bool full = kb < 0 && px >= 2 && px < a.g.W - 2 && py >= 2 && py < a.g.H - 2 && pt >= 2 && pt < a.g.T - 2;
     bool alive = true;
-    uint32_t D = thread_ssd<false>(a, p, px, py, pt, q, lambda, kb, full, 0, alive);
+    uint32_t S[5] = {0, 0, 0, 0, 0};
+    uint32_t D = a.psum ? thread_ssd<false, true>(a, p, px, py, pt, q, lambda, kb, full, 0, alive, S)
+                        : thread_ssd<false>(a, p, px, py, pt, q, lambda, kb, full, 0, alive);
+    // R42: a full target patch leaves its channel sums on the u this search runs on
+    if (a.psum && full) const_cast<uint4*>(a.psum)[p] = psum_pack(S);
     int n = 0;
     if (full) {
       n = 125;
@@ -358,21 +382,6 @@ __global__ void __launch_bounds__(256) k_evaluate(LevelArgs a, uint64_t* __restr
 // psum[p] = the five channel sums of vox over N_p (u16 each: <= 125 * 255), for voxels whose whole
 // patch lies in Omega.  With them 125 D(p, q) >= 4 |dS_rgb|^2 + lambda |dS_T|^2 (Cauchy-Schwarz
 // over the 125 voxels), the exact lower bound random search tests before reading any patch row.
-__device__ __forceinline__ void vox_add(uint64_t w, uint32_t (&s)[5]) {
-  const uint32_t lo = (uint32_t)w, hi = (uint32_t)(w >> 32);
-  s[0] = __dp4a(lo, 0x00000001u, s[0]);
-  s[1] = __dp4a(lo, 0x00000100u, s[1]);
-  s[2] = __dp4a(lo, 0x00010000u, s[2]);
-  s[3] = __dp4a(hi, 0x00000001u, s[3]);
-  s[4] = __dp4a(hi, 0x00000100u, s[4]);
-}
-__device__ __forceinline__ uint4 psum_pack(const uint32_t (&s)[5]) {
-  return make_uint4(s[0] | (s[1] << 16), s[2] | (s[3] << 16), s[4], 0u);
-}
-__device__ __forceinline__ bool interior(const Geo& g, int x, int y, int t) {
-  return x >= 2 && x < g.W - 2 && y >= 2 && y < g.H - 2 && t >= 2 && t < g.T - 2;
-}
-
 // every voxel: one thread per (x, y) column marching along t with a ring of the last five
 // per-frame 5x5 sums (25 gathers per voxel instead of 125)
 __global__ void __launch_bounds__(128) k_patch_sums_dense(LevelArgs a, uint4* __restrict__ psum) {
@@ -442,7 +451,7 @@ __device__ __forceinline__ bool lb_reject(const uint4 sp, const uint4 sq, int la
 }
 
 // ------------------------------------------------------------------ R41: targets with a live proposal
-// Before an R41-active pass over the whole level (single GPU, lv->active): every target copies its
+// Before an R41-active pass over the slots [b, e) of a level (lv->active): every target of [b, e) copies its
 // entry and stamp to the output buffer, and every target whose entry changed since the previous
 // pass with the same (step, sign) (stamp >= since) appends the targets that read it in this pass,
 // p - sign*step*e_axis (both signs for sign = 0), in a bitmap; k_prop_compact turns it into a list.
@@ -453,12 +462,17 @@ __host__ __device__ inline size_t active_bitmap_words(int32_t n) { return ((size
 __global__ void __launch_bounds__(256) k_prop_mark(LevelArgs a, const uint64_t* __restrict__ ein,
                                                    uint64_t* __restrict__ eout, const uint8_t* __restrict__ sin,
                                                    uint8_t* __restrict__ sout, uint32_t* __restrict__ ws, int step,
-                                                   int sign, int since, int32_t n) {
+                                                   int sign, int since, int32_t b, int32_t e, int32_t n) {
+  // every target's stamp is looked at (a changed entry outside the slab [b, e) is read by targets
+  // inside it; the caller has exchanged those rows), entries are copied and readers flagged in
+  // [b, e) only
   const int s = blockIdx.x * blockDim.x + threadIdx.x;
   if (s >= n) return;
   const uint8_t st = __ldg(sin + s);
-  eout[s] = __ldg(reinterpret_cast<const unsigned long long*>(ein) + s);
-  sout[s] = st;
+  if (s >= b && s < e) {
+    eout[s] = __ldg(reinterpret_cast<const unsigned long long*>(ein) + s);
+    sout[s] = st;
+  }
   if ((int)st < since) return;
   uint32_t* bitmap = ws + 8;
   const int p = __ldg(a.targets + s);
@@ -472,7 +486,7 @@ __global__ void __launch_bounds__(256) k_prop_mark(LevelArgs a, const uint64_t* 
     const int x = px + (ax == 0 ? sg * step : 0), y = py + (ax == 1 ? sg * step : 0), t = pt + (ax == 2 ? sg * step : 0);
     if (!inside(a.g, x, y, t)) continue;
     const int r = __ldg(a.slot + lin(a.g, x, y, t));
-    if (r < 0) continue;
+    if (r < b || r >= e) continue;  // (-1: not a target)
     atomicOr(bitmap + (r >> 5), 1u << (r & 31));
   }
 }
@@ -528,6 +542,7 @@ __global__ void __launch_bounds__(LIGHT ? 128 : 256, LIGHT ? VINP_PROP_LIGHT_MIN
   if (active) {
     // the pass runs over the list k_prop_mark built (the entries of the other targets are already
     // copied): [b, e) becomes [0, list length)
+    b = 0;
     e = (int32_t)active[0];
     list = reinterpret_cast<const int32_t*>(active + 8 + active_bitmap_words(a.n_targets));
     if ((int)(blockIdx.x * blockDim.x) >= e) return;
@@ -1390,12 +1405,6 @@ vinp_status launch_evaluate(const vinp_level* lv, vinp_nnf* nnf, const vinp_para
           args_of(lv), nnf->e, nnf->n, nnf->stamp, prm->lambda, kb, only_layer, b, e, list, counter,
           mirror_of(nnf));
     count_launch();
-    if (kb < 0 && lv->psum) {  // R42: the targets' patch sums on the u this search runs on
-      const int32_t sb = list ? 0 : b, se = list ? lv->n_targets : e;  // list launches: every target
-      k_patch_sums_targets<<<nblk(se - sb, 128), 128, 0, S(stream)>>>(args_of(lv), reinterpret_cast<uint4*>(lv->psum),
-                                                                      sb, se);
-      count_launch();
-    }
   }
   return check_launch("vinp_nnf_evaluate");
 }
@@ -1443,15 +1452,16 @@ vinp_status launch_propagate(const vinp_level* lv, const vinp_nnf* in, vinp_nnf*
       // lv->active (whole-range single-GPU passes): flag the targets with a non-stale proposal first
       // (levels below VINP_ACTIVE_MIN targets keep the whole-range kernel: three launches instead
       // of one cost more than they save there; c5 level 4, 335 K targets: 16.5 vs 21.1 ms per step)
-      uint32_t* active = (light && lv->active && !list && b == 0 && e == lv->n_targets && only_layer < 0 &&
-                          !in->mirror && !out->mirror && e >= active_min())
+      uint32_t* active = (light && lv->active && !list && only_layer < 0 && !in->mirror && !out->mirror &&
+                          e - b >= active_min())
                              ? lv->active : nullptr;
       if (active) {
         if (cudaMemsetAsync(active, 0, sizeof(uint32_t), S(stream)) != cudaSuccess)
           return check_launch("vinp_propagate(active)");
-        k_prop_mark<<<nblk(e, 256), 256, 0, S(stream)>>>(args_of(lv), in->e, out->e, in->stamp, out->stamp, active,
-                                                         step, sign, since, e);
-        k_prop_compact<<<nblk((int64_t)active_bitmap_words(e), 256), 256, 0, S(stream)>>>(active, e);
+        const int32_t n = lv->n_targets;
+        k_prop_mark<<<nblk(n, 256), 256, 0, S(stream)>>>(args_of(lv), in->e, out->e, in->stamp, out->stamp, active,
+                                                         step, sign, since, b, e, n);
+        k_prop_compact<<<nblk((int64_t)active_bitmap_words(n), 256), 256, 0, S(stream)>>>(active, n);
         count_launch();
         count_launch();
       }

@@ -62,7 +62,7 @@ class Config:
     skip_stale: bool = True     # R41: exact skip of stale propagation candidates (NNF unchanged)
     lower_bound: bool = True    # R42: exact patch-sum lower-bound rejection in random search (NNF unchanged)
     # R41 diagnostics: count the stale candidates skipped (Stats.total_stale_skipped; equal to the
-    # oracle's stale count).  False (single GPU): the R41-active passes first flag the targets that
+    # oracle's stale count).  False (not with the fused exchange): the R41-active passes first flag the targets that
     # read a changed entry and only those generate candidates (vinp_level.active): same NNF and
     # patch-update counts, faster, but the skipped candidates are never enumerated (count reported 0).
     # Default from VINP_COUNT_STALE (the test suite sets it to 1).
@@ -255,8 +255,8 @@ class Inpainter:
             if lv.n_sources == 0:
                 raise V.VinpError(f"D~ is empty at level {lv.level} (S:237)")
             lv.alloc_lists()
-            if (not self.cfg.count_stale and self.cfg.skip_stale and self.ex.world == 1
-                    and self.device.type == "cuda"):
+            if (not self.cfg.count_stale and self.cfg.skip_stale and self.device.type == "cuda"
+                    and (self.ex.world == 1 or self.cfg.exchange != "fused")):
                 nw = self.V.active_ws_bytes(lv) // 4
                 if lv.active is None or lv.active.numel() != nw:
                     lv.active = torch.empty(nw, dtype=torch.int32, device=self.device)

@@ -29,9 +29,12 @@ def _loaded(case, **kw):
     return ip
 
 
-@pytest.mark.parametrize("case,sign_policy", [("c2", 0), ("c2", 1), ("odd", 0), ("odd", 1)])
-def test_flagged_passes_equal_exhaustive_passes(V, case, sign_policy):
-    """One ANN search pass by pass on two copies of the state, with and without `active`."""
+@pytest.mark.parametrize("case,sign_policy,slabs", [("c2", 0, 1), ("c2", 1, 1), ("odd", 0, 1), ("odd", 1, 1),
+                                                    ("c2", 0, 3), ("odd", 1, 2)])
+def test_flagged_passes_equal_exhaustive_passes(V, case, sign_policy, slabs):
+    """One ANN search pass by pass on two copies of the state, with and without `active`; with
+    slabs > 1 the flagged pass runs slab by slab (the multi-GPU call pattern: stamps of the whole
+    level current, entries copied and targets listed per slab)."""
     ip = _loaded(case, count_stale=False)
     for st in ip.states:
         lv = st.lv
@@ -55,8 +58,10 @@ def test_flagged_passes_equal_exhaustive_passes(V, case, sign_policy):
                     for mode in ("flag", "all"):
                         a, b, cnt, clk = bufs[mode]
                         lv.active = act if mode == "flag" else None
-                        V.propagate(lv, a, b, ip.prm, s, sign, counter=cnt, pass_id=clk.pass_id,
-                                    since=clk.since(s, sign))
+                        nsl = slabs if mode == "flag" else 1
+                        for i in range(nsl):
+                            V.propagate(lv, a, b, ip.prm, s, sign, counter=cnt, pass_id=clk.pass_id,
+                                        since=clk.since(s, sign), b=i * n // nsl, e=(i + 1) * n // nsl)
                         flagged_passes += mode == "flag" and clk.since(s, sign) > 0
                         clk.tick(s, sign)
                         bufs[mode][0], bufs[mode][1] = b, a
