@@ -233,6 +233,7 @@ __device__ __forceinline__ void recon_hole(const ReconArgs& a, const LaneVox& LV
                       : (uint64_t)__double_as_longlong((double)Dq[i] / (double)nq[i]);
   }
   int64_t w[4];
+  bool unitw = true;  // warp-uniform: every weight is 0 or 1 (best patch, unweighted, sigma_p = 0)
   if (mode == VINP_BEST_PATCH) {
     uint64_t kmin;
     if (n125) {
@@ -312,6 +313,7 @@ __device__ __forceinline__ void recon_hole(const ReconArgs& a, const LaneVox& LV
 #pragma unroll
       for (int i = 0; i < 4; ++i) w[i] = ((valid >> i) & 1u) && Dq[i] == 0;
     } else if (n125) {
+      unitw = false;
       // a = D_q / (2 D_s) with all n = 125: the correctly rounded quotient from the correctly rounded
       // reciprocal y = RN(1/b) (once per hole), q = RN(a y), r = a - q b (exact, FMA), RN(q + r y)
       // (Markstein's theorem; b = 2 D_s < 2^32 has no all-ones significand) — equal to __ddiv_rn
@@ -327,6 +329,7 @@ __device__ __forceinline__ void recon_hole(const ReconArgs& a, const LaneVox& LV
         w[i] = ((valid >> i) & 1u) ? wi : 0;
       }
     } else {
+      unitw = false;
       // partial patches (volume border): a = D_q n_s / (2 n_q D_s), one correctly rounded division
       // of exact operands (R32)
 #pragma unroll
@@ -337,29 +340,51 @@ __device__ __forceinline__ void recon_hole(const ReconArgs& a, const LaneVox& LV
       }
     }
   }
-  // exact sums: w <= 2^36 is split as w = wh 2^32 + wl (wh <= 16); per channel the low part
-  // accumulates in 64 bits (one wide multiply-add per contributor) and the high part in 32 bits;
-  // the per-lane partials (< 2^46) are then summed over the warp as two 23-bit halves by REDUX
-  uint64_t Sl = 0, Nl[5] = {0, 0, 0, 0, 0};
-  uint32_t Sh = 0, Nh[5] = {0, 0, 0, 0, 0};
-#pragma unroll
-  for (int i = 0; i < 4; ++i) {
-    const uint32_t wl = (uint32_t)w[i], wh = (uint32_t)((uint64_t)w[i] >> 32);
-    const uint64_t x = val[i];
-    const uint32_t c0 = (uint32_t)x, c1 = (uint32_t)(x >> 32);
-    const uint32_t v[5] = {c0 & 255, (c0 >> 8) & 255, (c0 >> 16) & 255, c1 & 255, (c1 >> 8) & 255};
-    Sl += wl;
-    Sh += wh;
-#pragma unroll
-    for (int c = 0; c < 5; ++c) {
-      Nl[c] += (uint64_t)wl * v[c];
-      Nh[c] += wh * v[c];
-    }
-  }
-  int64_t S = warp_sum46((int64_t)(Sl + ((uint64_t)Sh << 32)));
+  int64_t S;
   int64_t N[5];
+  if (unitw) {
+    // weights 0 / 1: the six sums are at most 125 * 255 < 2^16, two per 32-bit REDUX
+    uint32_t p0 = 0, p1 = 0, p2 = 0;
 #pragma unroll
-  for (int c = 0; c < 5; ++c) N[c] = warp_sum46((int64_t)(Nl[c] + ((uint64_t)Nh[c] << 32)));
+    for (int i = 0; i < 4; ++i) {
+      const uint32_t c0 = w[i] ? (uint32_t)val[i] : 0u, c1 = w[i] ? (uint32_t)(val[i] >> 32) : 0u;
+      p0 += (c0 & 0xffu) | ((c0 & 0xff00u) << 8);
+      p1 += ((c0 >> 16) & 0xffu) | ((c1 & 0xffu) << 16);
+      p2 += ((c1 >> 8) & 0xffu) | (w[i] ? 0x10000u : 0u);
+    }
+    p0 = __reduce_add_sync(kFull, p0);
+    p1 = __reduce_add_sync(kFull, p1);
+    p2 = __reduce_add_sync(kFull, p2);
+    N[0] = p0 & 0xffffu;
+    N[1] = p0 >> 16;
+    N[2] = p1 & 0xffffu;
+    N[3] = p1 >> 16;
+    N[4] = p2 & 0xffffu;
+    S = p2 >> 16;
+  } else {
+    // exact sums: w <= 2^36 is split as w = wh 2^32 + wl (wh <= 16); per channel the low part
+    // accumulates in 64 bits (one wide multiply-add per contributor) and the high part in 32 bits;
+    // the per-lane partials (< 2^46) are then summed over the warp as two 23-bit halves by REDUX
+    uint64_t Sl = 0, Nl[5] = {0, 0, 0, 0, 0};
+    uint32_t Sh = 0, Nh[5] = {0, 0, 0, 0, 0};
+  #pragma unroll
+    for (int i = 0; i < 4; ++i) {
+      const uint32_t wl = (uint32_t)w[i], wh = (uint32_t)((uint64_t)w[i] >> 32);
+      const uint64_t x = val[i];
+      const uint32_t c0 = (uint32_t)x, c1 = (uint32_t)(x >> 32);
+      const uint32_t v[5] = {c0 & 255, (c0 >> 8) & 255, (c0 >> 16) & 255, c1 & 255, (c1 >> 8) & 255};
+      Sl += wl;
+      Sh += wh;
+  #pragma unroll
+      for (int c = 0; c < 5; ++c) {
+        Nl[c] += (uint64_t)wl * v[c];
+        Nh[c] += wh * v[c];
+      }
+    }
+    S = warp_sum46((int64_t)(Sl + ((uint64_t)Sh << 32)));
+  #pragma unroll
+    for (int c = 0; c < 5; ++c) N[c] = warp_sum46((int64_t)(Nl[c] + ((uint64_t)Nh[c] << 32)));
+  }
   if (lane < 5) {
     int64_t Nc = lane == 0 ? N[0] : lane == 1 ? N[1] : lane == 2 ? N[2] : lane == 3 ? N[3] : N[4];
     float o = (float)__ddiv_rn((double)Nc, (double)S);
