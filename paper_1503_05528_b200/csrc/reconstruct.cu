@@ -94,9 +94,13 @@ __device__ __forceinline__ int64_t weight36(double a, const double2* __restrict_
 // few rounds instead of one per bit.
 __device__ __forceinline__ uint32_t select_rank32(const uint32_t (&k)[4], unsigned valid, uint32_t r, uint32_t m) {
   const uint32_t kmin = __reduce_min_sync(kFull, min(min(k[0], k[1]), min(k[2], k[3])));
+  if (r == 1) return kmin;
+  if (kmin == 0) {  // sigma_p = 0 is common (exact copies): r or more zero keys settle it at once
+    uint32_t c = (k[0] == 0) + (k[1] == 0) + (k[2] == 0) + (k[3] == 0);
+    if (__reduce_add_sync(kFull, c) >= r) return 0;
+  }
   const uint32_t kmax = __reduce_max_sync(kFull, max(max((valid & 1) ? k[0] : 0u, (valid & 2) ? k[1] : 0u),
                                                      max((valid & 4) ? k[2] : 0u, (valid & 8) ? k[3] : 0u)));
-  if (r == 1) return kmin;
   if (r == m) return kmax;
   const uint32_t x = kmax ^ kmin;
   if (x == 0) return kmin;  // all keys equal
