@@ -286,3 +286,19 @@ def test_emulated_ranks_fused_exchange(case, world):
         assert [d["patch_updates"] for d in lev] == [d["patch_updates"] for d in ref[1]], rank
         assert [d["stale_skipped"] for d in lev] == [d["stale_skipped"] for d in ref[1]], rank
         assert pu == ref[2] and nb > 0
+
+
+@pytest.mark.parametrize("exchange,world", [("halo", 2), ("halo", 4), ("allgather", 3)])
+def test_emulated_ranks_listed_target_passes(exchange, world):
+    """The product default (Config.count_stale = False: R41-active passes over the listed targets
+    only, per slab) under emulated ranks, against one rank in the counting mode: same output video,
+    outer iterations and patch-update counts (the stale count is not reported in this mode)."""
+    from paper_1503_05528_b200 import Config
+    v, m = CASES["c2"]()
+    ref = _run_world(v, m, Config(levels=2, count_stale=True), 1)[0]
+    got = _run_world(v, m, Config(levels=2, exchange=exchange, replicate_below=0, count_stale=False), world)
+    for rank, (out, lev, pu, ng, nh, nb) in enumerate(got):
+        assert torch.equal(out, ref[0]), (rank, "output video")
+        assert [d["outer"] for d in lev] == [d["outer"] for d in ref[1]], rank
+        assert [d["patch_updates"] for d in lev] == [d["patch_updates"] for d in ref[1]], rank
+        assert pu == ref[2]
