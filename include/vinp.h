@@ -215,7 +215,10 @@ size_t vinp_active_ws_bytes(const vinp_level* lv);
  * v0 = in(p); for i = 1, 2, ...: R_i = rmax * rho^i (repeated fp64 multiplication) while
  * R_i >= 1; delta_c = (U_c - 2^31) 2^-31 from Philox(p, pm_iter, (level<<24)|(2<<16)|i,
  * outer_code); q_i = p + v0 + floor(R_i delta).  Same validity / duplicate / strict rules.
- * With stamps (as vinp_propagate), out->stamp[s] = pass if e[s] changed, else in->stamp[s]. */
+ * With stamps (as vinp_propagate), out->stamp[s] = pass if e[s] changed, else in->stamp[s].
+ * counter (device, may be NULL) += the valid, distinct candidates tested against the incumbent,
+ * whether by their full distance, by a partial sum that already exceeds the best (R35) or, with
+ * lv->psum, by the patch-sum lower bound (R42, see vinp_patch_sums): the same number in all cases. */
 vinp_status vinp_random_search(const vinp_level* lv, const vinp_nnf* in, vinp_nnf* out,
                                const vinp_params* prm, uint32_t outer_code, int pm_iter, int kb,
                                int only_layer, int32_t b, int32_t e, int pass,

@@ -6,7 +6,10 @@
 // x-adjacent target, so the coherent candidate gathers coalesce), random search runs 5-lane column
 // groups over a per-warp pair queue (incoherent candidates), onion-layer propagation runs warp per
 // target (short latency chain for small launches).  Distances are exact integers (VABSDIFF4 +
-// IDP.4A per colour / texture word); early aborts change no comparison.  Every pass reads NNF
+// IDP.4A per colour / texture word); early aborts change no comparison, and neither do the three
+// exact savings: stale propagation candidates (R41), R41-active passes over the targets that read
+// a changed entry only (R41b: k_prop_mark, k_prop_compact), and the patch-sum lower bound that
+// rejects candidates before any patch row is read (R42: k_patch_sums_*).  Every pass reads NNF
 // buffer `in` and writes `out` (double buffering): no atomics on the NNF, results independent of
 // scheduling.
 #include <cstdlib>
