@@ -106,3 +106,27 @@ def test_default_mode_equals_counting_mode_on_c3():
         res.append((out.cpu(), [l["patch_updates"] for l in stats.levels], [l["outer"] for l in stats.levels]))
     assert torch.equal(res[0][0], res[1][0])
     assert res[0][1:] == res[1][1:]
+
+
+@pytest.mark.parametrize("name", ["c4", "c5"])
+def test_full_size_modes_agree(name):
+    """BASELINE's full-size configs, whole Alg. 4: the product default (listed targets, R42 lower
+    bound) against the exhaustive counting mode without the lower bound — the mode the full-size
+    oracle parity test (tests/test_gpu_fullsize_e2e.py) runs c4 in.  Output video, outer iterations
+    and patch-update counts per level must be equal."""
+    from gen.synth import CONFIGS
+    from paper_1503_05528_b200 import Config, Inpainter
+    c = CONFIGS[name]
+    v, m, _ = generate(name, device="cuda")
+    res = []
+    for fast in (True, False):
+        cfg = Config(levels=c.levels, pm_iters=c.pm_iters, fixed_outer=c.fixed_outer, max_outer=c.max_outer,
+                     lam=c.lam, seed=c.seed, count_stale=not fast, lower_bound=fast)
+        ip = Inpainter(c.W, c.H, c.T, cfg, "cuda")
+        ip.load(v, m)
+        st = ip.run()
+        res.append((ip.output(v).clone(), [l["patch_updates"] for l in st.levels], [l["outer"] for l in st.levels]))
+        del ip
+        torch.cuda.empty_cache()
+    assert torch.equal(res[0][0], res[1][0])
+    assert res[0][1:] == res[1][1:]
