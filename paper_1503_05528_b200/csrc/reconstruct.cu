@@ -49,8 +49,11 @@ __device__ __forceinline__ uint8_t round_u8(float x) {
 #ifndef VINP_REC_PREFETCH
 #define VINP_REC_PREFETCH 0  // 1: stage A (slot gathers) of the next hole issued before this hole's arithmetic (A/B: 17.5 vs 17.5-17.9 ms, 44 B of spills at 64 registers; 85 registers: 18.9 ms)
 #endif
+#ifndef VINP_REC_CHUNKED
+#define VINP_REC_CHUNKED 1  // A/B at c5 level 1: strided persistent warps 15.2 ms (2 waves) / 14.2 (64); contiguous chunks 16.9 (2 waves: imbalance) / 13.3 (32) / 13.2 (64) / 13.3 (256) / 14.7 (1024)
+#endif
 #ifndef VINP_REC_WAVES
-#define VINP_REC_WAVES 2
+#define VINP_REC_WAVES 64
 #endif
 #ifndef VINP_REC_MINB
 #define VINP_REC_MINB 4
@@ -428,8 +431,18 @@ __global__ void __launch_bounds__(32 * kWPB, VINP_REC_MINB * 8 / kWPB) k_reconst
     LV.dt[i] = (int8_t)dt;
     LV.real[i] = v < kPatch;
   }
+#if VINP_REC_CHUNKED
+  // each block owns a contiguous chunk of holes, its warps 8 adjacent holes at a time: co-resident
+  // blocks (consecutive ids) then work on neighbouring holes, whose contributors share cache lines
+  const int chunk = ((he - hb) + gridDim.x - 1) / gridDim.x;
+  const int cb = hb + blockIdx.x * chunk;
+  he = min(he, cb + chunk);
+  const int nw = kWPB;
+  int idx = cb + (threadIdx.x >> 5);
+#else
   const int nw = gridDim.x * kWPB;
   int idx = hb + blockIdx.x * kWPB + (threadIdx.x >> 5);
+#endif
   if (idx >= he) return;
 #if VINP_REC_PREFETCH
   HoleA cur = recon_stage_a(a, LV, layer_j, list ? __ldg(list + idx) : idx);
